@@ -1,0 +1,83 @@
+"""Seeded synthetic problem generators for the BASELINE.json configurations.
+
+The reference benchmarks on Gaussian-mixture images (paper §4.3.1, "Gaussian
+mixtures supported on X = [0,1]^2 with random variances, means, and
+magnitudes"); no image files travel, so every config is regenerated from a
+seed.  The generator is host-side setup, shared verbatim by the CUDA path,
+the CPU oracle and the golden-fixture script, so both arms of every
+comparison see bit-identical inputs.
+
+Density recipe (documented in DESIGN.md §Data):
+    dens = sum_k w_k exp(-|x - c_k|^2 / (2 sigma_k^2))      (isotropic)
+    dens = dens / dens.sum() + floor                         (floor per pixel)
+    mass = total * dens / dens.sum()
+with c_k ~ U[0.2, 0.8]^d, sigma_k ~ U[0.05, 0.15], w_k ~ U[0.5, 1].
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["MixtureSpec", "gaussian_mixture", "BASELINE_CONFIGS", "config_problem_arrays"]
+
+
+@dataclass(frozen=True)
+class MixtureSpec:
+    n_bumps: int
+    floor: float
+    total: float
+    centre_lo: float = 0.2
+    centre_hi: float = 0.8
+    sigma_lo: float = 0.05
+    sigma_hi: float = 0.15
+    w_lo: float = 0.5
+    w_hi: float = 1.0
+
+
+def gaussian_mixture(dims: tuple, dx: float, origin: tuple, spec: MixtureSpec,
+                     rng: np.random.Generator) -> np.ndarray:
+    """Floored, normalised isotropic Gaussian mixture on a regular grid."""
+    d = len(dims)
+    axes = [origin[a] + dx * np.arange(dims[a], dtype=np.float64) for a in range(d)]
+    dens = np.zeros(dims, dtype=np.float64)
+    for _ in range(spec.n_bumps):
+        c = rng.uniform(spec.centre_lo, spec.centre_hi, size=d)
+        sig = rng.uniform(spec.sigma_lo, spec.sigma_hi)
+        w = rng.uniform(spec.w_lo, spec.w_hi)
+        q = np.zeros(dims, dtype=np.float64)
+        for a in range(d):
+            shape = [1] * d
+            shape[a] = dims[a]
+            q = q + ((axes[a] - c[a]) ** 2).reshape(shape)
+        dens += w * np.exp(-q / (2.0 * sig * sig))
+    dens = dens / dens.sum() + spec.floor
+    return dens * (spec.total / dens.sum())
+
+
+# BASELINE.json "configs", index-aligned.  Only the fields the solver needs.
+BASELINE_CONFIGS = [
+    dict(name="pr1_64", n=64, mu=MixtureSpec(3, 1e-4, 1.0), nu=MixtureSpec(3, 1e-4, 1.3),
+         lam=1.0, eps_final_h2=2.0, eps_start_h2=2.0, coarsest=64, cell=4, domdec_sweeps=30,
+         inner_tol=1e-7),
+    dict(name="ms_256", n=256, mu=MixtureSpec(5, 1e-4, 1.0), nu=MixtureSpec(5, 1e-4, 0.8),
+         lam=0.5, eps_final_h2=2.0, eps_start_h2=64.0, coarsest=32, cell=4),
+    dict(name="ms_1024", n=1024, mu=MixtureSpec(8, 1e-5, 1.0), nu=MixtureSpec(8, 1e-5, 1.5),
+         lam=1.0, eps_final_h2=2.0, eps_start_h2=256.0, coarsest=64, cell=8),
+    dict(name="ms_2048", n=2048, mu=MixtureSpec(16, 1e-5, 1.0), nu=MixtureSpec(16, 1e-5, 0.7),
+         lam=2.0, eps_final_h2=2.0, eps_start_h2=None, coarsest=128, cell=8),
+]
+
+
+def config_problem_arrays(index: int, seed: int = 0, n: int | None = None):
+    """(mu, nu, dx, origin, cfg) for a BASELINE config; ``n`` overrides the size."""
+    cfg = dict(BASELINE_CONFIGS[index])
+    n = int(n or cfg["n"])
+    dx = 1.0 / n
+    origin = (0.5 * dx, 0.5 * dx)
+    rng = np.random.default_rng(seed)
+    mu = gaussian_mixture((n, n), dx, origin, cfg["mu"], rng)
+    nu = gaussian_mixture((n, n), dx, origin, cfg["nu"], rng)
+    cfg["n"] = n
+    return mu, nu, dx, origin, cfg
