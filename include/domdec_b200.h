@@ -1,0 +1,218 @@
+/*
+ * domdec_b200.h — C ABI of the B200 domain-decomposition library.
+ *
+ * Every entry point takes plain device pointers (allocated by the host, e.g.
+ * through torch), sizes and a cudaStream_t (passed as void*), enqueues its
+ * kernels on that stream and returns 0 or a negative error code (the CUDA
+ * error string is available from dd_last_error()).  No torch types cross
+ * this boundary; the Python host layer (paper_2410_08859_b200/engine.py)
+ * binds it with ctypes, exactly as a ctypes/cffi binding of the reference
+ * package would.
+ *
+ * Problems are embedded as 2D grids: a 1D grid of n nodes is the 2D grid
+ * (1, n).  A box is four int32 (off0, ext0, off1, ext1); an empty box has
+ * ext0 == 0 or ext1 == 0.
+ *
+ * Reference interfaces replaced (paths under the reference package
+ * pkg/src/domdec/):
+ *   dd_grid_lse          sinkhorn.py:133-175   SeparableKernel.lse_x / lse_y
+ *   dd_newton_global     sinkhorn.py:256-260   y_halfstep_newton, m = None branch
+ *   dd_global_terms      sinkhorn.py:336-358   gap_kl_terms / _gap_kl
+ *                        engine.py:654-662     StitchedGapEvaluator._dual_at sums
+ *   dd_cell_solve        cells.py:165-393      make_cell_problems + solve_cell_batch
+ *                                              (+ balance_cell_masses :446, _finalize :396)
+ *   dd_cell_delta        engine.py:388-433     BlendScorer.__init__ (per-cell deltas)
+ *   dd_blend_energy      engine.py:441-456     BlendScorer.energy_at
+ *   dd_cell_commit       engine.py:726-785     _commit_cell + _stitch_alpha
+ *   dd_assemble          measures.py:410-425   assemble_y_marginal
+ *   dd_energy_terms      engine.py:185-196     PlanState.energy
+ *   dd_product_init      engine.py:234-257     initial_plan_state (+ cells.py:566 product_plan_fragments)
+ *   dd_cut_plan          engine.py:294-322     warm_start_plan (plan cut along basic cells)
+ */
+#ifndef DOMDEC_B200_H
+#define DOMDEC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Geometry and parameters of one transport problem (2D embedding). */
+typedef struct dd_geom {
+    int32_t nx0, nx1;          /* X grid dims */
+    int32_t ny0, ny1;          /* Y grid dims */
+    double x_dx, x_org0, x_org1;
+    double y_dx, y_org0, y_org1;
+    double eps, lam;
+    double nu_total;           /* |nu| */
+} dd_geom;
+
+/* Device-resident plan state shared by the cell kernels. */
+typedef struct dd_state {
+    const double* mu;          /* X grid masses  [nx0*nx1] */
+    const double* nu;          /* Y grid masses  [ny0*ny1] */
+    const double* log_mu;      /* log mu (-inf where mu == 0) */
+    const double* log_nu;
+    int32_t n_basic;
+    int32_t block0, block1;    /* basic block shape (s or 1, s) */
+    const int32_t* basic_xbox; /* [n_basic*4] X block of each basic cell */
+    const double* basic_mass;  /* [n_basic] mu mass per basic cell */
+    int32_t* ybox;             /* [n_basic*4] Y-marginal boxes */
+    double* yval;              /* [n_basic*cap] compact row-major values */
+    int64_t cap;               /* slot capacity (entries) */
+    double* x_marg;            /* [n_basic*block0*block1] dense over the block */
+    double* transport;         /* [n_basic] */
+    double* kl;                /* [n_basic] */
+    /* dual store of the partition being processed */
+    double* d_alpha;           /* [n_comp*nx_win] */
+    int32_t* d_has;            /* [n_comp] */
+    int32_t* d_box;            /* [n_comp*4] */
+    double* d_beta;            /* [n_comp*d_cap] */
+    int64_t d_cap;
+} dd_state;
+
+/* One batch of composite cells. Descriptor rows (int32, 12 per cell):
+ *   j, xo0, xe0, xo1, xe1, yo0, ye0, yo1, ye1, n_mem, mem_base, flags
+ * Offsets (int64, 4 per cell): y arena offset (ny entries), member arena
+ * offset (6*n_mem*ny entries), workspace offset (global-memory mode),
+ * member-x arena offset (n_mem*block entries). */
+typedef struct dd_batch {
+    int32_t n_cells;
+    int32_t nxw0, nxw1;        /* common X window shape */
+    const int32_t* desc;       /* [n_cells*12] */
+    const int64_t* offs;       /* [n_cells*4] */
+    const int32_t* members;    /* member basic ids */
+    const double* snapshot;    /* assembled Y-marginal [ny0*ny1] */
+    /* outputs / arenas */
+    double* alpha;             /* [n_cells*nxw0*nxw1] */
+    double* beta;              /* y arena: beta (in: warm start written by kernel) */
+    double* mdens;             /* y arena: background density m */
+    double* marena;            /* member arena */
+    double* work;              /* workspace arena (global mode) */
+    double* xarena;            /* member x-marginal arena */
+    int32_t* mbox;             /* [n_members_total*4] new member boxes, by member slot */
+    double* mstat;             /* [n_members_total*4] transport, kl, truncated, extra */
+    double* cstat;             /* [n_cells*8] gap, first_gap, iters, conv, nclamped,
+                                  newton_clamped, balance_fallbacks, target_miss */
+    double* cstat2;            /* [n_cells*4] drift_nodes, trunc_total, unused, unused */
+    int32_t smem_mode;         /* 1: workspace in shared memory */
+    int32_t smem_bytes;
+    /* solver configuration */
+    double delta;              /* cell tolerance */
+    int32_t max_iters;
+    int32_t newton_max_iters;
+    double newton_tol;
+    double trunc;
+} dd_batch;
+
+const char* dd_last_error(void);
+int dd_device_count(void);
+int dd_abi_version(void);
+
+/* out = separable log-sum-exp sweep (to_x = 1: Y grid -> X grid). work holds
+ * max(ny0*nx1, nx0*ny1) doubles. */
+int dd_grid_lse(const dd_geom* g, const double* v, double* out, int to_x, double* work,
+                void* stream);
+
+/* Elementwise: out[i] = a[i]*s + b[i], or a[i]/s + b[i] when divide != 0
+ * (b may be NULL). */
+int dd_axpb(int64_t n, const double* a, double s, const double* b, double* out, int divide,
+            void* stream);
+
+/* Zero-background Y step: beta = finite(z) ? -ratio*z : lam*700; counts
+ * degenerate nodes into *n_deg (device int, accumulated). */
+int dd_newton_global(int64_t n, const double* z, double ratio, double lam, double* beta,
+                     int32_t* n_deg, void* stream);
+
+/* Per-node unbalanced Y step (sinkhorn.py:230-333): root of
+ * log(m + exp(beta/eps + z)) + beta/lam = 0 by safeguarded Newton, with the
+ * closed forms for m == 0 / z == -inf.  m == NULL means zero background;
+ * eps and lam are per node. */
+int dd_newton_nodes(int64_t n, const double* z, const double* m, const double* beta0,
+                    const double* eps, const double* lam, double tol, int max_iters, double* beta,
+                    int32_t* n_deg, void* stream);
+
+/* Global reductions.  mode 0 (gap):  sums[0] = sum_x gap terms of
+ *   KL(P_X pi | e^{-alpha/lam} mu) given L, px written if non-NULL.
+ * mode 1 (dual): sums[0] = sum nu e^{b/eps + z}, sums[1] = sum mu(1-e^{-a/lam}),
+ *   sums[2] = sum nu(1-e^{-b/lam}).  partial holds >= 2*1024 doubles. */
+int dd_global_terms(int mode, int64_t n_x, int64_t n_y, const double* a, const double* l,
+                    const double* w, const double* b, const double* z, const double* w2,
+                    double eps, double lam, double* px, double* partial, double* sums,
+                    void* stream);
+
+/* Cell batch: assemble windows, Sinkhorn to tolerance, split, balance,
+ * truncate, fragments, x-marginals. */
+int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream);
+
+/* Blend scoring: per-cell dy windows (into dy arena at the y offsets) and
+ * per-cell scalars cd[c*4] = t_delta, k_delta, d1_old, unused. */
+int dd_cell_delta(const dd_geom* g, const dd_state* s, const dd_batch* b, double* dy,
+                  double* cd, void* stream);
+
+/* Tracked energy pieces for per-cell weights theta: ywork (grid) = snapshot
+ * + sum theta dy, then out[0] = KL(clip(ywork) | nu), out[1..3] =
+ * sum theta t_delta, sum theta k_delta, sum (d1_blend - d1_old). */
+int dd_blend_energy(const dd_geom* g, const dd_state* s, const dd_batch* b, const double* dy,
+                    const double* cd, const double* theta, double* ywork, double* partial,
+                    double* out, void* stream);
+
+/* Commit theta-blends; stores duals, stitches alpha into alpha_grid, writes
+ * per-cell errs[c*4] = x_err, y_err, truncated added, unused.  If yrun is
+ * non-NULL it is updated in place (sequential mode). */
+int dd_cell_commit(const dd_geom* g, const dd_state* s, const dd_batch* b, const double* theta,
+                   double* alpha_grid, double* yrun, double* errs, void* stream);
+
+/* out (Y grid) = sum of the basic-cell marginals. */
+int dd_assemble(const dd_geom* g, const dd_state* s, double* out, void* stream);
+
+/* sums[0] = sum transport, [1] = sum kl, [2] = sum_i KL(x_marg_i | mu_i),
+ * [3] = KL(y | nu) for the given Y grid y. */
+int dd_energy_terms(const dd_geom* g, const dd_state* s, const double* y, double* partial,
+                    double* sums, void* stream);
+
+/* Product start nu_i = (m_i/|mu|) nu on the full box (cap >= ny0*ny1). */
+int dd_product_init(const dd_geom* g, const dd_state* s, double mu_total, void* stream);
+
+/* Cut the diagonal-scaling plan of global duals (alpha on X, beta on Y)
+ * along the basic cells: fragments and x-marginals into the state, the
+ * truncated bounding box of each cell's Y-marginal into boxes_out and the
+ * removed mass into trunc_out[i].  Values are written into the slots when
+ * s->yval is non-NULL and the box fits s->cap (call once with yval = NULL to
+ * size the slots, then again to fill them).  Requires block0*block1 <= 64. */
+int dd_cut_plan(const dd_geom* g, const dd_state* s, const double* alpha, const double* beta,
+                double trunc, double* trunc_out, int32_t* boxes_out, void* stream);
+
+/* Seed the dual store of one partition (n_comp cells, X windows xbox,
+ * Y boxes ybox) from global duals. */
+int dd_seed_duals(const dd_geom* g, const dd_state* s, int n_comp, int nw0, int nw1,
+                  const int32_t* xbox, const int32_t* ybox, const double* alpha,
+                  const double* beta, void* stream);
+
+/* opt strategy (engine.py:465-503): lam-free derivative pieces of the blend
+ * objective of cell c at weight th (th_cur = its current weight, ycur = the
+ * running blended Y-marginal): out[0..3] = sum d log(x/mu), sum d^2/x,
+ * sum dy log(y/nu), sum dy^2/y. */
+int dd_opt_gh(const dd_geom* g, const dd_state* s, const dd_batch* b, const double* dy, int c,
+              double th, double th_cur, const double* ycur, double* out, void* stream);
+
+/* ycur on cell c's window = clip(ycur + dth * dy, 0). */
+int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy, int c, double dth,
+               double* ycur, void* stream);
+
+/* Workspace doubles one cell of the given window shape needs. */
+int64_t dd_cell_ws_size(int nw0, int nw1, int ny0, int ny1);
+
+/* out[q] = sum over rows of in[r*width + q] (fixed order), q < width. */
+int dd_reduce_rows(int64_t n_rows, int width, const double* in, double* out, void* stream);
+
+/* out[0] = sum KL(max(y,0) | nu) (clip != 0) or KL(y | nu). */
+int dd_grid_kl(int64_t n, const double* y, const double* nu, int clip, double* partial,
+               double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOMDEC_B200_H */

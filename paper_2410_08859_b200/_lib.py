@@ -1,0 +1,129 @@
+"""ctypes binding of the C ABI in include/domdec_b200.h.
+
+The shared library is built in-tree (``paper_2410_08859_b200/libdomdec_b200.so``)
+by ``__graft_entry__.build()`` / ``make -C paper_2410_08859_b200/csrc``.  There is
+no fallback: every solver entry point calls :func:`lib` which raises when the
+library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdomdec_b200.so")
+
+EXPORTS = [
+    "dd_last_error", "dd_device_count", "dd_abi_version", "dd_grid_lse", "dd_axpb",
+    "dd_newton_global", "dd_global_terms", "dd_cell_solve", "dd_cell_delta", "dd_blend_energy",
+    "dd_cell_commit", "dd_assemble", "dd_energy_terms", "dd_product_init", "dd_cut_plan",
+    "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
+    "dd_opt_set", "dd_newton_nodes",
+]
+
+i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
+
+
+class Geom(C.Structure):
+    _fields_ = [("nx0", i32), ("nx1", i32), ("ny0", i32), ("ny1", i32),
+                ("x_dx", dbl), ("x_org0", dbl), ("x_org1", dbl),
+                ("y_dx", dbl), ("y_org0", dbl), ("y_org1", dbl),
+                ("eps", dbl), ("lam", dbl), ("nu_total", dbl)]
+
+
+class State(C.Structure):
+    _fields_ = [("mu", vp), ("nu", vp), ("log_mu", vp), ("log_nu", vp),
+                ("n_basic", i32), ("block0", i32), ("block1", i32),
+                ("basic_xbox", vp), ("basic_mass", vp), ("ybox", vp), ("yval", vp), ("cap", i64),
+                ("x_marg", vp), ("transport", vp), ("kl", vp),
+                ("d_alpha", vp), ("d_has", vp), ("d_box", vp), ("d_beta", vp), ("d_cap", i64)]
+
+
+class Batch(C.Structure):
+    _fields_ = [("n_cells", i32), ("nxw0", i32), ("nxw1", i32),
+                ("desc", vp), ("offs", vp), ("members", vp), ("snapshot", vp),
+                ("alpha", vp), ("beta", vp), ("mdens", vp), ("marena", vp), ("work", vp),
+                ("xarena", vp), ("mbox", vp), ("mstat", vp), ("cstat", vp), ("cstat2", vp),
+                ("smem_mode", i32), ("smem_bytes", i32),
+                ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
+                ("newton_tol", dbl), ("trunc", dbl)]
+
+
+_SIGS = {
+    "dd_last_error": ([], C.c_char_p),
+    "dd_device_count": ([], C.c_int),
+    "dd_abi_version": ([], C.c_int),
+    "dd_grid_lse": ([C.POINTER(Geom), vp, vp, C.c_int, vp, vp], C.c_int),
+    "dd_axpb": ([i64, vp, dbl, vp, vp, C.c_int, vp], C.c_int),
+    "dd_newton_global": ([i64, vp, dbl, dbl, vp, vp, vp], C.c_int),
+    "dd_global_terms": ([C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, dbl, dbl, vp, vp, vp, vp],
+                        C.c_int),
+    "dd_cell_solve": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp], C.c_int),
+    "dd_cell_delta": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp], C.c_int),
+    "dd_blend_energy": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp,
+                         vp, vp], C.c_int),
+    "dd_cell_commit": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp],
+                       C.c_int),
+    "dd_assemble": ([C.POINTER(Geom), C.POINTER(State), vp, vp], C.c_int),
+    "dd_energy_terms": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, vp], C.c_int),
+    "dd_product_init": ([C.POINTER(Geom), C.POINTER(State), dbl, vp], C.c_int),
+    "dd_cut_plan": ([C.POINTER(Geom), C.POINTER(State), vp, vp, dbl, vp, vp, vp], C.c_int),
+    "dd_seed_duals": ([C.POINTER(Geom), C.POINTER(State), C.c_int, C.c_int, C.c_int, vp, vp, vp,
+                       vp, vp], C.c_int),
+    "dd_cell_ws_size": ([C.c_int, C.c_int, C.c_int, C.c_int], i64),
+    "dd_reduce_rows": ([i64, C.c_int, vp, vp, vp], C.c_int),
+    "dd_grid_kl": ([i64, vp, vp, C.c_int, vp, vp, vp], C.c_int),
+    "dd_opt_gh": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, C.c_int, dbl, dbl, vp,
+                   vp, vp], C.c_int),
+    "dd_newton_nodes": ([i64, vp, vp, vp, vp, vp, dbl, C.c_int, vp, vp, vp], C.c_int),
+    "dd_opt_set": ([C.POINTER(Geom), C.POINTER(Batch), vp, C.c_int, dbl, vp, vp], C.c_int),
+}
+
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load the shared library and declare every signature (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LibraryError(
+            f"CUDA library {path} is missing; build it with __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    h = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(h, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = h
+    return h
+
+
+def lib() -> C.CDLL:
+    """The loaded library, requiring a visible CUDA device."""
+    h = load()
+    if h.dd_device_count() < 1:
+        raise LibraryError("no CUDA device visible to libdomdec_b200 (there is no CPU fallback)")
+    return h
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.dd_last_error().decode() if _lib is not None else ""
+        raise LibraryError(f"libdomdec_b200 call failed (rc={rc}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -1,0 +1,1293 @@
+// Batched composite-cell kernels: solve, blend scoring, commit.
+//
+// One CTA per composite cell.  The cell's X window (2s x 2s nodes) and Y
+// window (union of its members' Y-marginal boxes) are staged in a per-cell
+// workspace (shared memory when it fits, else a global arena), the separable
+// squared-Euclidean kernel is applied one grid axis at a time, and the whole
+// unbalanced Sinkhorn loop runs inside the CTA until the cell's own PD gap
+// test passes.  The epilogue splits the cell plan's Y-marginal by member
+// basic cells, balances member masses, truncates to fresh boxes, and forms
+// the score fragments and X-marginals — the same outputs the reference
+// produces in cells.py:283-443.
+
+#include "common.cuh"
+#include "domdec_b200.h"
+
+namespace dd {
+
+struct CellWin {
+    int xo0, xe0, xo1, xe1;  // X window
+    int yo0, ye0, yo1, ye1;  // Y window
+    int nx, ny;
+};
+
+// Workspace layout (doubles), identical on host and device.
+struct WsLayout {
+    int64_t xc0, xc1, yc0, yc1;
+    int64_t alpha, u, L, mu, tx, lmu;
+    int64_t beta, lnu, m, ty;
+    int64_t K0, K1, mid;
+    int64_t midstride;
+    int64_t total;
+};
+
+__host__ __device__ inline WsLayout ws_layout(int nw0, int nw1, int ny0, int ny1) {
+    WsLayout w;
+    const int64_t nx = (int64_t)nw0 * nw1, ny = (int64_t)ny0 * ny1;
+    int64_t o = 0;
+    w.xc0 = o; o += nw0;
+    w.xc1 = o; o += nw1;
+    w.yc0 = o; o += ny0;
+    w.yc1 = o; o += ny1;
+    w.alpha = o; o += nx;
+    w.u = o; o += nx;
+    w.L = o; o += nx;
+    w.mu = o; o += nx;
+    w.tx = o; o += nx;
+    w.lmu = o; o += nx;
+    w.beta = o; o += ny;
+    w.lnu = o; o += ny;
+    w.m = o; o += ny;
+    w.ty = o; o += ny;
+    w.K0 = o; o += (int64_t)nw0 * ny0;
+    w.K1 = o; o += (int64_t)nw1 * ny1;
+    int64_t ms = (int64_t)ny0 * nw1;
+    const int64_t ms2 = (int64_t)nw0 * ny1;
+    if (ms2 > ms) ms = ms2;
+    ms += nw0;  // row sums for the mc fragment
+    w.midstride = ms;
+    w.mid = o; o += 5 * ms;
+    w.total = o;
+    return w;
+}
+
+struct Ws {
+    double *xc0, *xc1, *yc0, *yc1;
+    double *alpha, *u, *L, *mu, *tx, *lmu;
+    double *beta, *lnu, *m, *ty;
+    double *K0, *K1, *mid;
+    int64_t ms;
+};
+
+__device__ inline Ws ws_bind(double* base, const WsLayout& l) {
+    Ws w;
+    w.xc0 = base + l.xc0; w.xc1 = base + l.xc1; w.yc0 = base + l.yc0; w.yc1 = base + l.yc1;
+    w.alpha = base + l.alpha; w.u = base + l.u; w.L = base + l.L; w.mu = base + l.mu;
+    w.tx = base + l.tx; w.lmu = base + l.lmu;
+    w.beta = base + l.beta; w.lnu = base + l.lnu; w.m = base + l.m; w.ty = base + l.ty;
+    w.K0 = base + l.K0; w.K1 = base + l.K1; w.mid = base + l.mid;
+    w.ms = l.midstride;
+    return w;
+}
+
+__device__ inline CellWin load_win(const int32_t* d, int nw0, int nw1) {
+    CellWin c;
+    c.xo0 = d[1]; c.xe0 = d[2]; c.xo1 = d[3]; c.xe1 = d[4];
+    c.yo0 = d[5]; c.ye0 = d[6]; c.yo1 = d[7]; c.ye1 = d[8];
+    c.nx = nw0 * nw1;
+    c.ny = c.ye0 * c.ye1;
+    return c;
+}
+
+__device__ __forceinline__ double negsq(double a, double b, double eps) {
+    const double d = a - b;
+    return -(d * d) / eps;
+}
+
+// Two-pass log-sum-exp with exact skipping of terms that underflow to zero.
+// Used by the log-domain (wide-window) path.
+
+// ---- separable sweeps ------------------------------------------------------
+
+// L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (matrix or log mode).
+__device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                           bool matrix, double* out, double* red) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny;
+    double lmax = kNegInf;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const double bv = w.beta[y] / eps + w.lnu[y];
+        w.ty[y] = bv;
+        lmax = fmax(lmax, bv);
+    }
+    if (matrix) {
+        double B = block_max(lmax, red);
+        if (!isfinite(B)) B = 0.0;
+        for (int y = threadIdx.x; y < ny; y += DD_NT) w.ty[y] = exp(w.ty[y] - B);
+        __syncthreads();
+        for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
+            const int y0 = o / nw1, x1 = o - y0 * nw1;
+            const double* tr = w.ty + (int64_t)y0 * ny1;
+            const double* kr = w.K1 + (int64_t)x1 * ny1;
+            double s = 0.0;
+            for (int y1 = 0; y1 < ny1; ++y1) s = fma(tr[y1], kr[y1], s);
+            w.mid[o] = s;
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < nw0 * nw1; o += DD_NT) {
+            const int x0 = o / nw1, x1 = o - x0 * nw1;
+            const double* kr = w.K0 + (int64_t)x0 * ny0;
+            double s = 0.0;
+            for (int y0 = 0; y0 < ny0; ++y0) s = fma(kr[y0], w.mid[(int64_t)y0 * nw1 + x1], s);
+            out[o] = log(s) + B;
+        }
+        __syncthreads();
+    } else {
+        __syncthreads();
+        for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
+            const int y0 = o / nw1, x1 = o - y0 * nw1;
+            const double* tr = w.ty + (int64_t)y0 * ny1;
+            const double xc = w.xc1[x1];
+            double mx = kNegInf;
+            for (int y1 = 0; y1 < ny1; ++y1) mx = fmax(mx, tr[y1] + negsq(xc, w.yc1[y1], eps));
+            double r;
+            if (!isfinite(mx)) {
+                r = kNegInf;
+            } else {
+                double s = 0.0;
+                for (int y1 = 0; y1 < ny1; ++y1) {
+                    const double t = tr[y1] + negsq(xc, w.yc1[y1], eps) - mx;
+                    if (t > -760.0) s += exp(t);
+                }
+                r = log(s) + mx;
+            }
+            w.mid[o] = r;
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < nw0 * nw1; o += DD_NT) {
+            const int x0 = o / nw1, x1 = o - x0 * nw1;
+            const double xc = w.xc0[x0];
+            double mx = kNegInf;
+            for (int y0 = 0; y0 < ny0; ++y0)
+                mx = fmax(mx, w.mid[(int64_t)y0 * nw1 + x1] + negsq(xc, w.yc0[y0], eps));
+            double r;
+            if (!isfinite(mx)) {
+                r = kNegInf;
+            } else {
+                double s = 0.0;
+                for (int y0 = 0; y0 < ny0; ++y0) {
+                    const double t = w.mid[(int64_t)y0 * nw1 + x1] + negsq(xc, w.yc0[y0], eps) - mx;
+                    if (t > -760.0) s += exp(t);
+                }
+                r = log(s) + mx;
+            }
+            out[o] = r;
+        }
+        __syncthreads();
+    }
+}
+
+// z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu.
+__device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                           bool matrix, double* out, double* red) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    double lmax = kNegInf;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) {
+        const double av = w.alpha[x] / eps + w.lmu[x];
+        w.tx[x] = av;
+        lmax = fmax(lmax, av);
+    }
+    if (matrix) {
+        double A = block_max(lmax, red);
+        if (!isfinite(A)) A = 0.0;
+        for (int x = threadIdx.x; x < nx; x += DD_NT) w.tx[x] = exp(w.tx[x] - A);
+        __syncthreads();
+        for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
+            const int x0 = o / ny1, y1 = o - x0 * ny1;
+            const double* tr = w.tx + (int64_t)x0 * nw1;
+            double s = 0.0;
+            for (int x1 = 0; x1 < nw1; ++x1) s = fma(tr[x1], w.K1[(int64_t)x1 * ny1 + y1], s);
+            w.mid[o] = s;
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < ny; o += DD_NT) {
+            const int y0 = o / ny1, y1 = o - y0 * ny1;
+            double s = 0.0;
+            for (int x0 = 0; x0 < nw0; ++x0)
+                s = fma(w.K0[(int64_t)x0 * ny0 + y0], w.mid[(int64_t)x0 * ny1 + y1], s);
+            out[o] = log(s) + A;
+        }
+        __syncthreads();
+    } else {
+        __syncthreads();
+        for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
+            const int x0 = o / ny1, y1 = o - x0 * ny1;
+            const double* tr = w.tx + (int64_t)x0 * nw1;
+            const double yc = w.yc1[y1];
+            double mx = kNegInf;
+            for (int x1 = 0; x1 < nw1; ++x1) mx = fmax(mx, tr[x1] + negsq(w.xc1[x1], yc, eps));
+            double r;
+            if (!isfinite(mx)) {
+                r = kNegInf;
+            } else {
+                double s = 0.0;
+                for (int x1 = 0; x1 < nw1; ++x1) {
+                    const double t = tr[x1] + negsq(w.xc1[x1], yc, eps) - mx;
+                    if (t > -760.0) s += exp(t);
+                }
+                r = log(s) + mx;
+            }
+            w.mid[o] = r;
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < ny; o += DD_NT) {
+            const int y0 = o / ny1, y1 = o - y0 * ny1;
+            const double yc = w.yc0[y0];
+            double mx = kNegInf;
+            for (int x0 = 0; x0 < nw0; ++x0)
+                mx = fmax(mx, w.mid[(int64_t)x0 * ny1 + y1] + negsq(w.xc0[x0], yc, eps));
+            double r;
+            if (!isfinite(mx)) {
+                r = kNegInf;
+            } else {
+                double s = 0.0;
+                for (int x0 = 0; x0 < nw0; ++x0) {
+                    const double t = w.mid[(int64_t)x0 * ny1 + y1] + negsq(w.xc0[x0], yc, eps) - mx;
+                    if (t > -760.0) s += exp(t);
+                }
+                r = log(s) + mx;
+            }
+            out[o] = r;
+        }
+        __syncthreads();
+    }
+}
+
+// Value of a boxed marginal at absolute node (r, q); zero outside.
+__device__ __forceinline__ double boxed_at(const int32_t* box, const double* vals, int r, int q) {
+    const int o0 = box[0], e0 = box[1], o1 = box[2], e1 = box[3];
+    if (e0 <= 0 || e1 <= 0) return 0.0;
+    const int a = r - o0, bq = q - o1;
+    if (a < 0 || a >= e0 || bq < 0 || bq >= e1) return 0.0;
+    return vals[(int64_t)a * e1 + bq];
+}
+
+// ---- the solve kernel -----------------------------------------------------
+
+__global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
+    extern __shared__ double smem[];
+    __shared__ double red[DD_NW + 1];
+    __shared__ int redi[DD_NW + 1];
+    __shared__ double sh_sc[16];
+    __shared__ int sh_flag[4];
+
+    const int c = blockIdx.x;
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t* off = b.offs + (int64_t)c * 4;
+    const int nw0 = b.nxw0, nw1 = b.nxw1;
+    const CellWin cw = load_win(d, nw0, nw1);
+    const int j = d[0];
+    const int nmem = d[9];
+    const int32_t* mem = b.members + d[10];
+    const int nx = cw.nx, ny = cw.ny, ny0 = cw.ye0, ny1 = cw.ye1;
+    const WsLayout lay = ws_layout(nw0, nw1, ny0, ny1);
+    double* base = b.smem_mode ? smem : (b.work + off[2]);
+    const Ws w = ws_bind(base, lay);
+    const double eps = g.eps, lam = g.lam;
+    const double ratio = eps * lam / (eps + lam);
+    const int tid = threadIdx.x;
+    const int64_t yoff = off[0];
+    double* marena = b.marena + off[1];
+
+    // coordinates
+    for (int i = tid; i < nw0; i += DD_NT) w.xc0[i] = g.x_org0 + g.x_dx * (double)(cw.xo0 + i);
+    for (int i = tid; i < nw1; i += DD_NT) w.xc1[i] = g.x_org1 + g.x_dx * (double)(cw.xo1 + i);
+    for (int i = tid; i < ny0; i += DD_NT) w.yc0[i] = g.y_org0 + g.y_dx * (double)(cw.yo0 + i);
+    for (int i = tid; i < ny1; i += DD_NT) w.yc1[i] = g.y_org1 + g.y_dx * (double)(cw.yo1 + i);
+
+    // X window: mu, log mu (zero / -inf off the grid), warm-start alpha
+    const bool has_dual = s.d_has[j] != 0;
+    double musum_part = 0.0;
+    for (int x = tid; x < nx; x += DD_NT) {
+        const int x0 = x / nw1, x1 = x - x0 * nw1;
+        const int r = cw.xo0 + x0, q = cw.xo1 + x1;
+        double mu = 0.0, lmu = kNegInf;
+        if (r >= 0 && r < g.nx0 && q >= 0 && q < g.nx1) {
+            const int64_t id = (int64_t)r * g.nx1 + q;
+            mu = s.mu[id];
+            lmu = s.log_mu[id];
+        }
+        w.mu[x] = mu;
+        w.lmu[x] = lmu;
+        w.alpha[x] = has_dual ? s.d_alpha[(int64_t)j * nx + x] : 0.0;
+        musum_part += mu;
+    }
+    const double musum = block_sum(musum_part, red);
+    const double thr = b.delta * musum;
+
+    // Y window: log nu, background density m, warm-start beta
+    const int32_t* dbox = s.d_box + (int64_t)j * 4;
+    const double* dbeta = s.d_beta + (int64_t)j * s.d_cap;
+    int nclamp = 0;
+    int anym = 0;
+    for (int y = tid; y < ny; y += DD_NT) {
+        const int y0 = y / ny1, y1 = y - y0 * ny1;
+        const int r = cw.yo0 + y0, q = cw.yo1 + y1;
+        const int64_t id = (int64_t)r * g.ny1 + q;
+        const double nu = s.nu[id];
+        w.lnu[y] = s.log_nu[id];
+        double cs = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            cs += boxed_at(s.ybox + (int64_t)i * 4, s.yval + (int64_t)i * s.cap, r, q);
+        }
+        const double pw = b.snapshot[id];
+        const double diff = pw - cs;
+        if (diff < -1e-12 * fmax(pw, cs)) ++nclamp;
+        const double mm = fmax(diff, 0.0) / nu;
+        w.m[y] = mm;
+        b.mdens[yoff + y] = mm;
+        if (mm != 0.0) anym = 1;
+        w.beta[y] = has_dual ? boxed_at(dbox, dbeta, r, q) : 0.0;
+    }
+    const int n_clamped = (int)block_sum((double)nclamp, red);
+    const bool has_m = block_max_i(anym, redi) != 0;
+
+    // kernel mode (reference: DenseKernel matrix mode iff min(-c/eps) > -700)
+    const double d0 = fmax(fabs(g.x_org0 + g.x_dx * (double)cw.xo0 - (g.y_org0 + g.y_dx * (double)(cw.yo0 + ny0 - 1))),
+              fabs(g.x_org0 + g.x_dx * (double)(cw.xo0 + nw0 - 1) - (g.y_org0 + g.y_dx * (double)cw.yo0)));
+    const double d1 = fmax(fabs(g.x_org1 + g.x_dx * (double)cw.xo1 - (g.y_org1 + g.y_dx * (double)(cw.yo1 + ny1 - 1))),
+              fabs(g.x_org1 + g.x_dx * (double)(cw.xo1 + nw1 - 1) - (g.y_org1 + g.y_dx * (double)cw.yo1)));
+    const bool matrix = -((d0 * d0 + d1 * d1) / eps) > -700.0;
+    if (matrix) {
+        for (int o = tid; o < nw0 * ny0; o += DD_NT) {
+            const int x0 = o / ny0, y0 = o - x0 * ny0;
+            w.K0[o] = exp(negsq(w.xc0[x0], w.yc0[y0], eps));
+        }
+        for (int o = tid; o < nw1 * ny1; o += DD_NT) {
+            const int x1 = o / ny1, y1 = o - x1 * ny1;
+            w.K1[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps));
+        }
+    }
+    __syncthreads();
+
+    // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
+    bool converged = false;
+    bool have_first = false;
+    double gap = __builtin_huge_val(), first_gap = 0.0;
+    int iters = 0, newton_clamped = 0;
+    const double inv_lam = 1.0 / lam;
+    for (int k = 1; k <= b.max_iters; ++k) {
+        cell_lse_x(w, cw, nw0, nw1, eps, matrix, w.L, red);
+        if (k >= 2) {
+            double part = 0.0;
+            for (int x = tid; x < nx; x += DD_NT) {
+                const double mu = w.mu[x];
+                if (mu > 0) {
+                    const double a = w.alpha[x];
+                    const double lr = a / eps + w.L[x];
+                    const double px = mu * exp(lr);
+                    const double ref = mu * exp(-a / lam);
+                    part += px * (lr + a / lam) - px + ref;
+                }
+            }
+            gap = lam * block_sum(part, red);
+            if (!have_first) { first_gap = gap; have_first = true; }
+            if (gap / lam <= thr) { converged = true; break; }
+        }
+        for (int x = tid; x < nx; x += DD_NT) w.alpha[x] = -ratio * w.L[x];
+        __syncthreads();
+        cell_lse_y(w, cw, nw0, nw1, eps, matrix, w.ty, red);
+        int ndeg = 0;
+        for (int y = tid; y < ny; y += DD_NT) {
+            int dg = 0;
+            w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
+                                    b.newton_max_iters, &dg);
+            ndeg += dg;
+        }
+        const int nd = (int)block_sum((double)ndeg, red);
+        newton_clamped = max(newton_clamped, nd);
+        iters = k;
+    }
+    (void)inv_lam;
+    if (!converged) {
+        cell_lse_x(w, cw, nw0, nw1, eps, matrix, w.L, red);
+        double part = 0.0;
+        for (int x = tid; x < nx; x += DD_NT) {
+            const double mu = w.mu[x];
+            if (mu > 0) {
+                const double a = w.alpha[x];
+                const double lr = a / eps + w.L[x];
+                const double px = mu * exp(lr);
+                const double ref = mu * exp(-a / lam);
+                part += px * (lr + a / lam) - px + ref;
+            }
+        }
+        gap = lam * block_sum(part, red);
+        if (!have_first) { first_gap = gap; have_first = true; }
+        converged = gap / lam <= thr;
+    }
+    // outputs: duals
+    for (int x = tid; x < nx; x += DD_NT) b.alpha[(int64_t)c * nx + x] = w.alpha[x];
+    for (int y = tid; y < ny; y += DD_NT) b.beta[yoff + y] = w.beta[y];
+
+    // balancing reference mu_bar = exp(-alpha_extra/lam) mu, alpha_extra = -ratio L
+    for (int x = tid; x < nx; x += DD_NT) {
+        const double ae = -ratio * w.L[x];
+        w.L[x] = exp(-ae / lam) * w.mu[x];
+        w.u[x] = w.alpha[x] / eps + w.lmu[x];
+    }
+    // v[y] = beta/eps + lnu (kept in ty for the epilogue)
+    for (int y = tid; y < ny; y += DD_NT) w.ty[y] = w.beta[y] / eps + w.lnu[y];
+    __syncthreads();
+
+    // ---- per-member split of the plan's Y-marginal + fragment columns ----
+    double* RAW = marena;
+    double* TC = marena + (int64_t)nmem * ny;
+    double* TL = marena + (int64_t)2 * nmem * ny;
+    double* MC = marena + (int64_t)3 * nmem * ny;
+    double* VALS = marena + (int64_t)4 * nmem * ny;
+    double* NEWV = marena + (int64_t)5 * nmem * ny;
+    double* M1 = w.mid;
+    double* M2 = w.mid + w.ms;
+    double* M3 = w.mid + 2 * w.ms;
+    double* M4 = w.mid + 3 * w.ms;
+    double* M5 = w.mid + 4 * w.ms;
+    __shared__ double mbar[64], Ak[64], masses[64], targets[64], surplus[64], tol[64];
+    for (int k = 0; k < nmem; ++k) {
+        const int i = mem[k];
+        const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+        const int r0 = bx[0] - cw.xo0, e0 = bx[1], c0 = bx[2] - cw.xo1, e1 = bx[3];
+        double am = kNegInf, mb = 0.0;
+        for (int t = tid; t < e0 * e1; t += DD_NT) {
+            const int a0 = t / e1, a1 = t - a0 * e1;
+            const int x = (r0 + a0) * nw1 + (c0 + a1);
+            am = fmax(am, w.u[x]);
+            mb += w.L[x];
+        }
+        const double A = block_max(am, red);
+        const double mbk = block_sum(mb, red);
+        if (tid == 0) { mbar[k] = mbk; Ak[k] = A; }
+        double* raw = RAW + (int64_t)k * ny;
+        double* tc = TC + (int64_t)k * ny;
+        double* tl = TL + (int64_t)k * ny;
+        double* mc = MC + (int64_t)k * ny;
+        if (matrix) {
+            for (int t = tid; t < e0 * e1; t += DD_NT) {
+                const int a0 = t / e1, a1 = t - a0 * e1;
+                const int x = (r0 + a0) * nw1 + (c0 + a1);
+                w.tx[x] = exp(w.u[x] - A);
+            }
+            __syncthreads();
+            for (int o = tid; o < e0 * ny1; o += DD_NT) {
+                const int a0 = o / ny1, y1 = o - a0 * ny1;
+                const int x0 = r0 + a0;
+                const double yc = w.yc1[y1];
+                double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+                for (int a1 = 0; a1 < e1; ++a1) {
+                    const int x1 = c0 + a1;
+                    const int x = x0 * nw1 + x1;
+                    const double dd = w.xc1[x1] - yc;
+                    const double D1 = dd * dd;
+                    const double wk = w.tx[x] * w.K1[(int64_t)x1 * ny1 + y1];
+                    s1 += wk;
+                    s2 += wk * D1;
+                    s3 += wk * w.alpha[x];
+                    s4 += w.mu[x] * D1;
+                }
+                M1[o] = s1; M2[o] = s2; M3[o] = s3; M4[o] = s4;
+            }
+            for (int a0 = tid; a0 < e0; a0 += DD_NT) {
+                double ssum = 0.0;
+                for (int a1 = 0; a1 < e1; ++a1) ssum += w.mu[(r0 + a0) * nw1 + c0 + a1];
+                M5[a0] = ssum;
+            }
+            __syncthreads();
+            for (int y = tid; y < ny; y += DD_NT) {
+                const int y0 = y / ny1, y1 = y - y0 * ny1;
+                const double yc = w.yc0[y0];
+                double P = 0.0, C = 0.0, Q = 0.0, MCv = 0.0;
+                for (int a0 = 0; a0 < e0; ++a0) {
+                    const int x0 = r0 + a0;
+                    const double dd = w.xc0[x0] - yc;
+                    const double D0 = dd * dd;
+                    const double k0 = w.K0[(int64_t)x0 * ny0 + y0];
+                    const int64_t o = (int64_t)a0 * ny1 + y1;
+                    P += k0 * M1[o];
+                    C += k0 * (D0 * M1[o] + M2[o]);
+                    Q += k0 * M3[o];
+                    MCv += D0 * M5[a0] + M4[o];
+                }
+                const double bv = w.beta[y] / eps;
+                const double sc = exp(A + w.ty[y]);
+                raw[y] = sc * P;
+                tc[y] = sc * C;
+                tl[y] = sc * (Q / eps + bv * P - C / eps);
+                mc[y] = MCv;
+            }
+        } else {
+            for (int y = tid; y < ny; y += DD_NT) {
+                const int y0 = y / ny1, y1 = y - y0 * ny1;
+                double P = 0.0, C = 0.0, T = 0.0, MCv = 0.0;
+                for (int a0 = 0; a0 < e0; ++a0) {
+                    const int x0 = r0 + a0;
+                    const double dd0 = w.xc0[x0] - w.yc0[y0];
+                    for (int a1 = 0; a1 < e1; ++a1) {
+                        const int x1 = c0 + a1;
+                        const int x = x0 * nw1 + x1;
+                        const double dd1 = w.xc1[x1] - w.yc1[y1];
+                        const double cost = dd0 * dd0 + dd1 * dd1;
+                        const double scv = w.alpha[x] / eps + w.beta[y] / eps + (-cost / eps);
+                        const double pl = exp(scv + w.lmu[x] + w.lnu[y]);
+                        P += pl;
+                        C += pl * cost;
+                        T += pl * scv;
+                        MCv += cost * w.mu[x];
+                    }
+                }
+                raw[y] = P;
+                tc[y] = C;
+                tl[y] = T;
+                mc[y] = MCv;
+            }
+        }
+        __syncthreads();
+        for (int y = tid; y < ny; y += DD_NT) VALS[(int64_t)k * ny + y] = raw[y];
+        __syncthreads();
+    }
+
+    // ---- balancing (cells.py:446-485) ----
+    int fallbacks = 0, drift = 0;
+    double target_miss = 0.0;
+    {
+        for (int k = 0; k < nmem; ++k) {
+            double p = 0.0;
+            for (int y = tid; y < ny; y += DD_NT) p += VALS[(int64_t)k * ny + y];
+            const double mk = block_sum(p, red);
+            if (tid == 0) masses[k] = mk;
+        }
+        __syncthreads();
+        double total = 0.0, nu_j = 0.0;
+        for (int k = 0; k < nmem; ++k) { total += mbar[k]; nu_j += masses[k]; }
+        __syncthreads();
+        if (tid == 0) {
+            for (int k = 0; k < nmem; ++k) {
+                targets[k] = mbar[k] * (nu_j / total);
+                surplus[k] = masses[k] - targets[k];
+                tol[k] = 1e-13 * fmax(targets[k], 1e-300);
+            }
+        }
+        __syncthreads();
+        int nd = 0, nr = 0;
+        int donors[64], recips[64];
+        for (int k = 0; k < nmem; ++k) {
+            if (surplus[k] > tol[k]) donors[nd++] = k;
+            if (surplus[k] < -tol[k]) recips[nr++] = k;
+        }
+        if (nd > 0 && nr > 0) {
+            // column sums before (member order), kept in ty
+            for (int y = tid; y < ny; y += DD_NT) {
+                double cs = 0.0;
+                for (int k = 0; k < nmem; ++k) cs += VALS[(int64_t)k * ny + y];
+                w.ty[y] = cs;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int di = 0, ri = 0;
+                while (di < nd && ri < nr) {
+                    const int dk = donors[di], rk = recips[ri];
+                    const double amount = fmin(surplus[dk], -surplus[rk]);
+                    // _move_mass (cells.py:488-507)
+                    if (amount > 0) {
+                        double* row = VALS + (int64_t)dk * ny;
+                        double* rrow = VALS + (int64_t)rk * ny;
+                        double cum = 0.0;
+                        int kk = -1;
+                        double prev = 0.0;
+                        for (int y = 0; y < ny; ++y) {
+                            prev = cum;
+                            cum += row[y];
+                            if (cum >= amount) { kk = y; break; }
+                        }
+                        if (kk < 0) {
+                            // donor cannot cover: hand over everything
+                            if (ny > 0 && cum > 0) {
+                                for (int y = 0; y < ny; ++y) { rrow[y] += row[y]; row[y] = 0.0; }
+                            }
+                            fallbacks += 1;
+                        } else {
+                            for (int y = 0; y < kk; ++y) { rrow[y] += row[y]; row[y] = 0.0; }
+                            const double part = amount - (kk ? prev : 0.0);
+                            row[kk] -= part;
+                            rrow[kk] += part;
+                        }
+                    }
+                    surplus[dk] -= amount;
+                    surplus[rk] += amount;
+                    if (surplus[dk] <= tol[dk]) ++di;
+                    if (surplus[rk] >= -tol[rk]) ++ri;
+                }
+                sh_flag[0] = fallbacks;
+            }
+            __syncthreads();
+            fallbacks = sh_flag[0];
+            for (int k = 0; k < nmem; ++k)
+                for (int y = tid; y < ny; y += DD_NT) {
+                    double v = VALS[(int64_t)k * ny + y];
+                    if (v < 0.0) VALS[(int64_t)k * ny + y] = 0.0;
+                }
+            __syncthreads();
+            // restore column sums bitwise (cells.py:510-563)
+            int bad = 0;
+            for (int y = tid; y < ny; y += DD_NT) {
+                const double target = w.ty[y];
+                double cs = 0.0;
+                for (int k = 0; k < nmem; ++k) cs += VALS[(int64_t)k * ny + y];
+                if (cs == target) continue;
+                // order by value descending
+                int order[64];
+                for (int k = 0; k < nmem; ++k) order[k] = k;
+                for (int a = 1; a < nmem; ++a) {
+                    int t = order[a];
+                    int q = a - 1;
+                    while (q >= 0 && VALS[(int64_t)order[q] * ny + y] < VALS[(int64_t)t * ny + y]) {
+                        order[q + 1] = order[q];
+                        --q;
+                    }
+                    order[q + 1] = t;
+                }
+                bool ok = false;
+                for (int oi = 0; oi < nmem && !ok; ++oi) {
+                    const int t = order[oi];
+                    double* e = VALS + (int64_t)t * ny + y;
+                    const double x0 = *e;
+                    double x = x0;
+                    for (int it = 0; it < 256; ++it) {
+                        double sm = 0.0;
+                        for (int k = 0; k < nmem; ++k) sm += VALS[(int64_t)k * ny + y];
+                        if (sm == target) { ok = true; break; }
+                        x = nextafter(x, sm < target ? __builtin_huge_val() : -__builtin_huge_val());
+                        if (x < 0) break;
+                        *e = x;
+                    }
+                    if (!ok) {
+                        double sm = 0.0;
+                        *e = x0;
+                        for (int k = 0; k < nmem; ++k) sm += VALS[(int64_t)k * ny + y];
+                        ok = sm == target;
+                    }
+                }
+                if (!ok) ++bad;
+            }
+            drift = (int)block_sum((double)bad, red);
+        }
+        double miss = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            double p = 0.0;
+            for (int y = tid; y < ny; y += DD_NT) p += VALS[(int64_t)k * ny + y];
+            const double mk = block_sum(p, red);
+            miss = fmax(miss, fabs(mk - targets[k]) / fmax(targets[k], 1e-300));
+        }
+        target_miss = miss;
+    }
+
+    // ---- truncation, fragments, x-marginals (cells.py:396-443) ----
+    double trunc_total = 0.0;
+    const int bs = s.block0 * s.block1;
+    for (int k = 0; k < nmem; ++k) {
+        const int i = mem[k];
+        const double* vals = VALS + (int64_t)k * ny;
+        const double* raw = RAW + (int64_t)k * ny;
+        // bounding box of kept entries, removed mass
+        int rmin = 0x7fffffff, rmax = -1, cmin = 0x7fffffff, cmax = -1;
+        double rem = 0.0;
+        for (int y = tid; y < ny; y += DD_NT) {
+            const double v = vals[y];
+            if (v >= b.trunc) {
+                const int y0 = y / ny1, y1 = y - y0 * ny1;
+                rmin = min(rmin, y0); rmax = max(rmax, y0);
+                cmin = min(cmin, y1); cmax = max(cmax, y1);
+            } else {
+                rem += v;
+            }
+        }
+        rmin = block_min_i(rmin, redi);
+        rmax = block_max_i(rmax, redi);
+        cmin = block_min_i(cmin, redi);
+        cmax = block_max_i(cmax, redi);
+        const double removed = block_sum(rem, red);
+        trunc_total += removed;
+        const int mslot = d[10] + k;
+        int nb0 = 0, ne0 = 0, nb1 = 0, ne1 = 0;
+        if (rmax >= 0) {
+            nb0 = cw.yo0 + rmin; ne0 = rmax - rmin + 1;
+            nb1 = cw.yo1 + cmin; ne1 = cmax - cmin + 1;
+        }
+        if (tid == 0) {
+            b.mbox[(int64_t)mslot * 4 + 0] = nb0;
+            b.mbox[(int64_t)mslot * 4 + 1] = ne0;
+            b.mbox[(int64_t)mslot * 4 + 2] = nb1;
+            b.mbox[(int64_t)mslot * 4 + 3] = ne1;
+        }
+        double* nv = NEWV + (int64_t)k * ny;
+        for (int t = tid; t < ne0 * ne1; t += DD_NT) {
+            const int a0 = t / ne1, a1 = t - a0 * ne1;
+            const double v = vals[(int64_t)(rmin + a0) * ny1 + (cmin + a1)];
+            nv[t] = v >= b.trunc ? v : 0.0;
+        }
+        const double mass = s.basic_mass[i];
+        double S1 = 0, S2 = 0, S3 = 0, S4 = 0, S5 = 0, S6 = 0, SX = 0;
+        const double* tc = TC + (int64_t)k * ny;
+        const double* tl = TL + (int64_t)k * ny;
+        const double* mc = MC + (int64_t)k * ny;
+        for (int y = tid; y < ny; y += DD_NT) {
+            const double v = vals[y];
+            const double fin = v >= b.trunc ? v : 0.0;
+            const double r = raw[y];
+            const bool pos = r > 0;
+            const double f = pos ? fin / r : 0.0;
+            const double extra = pos ? 0.0 : fin;
+            S1 += f * tc[y];
+            S2 += extra * mc[y];
+            S3 += f * tl[y];
+            S4 += xlogy(pos ? fin : 0.0, f);
+            {
+                const int y0 = y / ny1, y1 = y - y0 * ny1;
+                const double nu = s.nu[(int64_t)(cw.yo0 + y0) * g.ny1 + (cw.yo1 + y1)];
+                S5 += xlogy(extra, extra / (mass * nu));
+            }
+            S6 += fin;
+            SX += extra;
+            // stash f in the TL column (no longer needed after S3): use ty instead
+        }
+        S1 = block_sum(S1, red);
+        S2 = block_sum(S2, red);
+        S3 = block_sum(S3, red);
+        S4 = block_sum(S4, red);
+        S5 = block_sum(S5, red);
+        S6 = block_sum(S6, red);
+        SX = block_sum(SX, red);
+        const double transport = S1 + S2 / mass;
+        const double klv = S3 + S4 + S5 - S6 + mass * g.nu_total;
+        if (tid == 0) {
+            b.mstat[(int64_t)mslot * 4 + 0] = transport;
+            b.mstat[(int64_t)mslot * 4 + 1] = klv;
+            b.mstat[(int64_t)mslot * 4 + 2] = removed;
+            b.mstat[(int64_t)mslot * 4 + 3] = SX;
+        }
+        // x-marginal: xm[x] = sum_y plan[x,y] f[y] (+ mu[x] SX/mass)
+        const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+        const int r0 = bx[0] - cw.xo0, e0 = bx[1], c0 = bx[2] - cw.xo1, e1 = bx[3];
+        double* xout = b.xarena + off[3] + (int64_t)k * bs;
+        __syncthreads();
+        const double A = Ak[k];
+        // f into ty (ty currently holds v = beta/eps + lnu; rebuild after)
+        __syncthreads();
+        if (matrix) {
+            // gy[y] = exp(A + v[y]) f[y], staged in M3 region (size >= ny0*e1 needed for N1)
+            for (int y = tid; y < ny; y += DD_NT) {
+                const double v = vals[y];
+                const double fin = v >= b.trunc ? v : 0.0;
+                const double r = raw[y];
+                const double f = r > 0 ? fin / r : 0.0;
+                w.m[y] = f == 0.0 ? 0.0 : exp(A + w.beta[y] / eps + w.lnu[y]) * f;
+            }
+            __syncthreads();
+            for (int o = tid; o < ny0 * e1; o += DD_NT) {
+                const int y0 = o / e1, a1 = o - y0 * e1;
+                const int x1 = c0 + a1;
+                double sacc = 0.0;
+                for (int y1 = 0; y1 < ny1; ++y1)
+                    sacc = fma(w.m[(int64_t)y0 * ny1 + y1], w.K1[(int64_t)x1 * ny1 + y1], sacc);
+                M1[o] = sacc;
+            }
+            __syncthreads();
+            for (int t = tid; t < e0 * e1; t += DD_NT) {
+                const int a0 = t / e1, a1 = t - a0 * e1;
+                const int x0 = r0 + a0;
+                const int x = x0 * nw1 + (c0 + a1);
+                double sacc = 0.0;
+                for (int y0 = 0; y0 < ny0; ++y0)
+                    sacc = fma(w.K0[(int64_t)x0 * ny0 + y0], M1[(int64_t)y0 * e1 + a1], sacc);
+                double xm = exp(w.u[x] - A) * sacc;
+                if (SX != 0.0) xm = xm + w.mu[x] * (SX / mass);
+                xout[t] = w.mu[x] > 0 ? xm : 0.0;
+            }
+        } else {
+            for (int y = tid; y < ny; y += DD_NT) {
+                const double v = vals[y];
+                const double fin = v >= b.trunc ? v : 0.0;
+                const double r = raw[y];
+                w.m[y] = r > 0 ? fin / r : 0.0;
+            }
+            __syncthreads();
+            for (int t = tid; t < e0 * e1; t += DD_NT) {
+                const int a0 = t / e1, a1 = t - a0 * e1;
+                const int x0 = r0 + a0, x1 = c0 + a1;
+                const int x = x0 * nw1 + x1;
+                double sacc = 0.0;
+                if (w.mu[x] > 0) {
+                    for (int y = 0; y < ny; ++y) {
+                        const double f = w.m[y];
+                        if (f == 0.0) continue;
+                        const int y0 = y / ny1, y1 = y - y0 * ny1;
+                        const double dd0 = w.xc0[x0] - w.yc0[y0];
+                        const double dd1 = w.xc1[x1] - w.yc1[y1];
+                        const double cost = dd0 * dd0 + dd1 * dd1;
+                        const double scv = w.alpha[x] / eps + w.beta[y] / eps + (-cost / eps);
+                        sacc += exp(scv + w.lmu[x] + w.lnu[y]) * f;
+                    }
+                }
+                double xm = sacc;
+                if (SX != 0.0) xm = xm + w.mu[x] * (SX / mass);
+                xout[t] = w.mu[x] > 0 ? xm : 0.0;
+            }
+        }
+        __syncthreads();
+    }
+
+    if (tid == 0) {
+        double* cs = b.cstat + (int64_t)c * 8;
+        cs[0] = gap;
+        cs[1] = first_gap;
+        cs[2] = (double)iters;
+        cs[3] = converged ? 1.0 : 0.0;
+        cs[4] = (double)n_clamped;
+        cs[5] = (double)newton_clamped;
+        cs[6] = (double)fallbacks;
+        cs[7] = target_miss;
+        double* c2 = b.cstat2 + (int64_t)c * 4;
+        c2[0] = (double)drift;
+        c2[1] = trunc_total;
+        c2[2] = has_m ? 1.0 : 0.0;
+        c2[3] = matrix ? 1.0 : 0.0;
+    }
+}
+
+// ---- blend scoring -----------------------------------------------------------
+
+// Old (current plan) and new (solution) window sums of one cell, and deltas.
+__global__ void __launch_bounds__(DD_NT) cell_delta_kernel(dd_geom g, dd_state s, dd_batch b,
+                                                           double* dy, double* cd) {
+    __shared__ double red[DD_NW + 1];
+    const int c = blockIdx.x;
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t* off = b.offs + (int64_t)c * 4;
+    const CellWin cw = load_win(d, b.nxw0, b.nxw1);
+    const int nmem = d[9];
+    const int32_t* mem = b.members + d[10];
+    const int ny = cw.ny, ny1 = cw.ye1;
+    const int64_t yoff = off[0];
+    const double* NEWV = b.marena + off[1] + (int64_t)5 * nmem * ny;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const int y0 = y / ny1, y1 = y - y0 * ny1;
+        const int r = cw.yo0 + y0, q = cw.yo1 + y1;
+        double yo = 0.0, yn = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            yo += boxed_at(s.ybox + (int64_t)i * 4, s.yval + (int64_t)i * s.cap, r, q);
+            yn += boxed_at(b.mbox + (int64_t)(d[10] + k) * 4, NEWV + (int64_t)k * ny, r, q);
+        }
+        dy[yoff + y] = yn - yo;
+    }
+    // t_delta, k_delta, d1_old
+    const int bs = s.block0 * s.block1;
+    double d1o = 0.0;
+    for (int k = 0; k < nmem; ++k) {
+        const int i = mem[k];
+        const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+        double p = 0.0;
+        for (int t = threadIdx.x; t < bs; t += DD_NT) {
+            const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+            const double mu = s.mu[(int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1)];
+            if (mu > 0) p += kl_term(s.x_marg[(int64_t)i * bs + t], mu);
+        }
+        d1o += block_sum(p, red);
+    }
+    if (threadIdx.x == 0) {
+        double tn = 0.0, to = 0.0, kn = 0.0, ko = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            tn += b.mstat[(int64_t)(d[10] + k) * 4 + 0];
+            kn += b.mstat[(int64_t)(d[10] + k) * 4 + 1];
+            to += s.transport[i];
+            ko += s.kl[i];
+        }
+        cd[(int64_t)c * 4 + 0] = tn - to;
+        cd[(int64_t)c * 4 + 1] = kn - ko;
+        cd[(int64_t)c * 4 + 2] = g.lam * d1o;
+        cd[(int64_t)c * 4 + 3] = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(DD_NT) blend_scatter_kernel(dd_batch b, const double* dy,
+                                                              const double* theta, double* ywork,
+                                                              int ny1g) {
+    const int c = blockIdx.x;
+    const double th = theta[c];
+    if (th == 0.0) return;
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t yoff = b.offs[(int64_t)c * 4];
+    const int ye0 = d[6], ye1 = d[8];
+    for (int y = threadIdx.x; y < ye0 * ye1; y += DD_NT) {
+        const int y0 = y / ye1, y1 = y - y0 * ye1;
+        atomicAdd(ywork + (int64_t)(d[5] + y0) * ny1g + (d[7] + y1), th * dy[yoff + y]);
+    }
+}
+
+// per-cell blend pieces: out[c*4] = theta*t_delta, theta*k_delta, d1_blend - d1_old
+__global__ void __launch_bounds__(DD_NT) blend_cell_kernel(dd_geom g, dd_state s, dd_batch b,
+                                                           const double* cd, const double* theta,
+                                                           double* pc) {
+    __shared__ double red[DD_NW + 1];
+    const int c = blockIdx.x;
+    const double th = theta[c];
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t* off = b.offs + (int64_t)c * 4;
+    const int nmem = d[9];
+    const int32_t* mem = b.members + d[10];
+    const int bs = s.block0 * s.block1;
+    double d1b = 0.0;
+    if (th != 0.0) {
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+            const double* xn = b.xarena + off[3] + (int64_t)k * bs;
+            double p = 0.0;
+            for (int t = threadIdx.x; t < bs; t += DD_NT) {
+                const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+                const double mu = s.mu[(int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1)];
+                if (mu > 0) {
+                    const double xo = s.x_marg[(int64_t)i * bs + t];
+                    p += kl_term((1.0 - th) * xo + th * xn[t], mu);
+                }
+            }
+            d1b += block_sum(p, red);
+        }
+    }
+    if (threadIdx.x == 0) {
+        pc[(int64_t)c * 4 + 0] = th != 0.0 ? th * cd[(int64_t)c * 4 + 0] : 0.0;
+        pc[(int64_t)c * 4 + 1] = th != 0.0 ? th * cd[(int64_t)c * 4 + 1] : 0.0;
+        pc[(int64_t)c * 4 + 2] = th != 0.0 ? g.lam * d1b - cd[(int64_t)c * 4 + 2] : 0.0;
+        pc[(int64_t)c * 4 + 3] = 0.0;
+    }
+}
+
+// ---- commit ---------------------------------------------------------------------
+
+__global__ void __launch_bounds__(DD_NT) cell_commit_kernel(dd_geom g, dd_state s, dd_batch b,
+                                                            const double* theta,
+                                                            double* alpha_grid, double* yrun,
+                                                            double* errs) {
+    __shared__ double red[DD_NW + 1];
+    __shared__ int redi[DD_NW + 1];
+    const int c = blockIdx.x;
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t* off = b.offs + (int64_t)c * 4;
+    const int nw0 = b.nxw0, nw1 = b.nxw1;
+    const CellWin cw = load_win(d, nw0, nw1);
+    const int j = d[0];
+    const int nmem = d[9];
+    const int32_t* mem = b.members + d[10];
+    const int ny = cw.ny, ny1 = cw.ye1, nx = cw.nx;
+    const int64_t yoff = off[0];
+    double* marena = b.marena + off[1];
+    double* OLDW = marena;                        // raw region reused: old windows
+    double* BW = marena + (int64_t)4 * nmem * ny;   // vals region reused: blended windows
+    const double* NEWV = marena + (int64_t)5 * nmem * ny;
+    const double th = theta[c];
+    const int bs = s.block0 * s.block1;
+    const int tid = threadIdx.x;
+
+    // old member windows on the cell's Y box
+    for (int k = 0; k < nmem; ++k) {
+        const int i = mem[k];
+        for (int y = tid; y < ny; y += DD_NT) {
+            const int y0 = y / ny1, y1 = y - y0 * ny1;
+            OLDW[(int64_t)k * ny + y] =
+                boxed_at(s.ybox + (int64_t)i * 4, s.yval + (int64_t)i * s.cap, cw.yo0 + y0, cw.yo1 + y1);
+        }
+    }
+    __syncthreads();
+    double added = 0.0;
+    if (th >= 1.0) {
+        added = b.cstat2[(int64_t)c * 4 + 1];
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            const int mslot = d[10] + k;
+            const int32_t* nb = b.mbox + (int64_t)mslot * 4;
+            const int n = (nb[1] > 0 && nb[3] > 0) ? nb[1] * nb[3] : 0;
+            for (int t = tid; t < n; t += DD_NT) s.yval[(int64_t)i * s.cap + t] = NEWV[(int64_t)k * ny + t];
+            if (tid < 4) s.ybox[(int64_t)i * 4 + tid] = n ? nb[tid] : 0;
+            const double* xn = b.xarena + off[3] + (int64_t)k * bs;
+            for (int t = tid; t < bs; t += DD_NT) s.x_marg[(int64_t)i * bs + t] = xn[t];
+            if (tid == 0) {
+                s.transport[i] = b.mstat[(int64_t)mslot * 4 + 0];
+                s.kl[i] = b.mstat[(int64_t)mslot * 4 + 1];
+            }
+        }
+    } else if (th > 0.0) {
+        double removed_all = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            const int mslot = d[10] + k;
+            const int32_t* nb = b.mbox + (int64_t)mslot * 4;
+            double* bw = BW + (int64_t)k * ny;
+            for (int y = tid; y < ny; y += DD_NT) {
+                const int y0 = y / ny1, y1 = y - y0 * ny1;
+                const double nv = boxed_at(nb, NEWV + (int64_t)k * ny, cw.yo0 + y0, cw.yo1 + y1);
+                bw[y] = (1.0 - th) * OLDW[(int64_t)k * ny + y] + th * nv;
+            }
+            __syncthreads();
+            int rmin = 0x7fffffff, rmax = -1, cmin = 0x7fffffff, cmax = -1;
+            double rem = 0.0;
+            for (int y = tid; y < ny; y += DD_NT) {
+                const double v = bw[y];
+                if (v >= b.trunc) {
+                    const int y0 = y / ny1, y1 = y - y0 * ny1;
+                    rmin = min(rmin, y0); rmax = max(rmax, y0);
+                    cmin = min(cmin, y1); cmax = max(cmax, y1);
+                } else {
+                    rem += v;
+                }
+            }
+            rmin = block_min_i(rmin, redi);
+            rmax = block_max_i(rmax, redi);
+            cmin = block_min_i(cmin, redi);
+            cmax = block_max_i(cmax, redi);
+            removed_all += block_sum(rem, red);
+            int ne0 = 0, ne1 = 0;
+            if (rmax >= 0) { ne0 = rmax - rmin + 1; ne1 = cmax - cmin + 1; }
+            for (int t = tid; t < ne0 * ne1; t += DD_NT) {
+                const int a0 = t / ne1, a1 = t - a0 * ne1;
+                const double v = bw[(int64_t)(rmin + a0) * ny1 + (cmin + a1)];
+                s.yval[(int64_t)i * s.cap + t] = v >= b.trunc ? v : 0.0;
+            }
+            if (tid == 0) {
+                int* ob = s.ybox + (int64_t)i * 4;
+                if (rmax >= 0) {
+                    ob[0] = cw.yo0 + rmin; ob[1] = ne0; ob[2] = cw.yo1 + cmin; ob[3] = ne1;
+                } else {
+                    ob[0] = 0; ob[1] = 0; ob[2] = 0; ob[3] = 0;
+                }
+                s.transport[i] = (1.0 - th) * s.transport[i] + th * b.mstat[(int64_t)mslot * 4 + 0];
+                s.kl[i] = (1.0 - th) * s.kl[i] + th * b.mstat[(int64_t)mslot * 4 + 1];
+            }
+            const double* xn = b.xarena + off[3] + (int64_t)k * bs;
+            for (int t = tid; t < bs; t += DD_NT)
+                s.x_marg[(int64_t)i * bs + t] = (1.0 - th) * s.x_marg[(int64_t)i * bs + t] + th * xn[t];
+            __syncthreads();
+        }
+        added = th * b.cstat2[(int64_t)c * 4 + 1] + removed_all;
+    }
+    __syncthreads();
+    // dual store
+    double* da = s.d_alpha + (int64_t)j * nx;
+    const double* al = b.alpha + (int64_t)c * nx;
+    for (int x = tid; x < nx; x += DD_NT) da[x] = al[x];
+    for (int y = tid; y < ny; y += DD_NT) s.d_beta[(int64_t)j * s.d_cap + y] = b.beta[yoff + y];
+    if (tid == 0) {
+        s.d_has[j] = 1;
+        s.d_box[(int64_t)j * 4 + 0] = cw.yo0;
+        s.d_box[(int64_t)j * 4 + 1] = cw.ye0;
+        s.d_box[(int64_t)j * 4 + 2] = cw.yo1;
+        s.d_box[(int64_t)j * 4 + 3] = cw.ye1;
+    }
+    __syncthreads();
+    // residuals of the committed state against the solution duals
+    double ye = 0.0;
+    for (int y = tid; y < ny; y += DD_NT) {
+        const int y0 = y / ny1, y1 = y - y0 * ny1;
+        const int r = cw.yo0 + y0, q = cw.yo1 + y1;
+        double yn = 0.0, yo = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            yn += boxed_at(s.ybox + (int64_t)i * 4, s.yval + (int64_t)i * s.cap, r, q);
+            yo += OLDW[(int64_t)k * ny + y];
+        }
+        if (th <= 0.0) yn = yo;
+        const double nu = s.nu[(int64_t)r * g.ny1 + q];
+        const double num = b.mdens[yoff + y] * nu;
+        ye += fabs(yn + num - exp(-b.beta[yoff + y] / g.lam) * nu);
+        if (yrun) {
+            const int64_t id = (int64_t)r * g.ny1 + q;
+            yrun[id] = fmax(yrun[id] + (yn - yo), 0.0);
+        }
+    }
+    ye = block_sum(ye, red);
+    double xe = 0.0;
+    for (int k = 0; k < nmem; ++k) {
+        const int i = mem[k];
+        const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+        const int r0 = bx[0] - cw.xo0, c0 = bx[2] - cw.xo1, e1 = bx[3];
+        double p = 0.0;
+        for (int t = tid; t < bs; t += DD_NT) {
+            const int a0 = t / e1, a1 = t - a0 * e1;
+            const int gr = bx[0] + a0, gq = bx[2] + a1;
+            const double mu = s.mu[(int64_t)gr * g.nx1 + gq];
+            const double a = al[(r0 + a0) * nw1 + (c0 + a1)];
+            if (alpha_grid) alpha_grid[(int64_t)gr * g.nx1 + gq] = a;
+            if (mu > 0) p += fabs(s.x_marg[(int64_t)i * bs + t] - exp(-a / g.lam) * mu);
+        }
+        xe += block_sum(p, red);
+    }
+    if (tid == 0) {
+        errs[(int64_t)c * 4 + 0] = xe;
+        errs[(int64_t)c * 4 + 1] = ye;
+        errs[(int64_t)c * 4 + 2] = added;
+        errs[(int64_t)c * 4 + 3] = 0.0;
+    }
+}
+
+// ---- opt strategy: derivative pieces of the 1D blend objective --------------------
+// (engine.py:473-503 g_and_h).  out[0] = sum of member terms d*log(x/mn),
+// out[1] = sum d^2/x, out[2] = sum dy*log(y/nu), out[3] = sum dy^2/y, all lam-free,
+// with x = (1-th) xo + th xn and y = clip(clip(ycur - th_cur dy, 0) + th dy, 0).
+__global__ void __launch_bounds__(DD_NT) opt_gh_kernel(dd_geom g, dd_state s, dd_batch b,
+                                                       const double* dy, int c, double th,
+                                                       double th_cur, const double* ycur,
+                                                       double* out) {
+    __shared__ double red[DD_NW + 1];
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t* off = b.offs + (int64_t)c * 4;
+    const int nmem = d[9];
+    const int32_t* mem = b.members + d[10];
+    const int bs = s.block0 * s.block1;
+    double gx = 0.0, hx = 0.0;
+    for (int k = 0; k < nmem; ++k) {
+        const int i = mem[k];
+        const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+        const double* xn = b.xarena + off[3] + (int64_t)k * bs;
+        for (int t = threadIdx.x; t < bs; t += DD_NT) {
+            const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+            const double mu = s.mu[(int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1)];
+            if (!(mu > 0)) continue;
+            const double xo = s.x_marg[(int64_t)i * bs + t];
+            const double dd = xn[t] - xo;
+            if (dd == 0.0) continue;
+            const double x = (1.0 - th) * xo + th * xn[t];
+            gx += dd * log(x / mu);
+            hx += dd * dd / x;
+        }
+    }
+    const int ye1 = d[8], ny = d[6] * d[8];
+    const int64_t yoff = off[0];
+    double gy = 0.0, hy = 0.0;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const double dv = dy[yoff + y];
+        if (dv == 0.0) continue;
+        const int y0 = y / ye1, y1 = y - y0 * ye1;
+        const int64_t id = (int64_t)(d[5] + y0) * g.ny1 + (d[7] + y1);
+        const double yb = fmax(ycur[id] - th_cur * dv, 0.0);
+        const double yv = fmax(yb + th * dv, 0.0);
+        gy += dv * log(yv / s.nu[id]);
+        hy += dv * dv / yv;
+    }
+    gx = block_sum(gx, red);
+    hx = block_sum(hx, red);
+    gy = block_sum(gy, red);
+    hy = block_sum(hy, red);
+    if (threadIdx.x == 0) { out[0] = gx; out[1] = hx; out[2] = gy; out[3] = hy; }
+}
+
+// ycur[ids of cell c] = clip(ycur + dth * dy, 0)   (BlendScorer.set_theta)
+__global__ void __launch_bounds__(DD_NT) opt_set_kernel(dd_batch b, const double* dy, int c,
+                                                        double dth, double* ycur, int ny1g) {
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t yoff = b.offs[(int64_t)c * 4];
+    const int ye1 = d[8], ny = d[6] * d[8];
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const int y0 = y / ye1, y1 = y - y0 * ye1;
+        const int64_t id = (int64_t)(d[5] + y0) * ny1g + (d[7] + y1);
+        ycur[id] = fmax(ycur[id] + dth * dy[yoff + y], 0.0);
+    }
+}
+
+}  // namespace dd
+
+// ---- host wrappers ---------------------------------------------------------------
+
+extern "C" int dd_set_error(cudaError_t e);
+
+extern "C" int64_t dd_cell_ws_size(int nw0, int nw1, int ny0, int ny1) {
+    return dd::ws_layout(nw0, nw1, ny0, ny1).total;
+}
+
+extern "C" int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream) {
+    if (b->n_cells <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int smem = b->smem_mode ? b->smem_bytes : 0;
+    static thread_local int configured = -1;
+    if (smem > configured) {
+        // opt in to the full per-block budget minus the kernel's static shared memory
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa;
+        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel);
+        if (e != cudaSuccess) return dd_set_error(e);
+        const int avail = optin - (int)fa.sharedSizeBytes;
+        if (smem > avail) return dd_set_error(cudaErrorInvalidValue);
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 avail);
+        if (e != cudaSuccess) return dd_set_error(e);
+        configured = avail;
+    }
+    dd::cell_solve_kernel<<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_cell_delta(const dd_geom* g, const dd_state* s, const dd_batch* b, double* dy,
+                             double* cd, void* stream) {
+    if (b->n_cells <= 0) return 0;
+    dd::cell_delta_kernel<<<b->n_cells, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, dy, cd);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_reduce_rows(int64_t n_rows, int width, const double* in, double* out,
+                              void* stream);
+
+extern "C" int dd_grid_kl(int64_t n, const double* y, const double* nu, int clip, double* partial,
+                          double* out, void* stream);
+
+extern "C" int dd_blend_energy(const dd_geom* g, const dd_state* s, const dd_batch* b,
+                               const double* dy, const double* cd, const double* theta,
+                               double* ywork, double* partial, double* out, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = (int64_t)g->ny0 * g->ny1;
+    cudaError_t e = cudaMemcpyAsync(ywork, b->snapshot, n * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return dd_set_error(e);
+    if (b->n_cells > 0) {
+        dd::blend_scatter_kernel<<<b->n_cells, DD_NT, 0, st>>>(*b, dy, theta, ywork, g->ny1);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
+    int rc = dd_grid_kl(n, ywork, s->nu, 1, partial, out, stream);
+    if (rc) return rc;
+    if (b->n_cells > 0) {
+        // per-cell pieces into partial + 2048.., then ordered row reduction
+        double* pc = partial + 4096;
+        dd::blend_cell_kernel<<<b->n_cells, DD_NT, 0, st>>>(*g, *s, *b, cd, theta, pc);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return dd_set_error(e);
+        rc = dd_reduce_rows(b->n_cells, 4, pc, out + 1, stream);
+        if (rc) return rc;
+    } else {
+        e = cudaMemsetAsync(out + 1, 0, 3 * sizeof(double), st);
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
+    return 0;
+}
+
+extern "C" int dd_cell_commit(const dd_geom* g, const dd_state* s, const dd_batch* b,
+                              const double* theta, double* alpha_grid, double* yrun, double* errs,
+                              void* stream) {
+    if (b->n_cells <= 0) return 0;
+    dd::cell_commit_kernel<<<b->n_cells, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, theta,
+                                                                          alpha_grid, yrun, errs);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_opt_gh(const dd_geom* g, const dd_state* s, const dd_batch* b, const double* dy,
+                         int c, double th, double th_cur, const double* ycur, double* out,
+                         void* stream) {
+    dd::opt_gh_kernel<<<1, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, dy, c, th, th_cur, ycur,
+                                                             out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy, int c, double dth,
+                          double* ycur, void* stream) {
+    dd::opt_set_kernel<<<1, DD_NT, 0, (cudaStream_t)stream>>>(*b, dy, c, dth, ycur, g->ny1);
+    return dd_set_error(cudaGetLastError());
+}

@@ -1,0 +1,157 @@
+// Shared device helpers for the domdec B200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#define DD_NT 256
+#define DD_NW (DD_NT / 32)
+
+namespace dd {
+
+constexpr double kNegInf = -__builtin_huge_val();
+constexpr double kDegenerateBetaScale = 700.0;  // sinkhorn.py:54
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_max_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block reductions (fixed tree). `red` is __shared__ double[DD_NW+1].
+// All threads of the block must call; all receive the result.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < DD_NW ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) red[DD_NW] = t;
+    }
+    __syncthreads();
+    return red[DD_NW];
+}
+__device__ __forceinline__ double block_max(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < DD_NW ? red[lane] : kNegInf;
+        t = warp_max(t);
+        if (lane == 0) red[DD_NW] = t;
+    }
+    __syncthreads();
+    return red[DD_NW];
+}
+__device__ __forceinline__ int block_min_i(int v, int* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_min_i(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < DD_NW ? red[lane] : 0x7fffffff;
+        t = warp_min_i(t);
+        if (lane == 0) red[DD_NW] = t;
+    }
+    __syncthreads();
+    return red[DD_NW];
+}
+__device__ __forceinline__ int block_max_i(int v, int* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_max_i(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < DD_NW ? red[lane] : -0x7fffffff;
+        t = warp_max_i(t);
+        if (lane == 0) red[DD_NW] = t;
+    }
+    __syncthreads();
+    return red[DD_NW];
+}
+
+// numpy.logaddexp semantics (npymath npy_logaddexp)
+__device__ __forceinline__ double logaddexp(double x, double y) {
+    if (x == y) return x + 0.693147180559945309417232121458176568;
+    const double t = x - y;
+    if (t > 0) return x + log1p(exp(-t));
+    if (t <= 0) return y + log1p(exp(t));
+    return t;  // nan
+}
+
+// scipy.special.expit
+__device__ __forceinline__ double expit(double u) { return 1.0 / (1.0 + exp(-u)); }
+
+// scipy.special.xlogy
+__device__ __forceinline__ double xlogy(double x, double y) {
+    return x == 0.0 ? 0.0 : x * log(y);
+}
+
+// Per-node KL contribution sigma*(r log r - r + 1) (measures.py:326-334)
+__device__ __forceinline__ double kl_term(double rho, double sigma) {
+    if (sigma > 0) return xlogy(rho, rho / sigma) - rho + sigma;
+    return rho > 0 ? __builtin_huge_val() : 0.0;
+}
+
+// Unbalanced Y step for one node (sinkhorn.py:230-333 restated per node).
+// Returns beta; *deg set when the node is degenerate (m == 0, z == -inf).
+__device__ __forceinline__ double newton_node(double z, double m, bool has_m, double beta0,
+                                              double eps, double lam, double tol, int max_iters,
+                                              int* deg) {
+    const double ratio = eps * lam / (eps + lam);
+    const bool fz = z > kNegInf;
+    if (!has_m || !(m > 0)) {
+        if (fz) return -ratio * z;
+        *deg = 1;
+        return lam * kDegenerateBetaScale;
+    }
+    if (!fz) return -lam * log(m);
+    const double inv_eps = 1.0 / eps, inv_lam = 1.0 / lam;
+    const double lm = log(m);
+    const double b1 = -lam * logaddexp(lm, z);
+    const double b2 = -ratio * z;
+    double lo = fmin(b1, b2) - lam;
+    double hi = fmax(b1, b2) + lam;
+    double b = fmin(fmax(beta0, lo), hi);  // np.clip
+    for (int it = 0; it < max_iters; ++it) {
+        const double w = b * inv_eps + z;
+        const double g = logaddexp(lm, w) + b * inv_lam;
+        const double gp = expit(w - lm) * inv_eps + inv_lam;
+        const double step = g / gp;
+        const bool active = (fabs(g) > tol) || (fabs(step) > 4e-16 * (1.0 + fabs(b)));
+        if (!active) break;
+        double nb = b - step;
+        if (!((nb > lo) && (nb < hi))) {
+            if (g > 0) hi = fmin(hi, b);
+            else lo = fmax(lo, b);
+            if ((nb <= lo) || (nb >= hi)) nb = 0.5 * (lo + hi);
+        }
+        b = nb;
+    }
+    return b;
+}
+
+}  // namespace dd

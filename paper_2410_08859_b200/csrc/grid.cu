@@ -1,0 +1,554 @@
+// Full-grid kernels: separable log-sum-exp sweeps, reductions, state setup.
+
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "domdec_b200.h"
+
+static thread_local char g_err[512] = "";
+
+extern "C" int dd_set_error(cudaError_t e) {
+    if (e == cudaSuccess) return 0;
+    snprintf(g_err, sizeof(g_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return -(int)e;
+}
+
+extern "C" const char* dd_last_error(void) { return g_err; }
+
+extern "C" int dd_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+extern "C" int dd_abi_version(void) { return 1; }
+
+namespace dd {
+
+// out[r][n] (or out[n][r] when transposed) =
+//   LSE_m( in[r][m] - (p0 + pd*n - (q0 + qd*m))^2 / eps )
+// Two passes (max, then sum) with exact skipping of terms whose exponent is
+// below -760 (exp underflows to exactly zero there).
+__global__ void __launch_bounds__(DD_NT) row_lse_kernel(int R, int M, int N, const double* in,
+                                                        double p0, double pd, double q0, double qd,
+                                                        double eps, double* out, int transpose) {
+    extern __shared__ double sh[];
+    double* row = sh;
+    double* qc = sh + M;
+    const int r = blockIdx.x;
+    for (int m = threadIdx.x; m < M; m += DD_NT) {
+        row[m] = in[(int64_t)r * M + m];
+        qc[m] = q0 + qd * (double)m;
+    }
+    __syncthreads();
+    const int n = blockIdx.y * DD_NT + threadIdx.x;
+    if (n >= N) return;
+    const double pc = p0 + pd * (double)n;
+    double mx = kNegInf;
+    for (int m = 0; m < M; ++m) {
+        const double d = pc - qc[m];
+        mx = fmax(mx, row[m] + (-(d * d) / eps));
+    }
+    double res;
+    if (!isfinite(mx)) {
+        res = kNegInf;
+    } else {
+        double s = 0.0;
+        for (int m = 0; m < M; ++m) {
+            const double d = pc - qc[m];
+            const double t = row[m] + (-(d * d) / eps) - mx;
+            if (t > -760.0) s += exp(t);
+        }
+        res = log(s) + mx;
+    }
+    if (transpose) out[(int64_t)n * R + r] = res;
+    else out[(int64_t)r * N + n] = res;
+}
+
+// divide == 0: out = a*s + b;  divide == 1: out = a/s + b  (b may be NULL)
+__global__ void axpb_kernel(int64_t n, const double* a, double s, const double* b, double* out,
+                            int divide) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = divide ? a[i] / s : a[i] * s;
+        out[i] = b ? t + b[i] : t;
+    }
+}
+
+__global__ void newton_global_kernel(int64_t n, const double* z, double ratio, double lam,
+                                     double* beta, int32_t* n_deg) {
+    int cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double zz = z[i];
+        if (zz > kNegInf) {
+            beta[i] = -ratio * zz;
+        } else {
+            beta[i] = lam * kDegenerateBetaScale;
+            ++cnt;
+        }
+    }
+    if (cnt && n_deg) atomicAdd(n_deg, cnt);
+}
+
+// General per-node Y step (m may be NULL = zero background).
+__global__ void newton_nodes_kernel(int64_t n, const double* z, const double* m,
+                                    const double* beta0, const double* eps, const double* lam,
+                                    double tol, int max_iters, double* beta, int32_t* n_deg) {
+    int cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int dg = 0;
+        beta[i] = newton_node(z[i], m ? m[i] : 0.0, m != nullptr, beta0 ? beta0[i] : 0.0, eps[i],
+                              lam[i], tol, max_iters, &dg);
+        cnt += dg;
+    }
+    if (cnt && n_deg) atomicAdd(n_deg, cnt);
+}
+
+constexpr int kRedBlocks = 1024;
+
+// stage 1: per-block partial sums of up to 3 quantities, partial[q*kRedBlocks + block]
+__global__ void __launch_bounds__(DD_NT) terms_kernel(int mode, int64_t n_x, int64_t n_y,
+                                                      const double* a, const double* l,
+                                                      const double* w, const double* b,
+                                                      const double* z, const double* w2, double eps,
+                                                      double lam, double* px, double* partial) {
+    __shared__ double red[DD_NW + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * DD_NT;
+    const int64_t t0 = blockIdx.x * (int64_t)DD_NT + threadIdx.x;
+    if (mode == 0) {
+        for (int64_t i = t0; i < n_x; i += stride) {
+            const double mu = w[i];
+            double p = 0.0;
+            if (mu > 0) {
+                const double al = a[i];
+                const double lr = al / eps + l[i];
+                p = mu * exp(lr);
+                const double ref = mu * exp(-al / lam);
+                s0 += p * (lr + al / lam) - p + ref;
+            }
+            if (px) px[i] = p;
+        }
+    } else if (mode == 1) {
+        for (int64_t i = t0; i < n_y; i += stride) {
+            const double nu = w2[i];
+            s0 += nu * exp(b[i] / eps + z[i]);
+            s2 += nu * (1.0 - exp(-b[i] / lam));
+        }
+        for (int64_t i = t0; i < n_x; i += stride) s1 += w[i] * (1.0 - exp(-a[i] / lam));
+    } else if (mode == 2) {
+        // KL(y | nu) with clipping at zero (a = y, w2 = nu), n_y entries
+        for (int64_t i = t0; i < n_y; i += stride) {
+            const double y = l ? fmax(a[i], 0.0) : a[i];
+            s0 += kl_term(y, w2[i]);
+        }
+    }
+    s0 = block_sum(s0, red);
+    s1 = block_sum(s1, red);
+    s2 = block_sum(s2, red);
+    if (threadIdx.x == 0) {
+        partial[blockIdx.x] = s0;
+        partial[kRedBlocks + blockIdx.x] = s1;
+        partial[2 * kRedBlocks + blockIdx.x] = s2;
+    }
+}
+
+// out[q] = sum_r in[r*width + q] in a fixed order (one block per q)
+__global__ void __launch_bounds__(DD_NT) reduce_rows_kernel(int64_t n_rows, int width,
+                                                            const double* in, double* out) {
+    __shared__ double red[DD_NW + 1];
+    const int q = blockIdx.x;
+    double s = 0.0;
+    for (int64_t r = threadIdx.x; r < n_rows; r += DD_NT) s += in[r * width + q];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) out[q] = s;
+}
+
+__global__ void __launch_bounds__(DD_NT) assemble_kernel(dd_geom g, dd_state s, double* out) {
+    const int i = blockIdx.x;
+    const int32_t* bx = s.ybox + (int64_t)i * 4;
+    const int o0 = bx[0], e0 = bx[1], o1 = bx[2], e1 = bx[3];
+    if (e0 <= 0 || e1 <= 0) return;
+    const double* v = s.yval + (int64_t)i * s.cap;
+    for (int t = threadIdx.x; t < e0 * e1; t += DD_NT) {
+        const int a0 = t / e1, a1 = t - a0 * e1;
+        atomicAdd(out + (int64_t)(o0 + a0) * g.ny1 + (o1 + a1), v[t]);
+    }
+}
+
+// per basic cell: [transport, kl, d1_i, 0]
+__global__ void __launch_bounds__(DD_NT) cell_terms_kernel(dd_geom g, dd_state s, double* pc) {
+    __shared__ double red[DD_NW + 1];
+    const int i = blockIdx.x;
+    const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+    const int bs = s.block0 * s.block1;
+    double p = 0.0;
+    for (int t = threadIdx.x; t < bs; t += DD_NT) {
+        const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+        const double mu = s.mu[(int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1)];
+        if (mu > 0) p += kl_term(s.x_marg[(int64_t)i * bs + t], mu);
+    }
+    p = block_sum(p, red);
+    if (threadIdx.x == 0) {
+        pc[(int64_t)i * 4 + 0] = s.transport[i];
+        pc[(int64_t)i * 4 + 1] = s.kl[i];
+        pc[(int64_t)i * 4 + 2] = p;
+        pc[(int64_t)i * 4 + 3] = 0.0;
+    }
+}
+
+// Product start (engine.py:234-257, cells.py:566-606)
+__global__ void __launch_bounds__(DD_NT) product_init_kernel(dd_geom g, dd_state s,
+                                                             double mu_total) {
+    __shared__ double red[DD_NW + 1];
+    const int i = blockIdx.x;
+    const int64_t ny = (int64_t)g.ny0 * g.ny1;
+    const double scale = s.basic_mass[i] / mu_total;
+    const double ratio = g.nu_total / mu_total;
+    double* v = s.yval + (int64_t)i * s.cap;
+    double mnu = 0.0, sy1a = 0.0, sy2a = 0.0, sy1b = 0.0, sy2b = 0.0, ent = 0.0;
+    for (int64_t t = threadIdx.x; t < ny; t += DD_NT) {
+        const int y0 = (int)(t / g.ny1), y1 = (int)(t - (int64_t)y0 * g.ny1);
+        const double nu = s.nu[t];
+        const double val = nu * scale;
+        v[t] = val;
+        mnu += val;
+        const double ya = g.y_org0 + g.y_dx * (double)y0;
+        const double yb = g.y_org1 + g.y_dx * (double)y1;
+        sy1a += val * ya;
+        sy2a += val * (ya * ya);
+        sy1b += val * yb;
+        sy2b += val * (yb * yb);
+        ent += xlogy(val, val / nu);
+    }
+    mnu = block_sum(mnu, red);
+    sy1a = block_sum(sy1a, red);
+    sy2a = block_sum(sy2a, red);
+    sy1b = block_sum(sy1b, red);
+    sy2b = block_sum(sy2b, red);
+    ent = block_sum(ent, red);
+    const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+    const int bs = s.block0 * s.block1;
+    double mmu = 0.0, sx1a = 0.0, sx2a = 0.0, sx1b = 0.0, sx2b = 0.0;
+    for (int t = threadIdx.x; t < bs; t += DD_NT) {
+        const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+        const int r = bx[0] + a0, q = bx[2] + a1;
+        const double mu = s.mu[(int64_t)r * g.nx1 + q];
+        s.x_marg[(int64_t)i * bs + t] = mu > 0 ? mu * ratio : 0.0;
+        if (mu > 0) {
+            const double xa = g.x_org0 + g.x_dx * (double)r;
+            const double xb = g.x_org1 + g.x_dx * (double)q;
+            mmu += mu;
+            sx1a += mu * xa;
+            sx2a += mu * (xa * xa);
+            sx1b += mu * xb;
+            sx2b += mu * (xb * xb);
+        }
+    }
+    mmu = block_sum(mmu, red);
+    sx1a = block_sum(sx1a, red);
+    sx2a = block_sum(sx2a, red);
+    sx1b = block_sum(sx1b, red);
+    sx2b = block_sum(sx2b, red);
+    if (threadIdx.x == 0) {
+        s.ybox[(int64_t)i * 4 + 0] = 0;
+        s.ybox[(int64_t)i * 4 + 1] = g.ny0;
+        s.ybox[(int64_t)i * 4 + 2] = 0;
+        s.ybox[(int64_t)i * 4 + 3] = g.ny1;
+        if (mnu == 0.0) {
+            s.transport[i] = 0.0;
+            s.kl[i] = mmu * g.nu_total;
+        } else {
+            double tr = 0.0;
+            tr += sx2a * mnu - 2.0 * sx1a * sy1a + mmu * sy2a;
+            tr += sx2b * mnu - 2.0 * sx1b * sy1b + mmu * sy2b;
+            tr /= mmu;
+            s.transport[i] = tr;
+            s.kl[i] = ent - mnu * log(mmu) - mnu + mmu * g.nu_total;
+        }
+    }
+}
+
+// Plan cut of global duals along one basic cell (engine.py:307-322).
+// pass 0: statistics + bounding box; pass 1: write truncated values.
+__global__ void __launch_bounds__(DD_NT) cut_plan_kernel(dd_geom g, dd_state s,
+                                                         const double* alpha, const double* beta,
+                                                         double trunc, double* trunc_out,
+                                                         int32_t* boxes_out) {
+    __shared__ double red[DD_NW + 1];
+    __shared__ int redi[DD_NW + 1];
+    __shared__ double xs_a[256], xs_mu[256], xs_c0[256], xs_c1[256];
+    __shared__ int xs_t[256];
+    __shared__ int n_sh;
+    const int i = blockIdx.x;
+    const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
+    const int bs = s.block0 * s.block1;
+    const double eps = g.eps;
+    if (threadIdx.x == 0) {
+        int n = 0;
+        for (int t = 0; t < bs; ++t) {
+            const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+            const int r = bx[0] + a0, q = bx[2] + a1;
+            const int64_t id = (int64_t)r * g.nx1 + q;
+            const double mu = s.mu[id];
+            if (mu > 0) {
+                xs_a[n] = alpha[id];
+                xs_mu[n] = mu;
+                xs_c0[n] = g.x_org0 + g.x_dx * (double)r;
+                xs_c1[n] = g.x_org1 + g.x_dx * (double)q;
+                xs_t[n] = t;
+                ++n;
+            }
+        }
+        n_sh = n;
+    }
+    __syncthreads();
+    const int nxn = n_sh;
+    const int64_t ny = (int64_t)g.ny0 * g.ny1;
+    double xacc[64];
+    for (int k = 0; k < 64; ++k) xacc[k] = 0.0;
+    double mass = 0.0, tr = 0.0, klp = 0.0, rem = 0.0;
+    int rmin = 0x7fffffff, rmax = -1, cmin = 0x7fffffff, cmax = -1;
+    for (int64_t t = threadIdx.x; t < ny; t += DD_NT) {
+        const int y0 = (int)(t / g.ny1), y1 = (int)(t - (int64_t)y0 * g.ny1);
+        const double yc0 = g.y_org0 + g.y_dx * (double)y0;
+        const double yc1 = g.y_org1 + g.y_dx * (double)y1;
+        const double nu = s.nu[t];
+        const double bt = beta[t];
+        double col = 0.0;
+        for (int k = 0; k < nxn; ++k) {
+            const double d0 = xs_c0[k] - yc0, d1 = xs_c1[k] - yc1;
+            const double cost = d0 * d0 + d1 * d1;
+            const double lr = (xs_a[k] + bt - cost) / eps;
+            const double blk = exp(lr) * xs_mu[k] * nu;
+            col += blk;
+            tr += cost * blk;
+            klp += blk * lr;
+            if (k < 64) xacc[k] += blk;
+        }
+        mass += col;
+        if (col >= trunc) {
+            rmin = min(rmin, y0); rmax = max(rmax, y0);
+            cmin = min(cmin, y1); cmax = max(cmax, y1);
+        } else {
+            rem += col;
+        }
+    }
+    mass = block_sum(mass, red);
+    tr = block_sum(tr, red);
+    klp = block_sum(klp, red);
+    rem = block_sum(rem, red);
+    rmin = block_min_i(rmin, redi);
+    rmax = block_max_i(rmax, redi);
+    cmin = block_min_i(cmin, redi);
+    cmax = block_max_i(cmax, redi);
+    for (int k = 0; k < bs; ++k) {
+        const double v = block_sum(k < nxn ? xacc[k] : 0.0, red);
+        if (threadIdx.x == 0) s.x_marg[(int64_t)i * bs + k] = 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0 && k < nxn) s.x_marg[(int64_t)i * bs + xs_t[k]] = v;
+        __syncthreads();
+    }
+    int ne0 = 0, ne1 = 0;
+    if (rmax >= 0) { ne0 = rmax - rmin + 1; ne1 = cmax - cmin + 1; }
+    if (threadIdx.x == 0) {
+        double mmu = 0.0;
+        for (int k = 0; k < nxn; ++k) mmu += xs_mu[k];
+        s.transport[i] = tr;
+        s.kl[i] = klp - mass + mmu * g.nu_total;
+        trunc_out[i] = rem;
+        int32_t* ob = boxes_out + (int64_t)i * 4;
+        if (rmax >= 0) { ob[0] = rmin; ob[1] = ne0; ob[2] = cmin; ob[3] = ne1; }
+        else { ob[0] = 0; ob[1] = 0; ob[2] = 0; ob[3] = 0; }
+    }
+    if (s.yval == nullptr || (int64_t)ne0 * ne1 > s.cap) return;
+    // pass 1: values inside the box
+    double* v = s.yval + (int64_t)i * s.cap;
+    for (int t = threadIdx.x; t < ne0 * ne1; t += DD_NT) {
+        const int a0 = t / ne1, a1 = t - a0 * ne1;
+        const int y0 = rmin + a0, y1 = cmin + a1;
+        const int64_t id = (int64_t)y0 * g.ny1 + y1;
+        const double yc0 = g.y_org0 + g.y_dx * (double)y0;
+        const double yc1 = g.y_org1 + g.y_dx * (double)y1;
+        const double nu = s.nu[id];
+        const double bt = beta[id];
+        double col = 0.0;
+        for (int k = 0; k < nxn; ++k) {
+            const double d0 = xs_c0[k] - yc0, d1 = xs_c1[k] - yc1;
+            const double cost = d0 * d0 + d1 * d1;
+            col += exp((xs_a[k] + bt - cost) / eps) * xs_mu[k] * nu;
+        }
+        v[t] = col >= trunc ? col : 0.0;
+    }
+    if (threadIdx.x < 4) s.ybox[(int64_t)i * 4 + threadIdx.x] = boxes_out[(int64_t)i * 4 + threadIdx.x];
+}
+
+// Seed cell duals of one partition from global duals.
+__global__ void __launch_bounds__(DD_NT) seed_duals_kernel(dd_geom g, dd_state s, int nw0, int nw1,
+                                                           const int32_t* xbox, const int32_t* ybox,
+                                                           const double* alpha, const double* beta) {
+    const int j = blockIdx.x;
+    const int32_t* xb = xbox + (int64_t)j * 4;
+    const int32_t* yb = ybox + (int64_t)j * 4;
+    const int nx = nw0 * nw1;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) {
+        const int x0 = x / nw1, x1 = x - x0 * nw1;
+        const int r = xb[0] + x0, q = xb[2] + x1;
+        double a = 0.0;
+        if (r >= 0 && r < g.nx0 && q >= 0 && q < g.nx1) a = alpha[(int64_t)r * g.nx1 + q];
+        s.d_alpha[(int64_t)j * nx + x] = a;
+    }
+    const int ny = yb[1] * yb[3];
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const int y0 = y / yb[3], y1 = y - y0 * yb[3];
+        s.d_beta[(int64_t)j * s.d_cap + y] = beta[(int64_t)(yb[0] + y0) * g.ny1 + (yb[2] + y1)];
+    }
+    if (threadIdx.x < 4) s.d_box[(int64_t)j * 4 + threadIdx.x] = yb[threadIdx.x];
+    if (threadIdx.x == 0) s.d_has[j] = 1;
+}
+
+}  // namespace dd
+
+// ---- host wrappers ------------------------------------------------------------------
+
+static int grid_blocks(int64_t n) {
+    int64_t b = (n + DD_NT - 1) / DD_NT;
+    if (b > 4096) b = 4096;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+static int row_lse(int R, int M, int N, const double* in, double p0, double pd, double q0,
+                   double qd, double eps, double* out, int transpose, cudaStream_t st) {
+    const size_t smem = (size_t)2 * M * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(dd::row_lse_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
+    dim3 grid(R, (N + DD_NT - 1) / DD_NT);
+    dd::row_lse_kernel<<<grid, DD_NT, smem, st>>>(R, M, N, in, p0, pd, q0, qd, eps, out, transpose);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_grid_lse(const dd_geom* g, const double* v, double* out, int to_x, double* work,
+                           void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if (to_x) {
+        // stage A: rows y0 of v (over y1) -> x1, stored transposed [nx1][ny0]
+        rc = row_lse(g->ny0, g->ny1, g->nx1, v, g->x_org1, g->x_dx, g->y_org1, g->y_dx, g->eps,
+                     work, 1, st);
+        if (rc) return rc;
+        // stage B: rows x1 (over y0) -> x0, stored transposed [nx0][nx1]
+        return row_lse(g->nx1, g->ny0, g->nx0, work, g->x_org0, g->x_dx, g->y_org0, g->y_dx,
+                       g->eps, out, 1, st);
+    }
+    rc = row_lse(g->nx0, g->nx1, g->ny1, v, g->y_org1, g->y_dx, g->x_org1, g->x_dx, g->eps, work,
+                 1, st);
+    if (rc) return rc;
+    return row_lse(g->ny1, g->nx0, g->ny0, work, g->y_org0, g->y_dx, g->x_org0, g->x_dx, g->eps,
+                   out, 1, st);
+}
+
+extern "C" int dd_axpb(int64_t n, const double* a, double s, const double* b, double* out,
+                       int divide, void* stream) {
+    dd::axpb_kernel<<<grid_blocks(n), DD_NT, 0, (cudaStream_t)stream>>>(n, a, s, b, out, divide);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_newton_global(int64_t n, const double* z, double ratio, double lam, double* beta,
+                                int32_t* n_deg, void* stream) {
+    dd::newton_global_kernel<<<grid_blocks(n), DD_NT, 0, (cudaStream_t)stream>>>(n, z, ratio, lam,
+                                                                                 beta, n_deg);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_newton_nodes(int64_t n, const double* z, const double* m, const double* beta0,
+                               const double* eps, const double* lam, double tol, int max_iters,
+                               double* beta, int32_t* n_deg, void* stream) {
+    dd::newton_nodes_kernel<<<grid_blocks(n), DD_NT, 0, (cudaStream_t)stream>>>(
+        n, z, m, beta0, eps, lam, tol, max_iters, beta, n_deg);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_reduce_rows(int64_t n_rows, int width, const double* in, double* out,
+                              void* stream) {
+    dd::reduce_rows_kernel<<<width, DD_NT, 0, (cudaStream_t)stream>>>(n_rows, width, in, out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_global_terms(int mode, int64_t n_x, int64_t n_y, const double* a,
+                               const double* l, const double* w, const double* b, const double* z,
+                               const double* w2, double eps, double lam, double* px,
+                               double* partial, double* sums, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    dd::terms_kernel<<<dd::kRedBlocks, DD_NT, 0, st>>>(mode, n_x, n_y, a, l, w, b, z, w2, eps, lam,
+                                                      px, partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dd_set_error(e);
+    // partial is [3][kRedBlocks] -> sums[0..2]: view it as rows of width 1 per quantity
+    for (int q = 0; q < 3; ++q) {
+        dd::reduce_rows_kernel<<<1, DD_NT, 0, st>>>(dd::kRedBlocks, 1, partial + q * dd::kRedBlocks,
+                                                   sums + q);
+    }
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_grid_kl(int64_t n, const double* y, const double* nu, int clip, double* partial,
+                          double* out, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    dd::terms_kernel<<<dd::kRedBlocks, DD_NT, 0, st>>>(2, 0, n, y, clip ? y : nullptr, nullptr,
+                                                      nullptr, nullptr, nu, 1.0, 1.0, nullptr,
+                                                      partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dd_set_error(e);
+    dd::reduce_rows_kernel<<<1, DD_NT, 0, st>>>(dd::kRedBlocks, 1, partial, out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_assemble(const dd_geom* g, const dd_state* s, double* out, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(out, 0, (size_t)g->ny0 * g->ny1 * sizeof(double), st);
+    if (e != cudaSuccess) return dd_set_error(e);
+    if (s->n_basic > 0) dd::assemble_kernel<<<s->n_basic, DD_NT, 0, st>>>(*g, *s, out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_energy_terms(const dd_geom* g, const dd_state* s, const double* y,
+                               double* partial, double* sums, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    double* pc = partial + 4096;
+    dd::cell_terms_kernel<<<s->n_basic, DD_NT, 0, st>>>(*g, *s, pc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dd_set_error(e);
+    int rc = dd_reduce_rows(s->n_basic, 4, pc, sums, stream);
+    if (rc) return rc;
+    return dd_grid_kl((int64_t)g->ny0 * g->ny1, y, s->nu, 0, partial, sums + 3, stream);
+}
+
+extern "C" int dd_product_init(const dd_geom* g, const dd_state* s, double mu_total, void* stream) {
+    dd::product_init_kernel<<<s->n_basic, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, mu_total);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_cut_plan(const dd_geom* g, const dd_state* s, const double* alpha,
+                           const double* beta, double trunc, double* trunc_out, int32_t* boxes_out,
+                           void* stream) {
+    if (s->block0 * s->block1 > 64) return -1000;
+    dd::cut_plan_kernel<<<s->n_basic, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, alpha, beta, trunc,
+                                                                       trunc_out, boxes_out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_seed_duals(const dd_geom* g, const dd_state* s, int n_comp, int nw0, int nw1,
+                             const int32_t* xbox, const int32_t* ybox, const double* alpha,
+                             const double* beta, void* stream) {
+    if (n_comp <= 0) return 0;
+    dd::seed_duals_kernel<<<n_comp, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, nw0, nw1, xbox, ybox,
+                                                                      alpha, beta);
+    return dd_set_error(cudaGetLastError());
+}
