@@ -95,7 +95,8 @@ typedef struct dd_batch {
     double* mstat;             /* [n_members_total*4] transport, kl, truncated, extra */
     double* cstat;             /* [n_cells*8] gap, first_gap, iters, conv, nclamped,
                                   newton_clamped, balance_fallbacks, target_miss */
-    double* cstat2;            /* [n_cells*4] drift_nodes, trunc_total, unused, unused */
+    double* cstat2;            /* [n_cells*4] drift_nodes, trunc_total, loop cycles,
+                                  Newton evaluations */
     int32_t smem_mode;         /* 1: workspace in shared memory */
     int32_t smem_bytes;
     /* solver configuration */
@@ -200,6 +201,21 @@ int dd_opt_gh(const dd_geom* g, const dd_state* s, const dd_batch* b, const doub
 /* ycur on cell c's window = clip(ycur + dth * dy, 0). */
 int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy, int c, double dth,
                double* ycur, void* stream);
+
+/* Multiscale refinement (SPEC multiscale.refine_plan): each fine basic cell
+ * j takes its coarse parent's Y-marginal (parent[j]; coarse boxes/slots
+ * cbox/cval with capacity ccap, coarse masses cmass, coarse nu grid nu_c of
+ * row length cny1), split by fine mu mass and, within Y, by fine nu mass;
+ * truncated at trunc (removed mass into trunc_out[j]); product-plan
+ * fragments and x-marginals.  The fine slots must hold 4x the coarse box. */
+int dd_refine(const dd_geom* g, const dd_state* s, const int32_t* parent, const int32_t* cbox,
+              const double* cval, int64_t ccap, const double* cmass, const double* nu_c,
+              int cny1, double trunc, double* trunc_out, void* stream);
+
+/* Bilinear prolongation of a cell-centred coarse field (nc0 x nc1) to the
+ * x2 finer grid (nf0 x nf1); constant beyond the outer coarse centres. */
+int dd_prolong(int nf0, int nf1, int nc0, int nc1, const double* coarse, double* fine,
+               void* stream);
 
 /* Workspace doubles one cell of the given window shape needs. */
 int64_t dd_cell_ws_size(int nw0, int nw1, int ny0, int ny1);

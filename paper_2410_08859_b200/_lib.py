@@ -19,7 +19,7 @@ EXPORTS = [
     "dd_newton_global", "dd_global_terms", "dd_cell_solve", "dd_cell_delta", "dd_blend_energy",
     "dd_cell_commit", "dd_assemble", "dd_energy_terms", "dd_product_init", "dd_cut_plan",
     "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
-    "dd_opt_set", "dd_newton_nodes",
+    "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -76,6 +76,9 @@ _SIGS = {
     "dd_grid_kl": ([i64, vp, vp, C.c_int, vp, vp, vp], C.c_int),
     "dd_opt_gh": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, C.c_int, dbl, dbl, vp,
                    vp, vp], C.c_int),
+    "dd_refine": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, i64, vp, vp, C.c_int, dbl, vp,
+                   vp], C.c_int),
+    "dd_prolong": ([C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
     "dd_newton_nodes": ([i64, vp, vp, vp, vp, vp, dbl, C.c_int, vp, vp, vp], C.c_int),
     "dd_opt_set": ([C.POINTER(Geom), C.POINTER(Batch), vp, C.c_int, dbl, vp, vp], C.c_int),
 }
@@ -105,12 +108,77 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     return h
 
 
-def lib() -> C.CDLL:
-    """The loaded library, requiring a visible CUDA device."""
+# kernels each entry point launches (used for the bench's gpu_launches count)
+KERNELS_PER_CALL = {
+    "dd_grid_lse": 2, "dd_axpb": 1, "dd_newton_global": 1, "dd_newton_nodes": 1,
+    "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_delta": 1, "dd_blend_energy": 5,
+    "dd_cell_commit": 1, "dd_assemble": 1, "dd_energy_terms": 4, "dd_product_init": 1,
+    "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
+    "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
+}
+
+
+class Tracer:
+    """Counts calls/kernel launches per entry point and times selected ones with
+    CUDA events recorded on the launching (current) stream."""
+
+    def __init__(self, timed=("dd_cell_solve", "dd_grid_lse")):
+        self.timed = set(timed)
+        self.calls: dict = {}
+        self.events: dict = {}
+
+    def launches(self) -> int:
+        return sum(KERNELS_PER_CALL.get(k, 1) * n for k, n in self.calls.items())
+
+    def times_ms(self) -> dict:
+        import torch
+        torch.cuda.synchronize()
+        out = {}
+        for k, evs in self.events.items():
+            out[k] = [a.elapsed_time(b) for a, b in evs]
+        return out
+
+
+_tracer: Tracer | None = None
+
+
+def set_tracer(t: Tracer | None) -> None:
+    global _tracer
+    _tracer = t
+
+
+class _Traced:
+    def __init__(self, h):
+        self._h = h
+
+    def __getattr__(self, name):
+        fn = getattr(self._h, name)
+        t = _tracer
+        if t is None or not name.startswith("dd_") or name in ("dd_last_error", "dd_device_count",
+                                                               "dd_abi_version", "dd_cell_ws_size"):
+            return fn
+
+        def call(*args):
+            t.calls[name] = t.calls.get(name, 0) + 1
+            if name in t.timed:
+                import torch
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record()
+                rc = fn(*args)
+                b.record()
+                t.events.setdefault(name, []).append((a, b))
+                return rc
+            return fn(*args)
+        return call
+
+
+def lib():
+    """The loaded library (traced when a Tracer is installed), requiring a CUDA device."""
     h = load()
     if h.dd_device_count() < 1:
         raise LibraryError("no CUDA device visible to libdomdec_b200 (there is no CPU fallback)")
-    return h
+    return _Traced(h) if _tracer is not None else h
 
 
 def check(rc: int) -> None:

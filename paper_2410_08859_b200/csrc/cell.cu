@@ -26,7 +26,8 @@ struct WsLayout {
     int64_t xc0, xc1, yc0, yc1;
     int64_t alpha, u, L, mu, tx, lmu;
     int64_t beta, lnu, m, ty;
-    int64_t K0, K1, mid;
+    int64_t wx, wy;
+    int64_t K0, K1, KT0, KT1, mid;
     int64_t midstride;
     int64_t total;
 };
@@ -49,11 +50,17 @@ __host__ __device__ inline WsLayout ws_layout(int nw0, int nw1, int ny0, int ny1
     w.lnu = o; o += ny;
     w.m = o; o += ny;
     w.ty = o; o += ny;
+    w.wx = o; o += nx;
+    w.wy = o; o += ny;
     w.K0 = o; o += (int64_t)nw0 * ny0;
     w.K1 = o; o += (int64_t)nw1 * ny1;
+    w.KT0 = o; o += (int64_t)nw0 * ny0;
+    w.KT1 = o; o += (int64_t)nw1 * ny1;
     int64_t ms = (int64_t)ny0 * nw1;
     const int64_t ms2 = (int64_t)nw0 * ny1;
     if (ms2 > ms) ms = ms2;
+    if (ny > ms) ms = ny;  // stage-1 weights of the X sweep
+    if (nx > ms) ms = nx;  // stage-1 weights of the Y sweep
     ms += nw0;  // row sums for the mc fragment
     w.midstride = ms;
     w.mid = o; o += 5 * ms;
@@ -65,7 +72,8 @@ struct Ws {
     double *xc0, *xc1, *yc0, *yc1;
     double *alpha, *u, *L, *mu, *tx, *lmu;
     double *beta, *lnu, *m, *ty;
-    double *K0, *K1, *mid;
+    double *wx, *wy;
+    double *K0, *K1, *KT0, *KT1, *mid;
     int64_t ms;
 };
 
@@ -75,7 +83,9 @@ __device__ inline Ws ws_bind(double* base, const WsLayout& l) {
     w.alpha = base + l.alpha; w.u = base + l.u; w.L = base + l.L; w.mu = base + l.mu;
     w.tx = base + l.tx; w.lmu = base + l.lmu;
     w.beta = base + l.beta; w.lnu = base + l.lnu; w.m = base + l.m; w.ty = base + l.ty;
-    w.K0 = base + l.K0; w.K1 = base + l.K1; w.mid = base + l.mid;
+    w.wx = base + l.wx; w.wy = base + l.wy;
+    w.K0 = base + l.K0; w.K1 = base + l.K1; w.KT0 = base + l.KT0; w.KT1 = base + l.KT1;
+    w.mid = base + l.mid;
     w.ms = l.midstride;
     return w;
 }
@@ -98,158 +108,114 @@ __device__ __forceinline__ double negsq(double a, double b, double eps) {
 // Used by the log-domain (wide-window) path.
 
 // ---- separable sweeps ------------------------------------------------------
+//
+// Both sweeps use the factorised kernel K(x,y) = K0[x0,y0] K1[x1,y1] with
+// K_a = exp(-(x_a - y_a)^2 / eps) and one global max shift of the input
+// vector (the reference's DenseKernel "matrix" form, cells.py via
+// sinkhorn.py:91-130), i.e. FMA contractions instead of per-term exp.  An
+// output whose shifted sum falls below kTiny may have lost its dominant
+// terms to underflow, so it is recomputed exactly in the log domain; every
+// other output carries all terms above 1e-308 and hence equals the
+// log-domain value to rounding.  This makes the result independent of the
+// window size (the reference switches to a fully log-domain sweep when
+// min(-c/eps) <= -700; both of its modes agree with this one to rounding).
 
-// L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (matrix or log mode).
-__device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           bool matrix, double* out, double* red) {
-    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny;
-    double lmax = kNegInf;
-    for (int y = threadIdx.x; y < ny; y += DD_NT) {
-        const double bv = w.beta[y] / eps + w.lnu[y];
-        w.ty[y] = bv;
-        lmax = fmax(lmax, bv);
+constexpr double kTiny = 1e-290;
+
+// Exact 1D log-sum-exp  log sum_k exp(v[k*stride] - (p - q[k])^2 / eps)  (two passes).
+__device__ __forceinline__ double lse1d(const double* v, int64_t stride, int n, double p,
+                                        const double* q, double eps) {
+    double mx = kNegInf;
+    for (int k = 0; k < n; ++k) mx = fmax(mx, v[k * stride] + negsq(p, q[k], eps));
+    if (!isfinite(mx)) return kNegInf;
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) {
+        const double t = v[k * stride] + negsq(p, q[k], eps) - mx;
+        if (t > -760.0) s += exp(t);
     }
-    if (matrix) {
-        double B = block_max(lmax, red);
-        if (!isfinite(B)) B = 0.0;
-        for (int y = threadIdx.x; y < ny; y += DD_NT) w.ty[y] = exp(w.ty[y] - B);
-        __syncthreads();
-        for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
-            const int y0 = o / nw1, x1 = o - y0 * nw1;
-            const double* tr = w.ty + (int64_t)y0 * ny1;
-            const double* kr = w.K1 + (int64_t)x1 * ny1;
-            double s = 0.0;
-            for (int y1 = 0; y1 < ny1; ++y1) s = fma(tr[y1], kr[y1], s);
-            w.mid[o] = s;
-        }
-        __syncthreads();
-        for (int o = threadIdx.x; o < nw0 * nw1; o += DD_NT) {
-            const int x0 = o / nw1, x1 = o - x0 * nw1;
-            const double* kr = w.K0 + (int64_t)x0 * ny0;
-            double s = 0.0;
-            for (int y0 = 0; y0 < ny0; ++y0) s = fma(kr[y0], w.mid[(int64_t)y0 * nw1 + x1], s);
-            out[o] = log(s) + B;
-        }
-        __syncthreads();
-    } else {
-        __syncthreads();
-        for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
-            const int y0 = o / nw1, x1 = o - y0 * nw1;
-            const double* tr = w.ty + (int64_t)y0 * ny1;
-            const double xc = w.xc1[x1];
-            double mx = kNegInf;
-            for (int y1 = 0; y1 < ny1; ++y1) mx = fmax(mx, tr[y1] + negsq(xc, w.yc1[y1], eps));
-            double r;
-            if (!isfinite(mx)) {
-                r = kNegInf;
-            } else {
-                double s = 0.0;
-                for (int y1 = 0; y1 < ny1; ++y1) {
-                    const double t = tr[y1] + negsq(xc, w.yc1[y1], eps) - mx;
-                    if (t > -760.0) s += exp(t);
-                }
-                r = log(s) + mx;
-            }
-            w.mid[o] = r;
-        }
-        __syncthreads();
-        for (int o = threadIdx.x; o < nw0 * nw1; o += DD_NT) {
-            const int x0 = o / nw1, x1 = o - x0 * nw1;
-            const double xc = w.xc0[x0];
-            double mx = kNegInf;
-            for (int y0 = 0; y0 < ny0; ++y0)
-                mx = fmax(mx, w.mid[(int64_t)y0 * nw1 + x1] + negsq(xc, w.yc0[y0], eps));
-            double r;
-            if (!isfinite(mx)) {
-                r = kNegInf;
-            } else {
-                double s = 0.0;
-                for (int y0 = 0; y0 < ny0; ++y0) {
-                    const double t = w.mid[(int64_t)y0 * nw1 + x1] + negsq(xc, w.yc0[y0], eps) - mx;
-                    if (t > -760.0) s += exp(t);
-                }
-                r = log(s) + mx;
-            }
-            out[o] = r;
-        }
-        __syncthreads();
-    }
+    return log(s) + mx;
 }
 
-// z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu.
+// One separable stage, in place of the reference's per-axis _lse
+// (sinkhorn.py:57-67 / 159-175):
+//   out[r][o] = log sum_k exp(in[r][k] - (p[o] - q[k])^2 / eps),  r < R, o < O, k < Kn,
+// with in row-major [R][Kn] and out row-major [R][O] (or [O][R] when tr).
+// Each row is shifted by its own max and contracted against the kernel table
+// Kt[o][k] = exp(-(p[o]-q[k])^2/eps) by FMAs; an output whose shifted sum is
+// below kTiny may have lost its dominant terms to underflow and is recomputed
+// by the exact 1D log-sum-exp.  `wts` receives exp(in - rowmax) (R*Kn),
+// `rmax` the row maxima (R).
+__device__ void lse_stage(const double* in, int R, int Kn, const double* Kt, int O,
+                          const double* p, const double* q, double eps, double* wts, double* rmax,
+                          double* out, bool tr) {
+    for (int r = threadIdx.x; r < R; r += DD_NT) {
+        double m = kNegInf;
+        for (int k = 0; k < Kn; ++k) m = fmax(m, in[(int64_t)r * Kn + k]);
+        rmax[r] = m;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < R * Kn; t += DD_NT) {
+        const int r = t / Kn;
+        const double m = rmax[r];
+        wts[t] = isfinite(m) ? exp(in[t] - m) : 0.0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < R * O; t += DD_NT) {
+        const int r = t / O, o = t - r * O;
+        const double m = rmax[r];
+        double res;
+        if (!isfinite(m)) {
+            res = kNegInf;
+        } else {
+            const double* wr = wts + (int64_t)r * Kn;
+            const double* kr = Kt + (int64_t)o * Kn;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int k = 0;
+            for (; k + 3 < Kn; k += 4) {
+                s0 = fma(wr[k], kr[k], s0);
+                s1 = fma(wr[k + 1], kr[k + 1], s1);
+                s2 = fma(wr[k + 2], kr[k + 2], s2);
+                s3 = fma(wr[k + 3], kr[k + 3], s3);
+            }
+            for (; k < Kn; ++k) s0 = fma(wr[k], kr[k], s0);
+            const double s = (s0 + s1) + (s2 + s3);
+            res = s >= kTiny ? log(s) + m : lse1d(in + (int64_t)r * Kn, 1, Kn, p[o], q, eps);
+        }
+        if (tr) out[(int64_t)o * R + r] = res;
+        else out[t] = res;
+    }
+    __syncthreads();
+}
+
+// L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (left in ty).
+// Stage 1 reduces y1 per row y0 -> T[x1][y0] (transposed), stage 2 reduces y0
+// per x1 -> out[x0][x1] (transposed back).  Scratch: mid (5 slabs of ms).
+__device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                           double* out, double* red) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) w.ty[y] = w.beta[y] / eps + w.lnu[y];
+    __syncthreads();
+    double* T = w.mid;                  // [nw1][ny0]
+    double* W = w.mid + w.ms;           // weights
+    double* RM = w.mid + 2 * w.ms;      // row maxima
+    // K1 is stored [x1][y1]: row o = x1 of length ny1 — exactly Kt for stage 1
+    lse_stage(w.ty, ny0, ny1, w.K1, nw1, w.xc1, w.yc1, eps, W, RM, T, true);
+    // stage 2: rows x1 (length ny0) against K0 [x0][y0]
+    lse_stage(T, nw1, ny0, w.K0, nw0, w.xc0, w.yc0, eps, W, RM, out, true);
+}
+
+// z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu (left in tx).
+// Needs K tables transposed ([y][x]) — stored in wx/wy-sized slabs KT0/KT1.
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           bool matrix, double* out, double* red) {
-    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
-    double lmax = kNegInf;
-    for (int x = threadIdx.x; x < nx; x += DD_NT) {
-        const double av = w.alpha[x] / eps + w.lmu[x];
-        w.tx[x] = av;
-        lmax = fmax(lmax, av);
-    }
-    if (matrix) {
-        double A = block_max(lmax, red);
-        if (!isfinite(A)) A = 0.0;
-        for (int x = threadIdx.x; x < nx; x += DD_NT) w.tx[x] = exp(w.tx[x] - A);
-        __syncthreads();
-        for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
-            const int x0 = o / ny1, y1 = o - x0 * ny1;
-            const double* tr = w.tx + (int64_t)x0 * nw1;
-            double s = 0.0;
-            for (int x1 = 0; x1 < nw1; ++x1) s = fma(tr[x1], w.K1[(int64_t)x1 * ny1 + y1], s);
-            w.mid[o] = s;
-        }
-        __syncthreads();
-        for (int o = threadIdx.x; o < ny; o += DD_NT) {
-            const int y0 = o / ny1, y1 = o - y0 * ny1;
-            double s = 0.0;
-            for (int x0 = 0; x0 < nw0; ++x0)
-                s = fma(w.K0[(int64_t)x0 * ny0 + y0], w.mid[(int64_t)x0 * ny1 + y1], s);
-            out[o] = log(s) + A;
-        }
-        __syncthreads();
-    } else {
-        __syncthreads();
-        for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
-            const int x0 = o / ny1, y1 = o - x0 * ny1;
-            const double* tr = w.tx + (int64_t)x0 * nw1;
-            const double yc = w.yc1[y1];
-            double mx = kNegInf;
-            for (int x1 = 0; x1 < nw1; ++x1) mx = fmax(mx, tr[x1] + negsq(w.xc1[x1], yc, eps));
-            double r;
-            if (!isfinite(mx)) {
-                r = kNegInf;
-            } else {
-                double s = 0.0;
-                for (int x1 = 0; x1 < nw1; ++x1) {
-                    const double t = tr[x1] + negsq(w.xc1[x1], yc, eps) - mx;
-                    if (t > -760.0) s += exp(t);
-                }
-                r = log(s) + mx;
-            }
-            w.mid[o] = r;
-        }
-        __syncthreads();
-        for (int o = threadIdx.x; o < ny; o += DD_NT) {
-            const int y0 = o / ny1, y1 = o - y0 * ny1;
-            const double yc = w.yc0[y0];
-            double mx = kNegInf;
-            for (int x0 = 0; x0 < nw0; ++x0)
-                mx = fmax(mx, w.mid[(int64_t)x0 * ny1 + y1] + negsq(w.xc0[x0], yc, eps));
-            double r;
-            if (!isfinite(mx)) {
-                r = kNegInf;
-            } else {
-                double s = 0.0;
-                for (int x0 = 0; x0 < nw0; ++x0) {
-                    const double t = w.mid[(int64_t)x0 * ny1 + y1] + negsq(w.xc0[x0], yc, eps) - mx;
-                    if (t > -760.0) s += exp(t);
-                }
-                r = log(s) + mx;
-            }
-            out[o] = r;
-        }
-        __syncthreads();
-    }
+                           double* out, double* red) {
+    const int ny0 = c.ye0, ny1 = c.ye1, nx = nw0 * nw1;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) w.tx[x] = w.alpha[x] / eps + w.lmu[x];
+    __syncthreads();
+    double* T = w.mid;                  // [ny1][nw0]
+    double* W = w.mid + w.ms;
+    double* RM = w.mid + 2 * w.ms;
+    lse_stage(w.tx, nw0, nw1, w.KT1, ny1, w.yc1, w.xc1, eps, W, RM, T, true);
+    lse_stage(T, ny1, nw0, w.KT0, ny0, w.yc0, w.xc0, eps, W, RM, out, true);
 }
 
 // Value of a boxed marginal at absolute node (r, q); zero outside.
@@ -263,7 +229,7 @@ __device__ __forceinline__ double boxed_at(const int32_t* box, const double* val
 
 // ---- the solve kernel -----------------------------------------------------
 
-__global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
+__global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
     extern __shared__ double smem[];
     __shared__ double red[DD_NW + 1];
     __shared__ int redi[DD_NW + 1];
@@ -280,7 +246,10 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
     const int32_t* mem = b.members + d[10];
     const int nx = cw.nx, ny = cw.ny, ny0 = cw.ye0, ny1 = cw.ye1;
     const WsLayout lay = ws_layout(nw0, nw1, ny0, ny1);
-    double* base = b.smem_mode ? smem : (b.work + off[2]);
+    // per-cell placement: shared memory when this cell's workspace fits the
+    // launch's dynamic allocation, else its slot of the global arena
+    const bool in_smem = b.smem_mode && lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes;
+    double* base = in_smem ? smem : (b.work + off[2]);
     const Ws w = ws_bind(base, lay);
     const double eps = g.eps, lam = g.lam;
     const double ratio = eps * lam / (eps + lam);
@@ -342,32 +311,37 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
     const int n_clamped = (int)block_sum((double)nclamp, red);
     const bool has_m = block_max_i(anym, redi) != 0;
 
-    // kernel mode (reference: DenseKernel matrix mode iff min(-c/eps) > -700)
-    const double d0 = fmax(fabs(g.x_org0 + g.x_dx * (double)cw.xo0 - (g.y_org0 + g.y_dx * (double)(cw.yo0 + ny0 - 1))),
-              fabs(g.x_org0 + g.x_dx * (double)(cw.xo0 + nw0 - 1) - (g.y_org0 + g.y_dx * (double)cw.yo0)));
-    const double d1 = fmax(fabs(g.x_org1 + g.x_dx * (double)cw.xo1 - (g.y_org1 + g.y_dx * (double)(cw.yo1 + ny1 - 1))),
-              fabs(g.x_org1 + g.x_dx * (double)(cw.xo1 + nw1 - 1) - (g.y_org1 + g.y_dx * (double)cw.yo1)));
-    const bool matrix = -((d0 * d0 + d1 * d1) / eps) > -700.0;
-    if (matrix) {
-        for (int o = tid; o < nw0 * ny0; o += DD_NT) {
-            const int x0 = o / ny0, y0 = o - x0 * ny0;
-            w.K0[o] = exp(negsq(w.xc0[x0], w.yc0[y0], eps));
-        }
-        for (int o = tid; o < nw1 * ny1; o += DD_NT) {
-            const int x1 = o / ny1, y1 = o - x1 * ny1;
-            w.K1[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps));
-        }
+    // per-axis kernel tables K_a = exp(-(x_a - y_a)^2 / eps) (entries may underflow;
+    // the sweeps recompute affected outputs exactly)
+    for (int o = tid; o < nw0 * ny0; o += DD_NT) {
+        const int x0 = o / ny0, y0 = o - x0 * ny0;
+        w.K0[o] = exp(negsq(w.xc0[x0], w.yc0[y0], eps));
+    }
+    for (int o = tid; o < nw1 * ny1; o += DD_NT) {
+        const int x1 = o / ny1, y1 = o - x1 * ny1;
+        w.K1[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps));
+    }
+    __syncthreads();
+    for (int o = tid; o < nw0 * ny0; o += DD_NT) {
+        const int y0 = o / nw0, x0 = o - y0 * nw0;
+        w.KT0[o] = w.K0[(int64_t)x0 * ny0 + y0];
+    }
+    for (int o = tid; o < nw1 * ny1; o += DD_NT) {
+        const int y1 = o / nw1, x1 = o - y1 * nw1;
+        w.KT1[o] = w.K1[(int64_t)x1 * ny1 + y1];
     }
     __syncthreads();
 
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
+    const long long t_loop0 = clock64();
+    long long newton_steps = 0;
     bool converged = false;
     bool have_first = false;
     double gap = __builtin_huge_val(), first_gap = 0.0;
     int iters = 0, newton_clamped = 0;
     const double inv_lam = 1.0 / lam;
     for (int k = 1; k <= b.max_iters; ++k) {
-        cell_lse_x(w, cw, nw0, nw1, eps, matrix, w.L, red);
+        cell_lse_x(w, cw, nw0, nw1, eps, w.L, red);
         if (k >= 2) {
             double part = 0.0;
             for (int x = tid; x < nx; x += DD_NT) {
@@ -386,12 +360,12 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
         }
         for (int x = tid; x < nx; x += DD_NT) w.alpha[x] = -ratio * w.L[x];
         __syncthreads();
-        cell_lse_y(w, cw, nw0, nw1, eps, matrix, w.ty, red);
+        cell_lse_y(w, cw, nw0, nw1, eps, w.ty, red);
         int ndeg = 0;
         for (int y = tid; y < ny; y += DD_NT) {
             int dg = 0;
             w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
-                                    b.newton_max_iters, &dg);
+                                    b.newton_max_iters, &dg, &newton_steps);
             ndeg += dg;
         }
         const int nd = (int)block_sum((double)ndeg, red);
@@ -400,7 +374,7 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
     }
     (void)inv_lam;
     if (!converged) {
-        cell_lse_x(w, cw, nw0, nw1, eps, matrix, w.L, red);
+        cell_lse_x(w, cw, nw0, nw1, eps, w.L, red);
         double part = 0.0;
         for (int x = tid; x < nx; x += DD_NT) {
             const double mu = w.mu[x];
@@ -416,6 +390,8 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
         if (!have_first) { first_gap = gap; have_first = true; }
         converged = gap / lam <= thr;
     }
+    const long long t_loop = clock64() - t_loop0;
+    const double nsteps = block_sum((double)newton_steps, red);
     // outputs: duals
     for (int x = tid; x < nx; x += DD_NT) b.alpha[(int64_t)c * nx + x] = w.alpha[x];
     for (int y = tid; y < ny; y += DD_NT) b.beta[yoff + y] = w.beta[y];
@@ -461,63 +437,64 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
         double* tc = TC + (int64_t)k * ny;
         double* tl = TL + (int64_t)k * ny;
         double* mc = MC + (int64_t)k * ny;
-        if (matrix) {
-            for (int t = tid; t < e0 * e1; t += DD_NT) {
-                const int a0 = t / e1, a1 = t - a0 * e1;
-                const int x = (r0 + a0) * nw1 + (c0 + a1);
-                w.tx[x] = exp(w.u[x] - A);
+        for (int t = tid; t < e0 * e1; t += DD_NT) {
+            const int a0 = t / e1, a1 = t - a0 * e1;
+            const int x = (r0 + a0) * nw1 + (c0 + a1);
+            w.tx[x] = exp(w.u[x] - A);
+        }
+        __syncthreads();
+        for (int o = tid; o < e0 * ny1; o += DD_NT) {
+            const int a0 = o / ny1, y1 = o - a0 * ny1;
+            const int x0 = r0 + a0;
+            const double yc = w.yc1[y1];
+            double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+            for (int a1 = 0; a1 < e1; ++a1) {
+                const int x1 = c0 + a1;
+                const int x = x0 * nw1 + x1;
+                const double dd = w.xc1[x1] - yc;
+                const double D1 = dd * dd;
+                const double wk = w.tx[x] * w.K1[(int64_t)x1 * ny1 + y1];
+                s1 += wk;
+                s2 += wk * D1;
+                s3 += wk * w.alpha[x];
+                s4 += w.mu[x] * D1;
             }
-            __syncthreads();
-            for (int o = tid; o < e0 * ny1; o += DD_NT) {
-                const int a0 = o / ny1, y1 = o - a0 * ny1;
+            M1[o] = s1; M2[o] = s2; M3[o] = s3; M4[o] = s4;
+        }
+        for (int a0 = tid; a0 < e0; a0 += DD_NT) {
+            double ssum = 0.0;
+            for (int a1 = 0; a1 < e1; ++a1) ssum += w.mu[(r0 + a0) * nw1 + c0 + a1];
+            M5[a0] = ssum;
+        }
+        __syncthreads();
+        for (int y = tid; y < ny; y += DD_NT) {
+            const int y0 = y / ny1, y1 = y - y0 * ny1;
+            const double yc = w.yc0[y0];
+            double P = 0.0, C = 0.0, Q = 0.0, MCv = 0.0;
+            for (int a0 = 0; a0 < e0; ++a0) {
                 const int x0 = r0 + a0;
-                const double yc = w.yc1[y1];
-                double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
-                for (int a1 = 0; a1 < e1; ++a1) {
-                    const int x1 = c0 + a1;
-                    const int x = x0 * nw1 + x1;
-                    const double dd = w.xc1[x1] - yc;
-                    const double D1 = dd * dd;
-                    const double wk = w.tx[x] * w.K1[(int64_t)x1 * ny1 + y1];
-                    s1 += wk;
-                    s2 += wk * D1;
-                    s3 += wk * w.alpha[x];
-                    s4 += w.mu[x] * D1;
-                }
-                M1[o] = s1; M2[o] = s2; M3[o] = s3; M4[o] = s4;
+                const double dd = w.xc0[x0] - yc;
+                const double D0 = dd * dd;
+                const double k0 = w.K0[(int64_t)x0 * ny0 + y0];
+                const int64_t o = (int64_t)a0 * ny1 + y1;
+                P += k0 * M1[o];
+                C += k0 * (D0 * M1[o] + M2[o]);
+                Q += k0 * M3[o];
+                MCv += D0 * M5[a0] + M4[o];
             }
-            for (int a0 = tid; a0 < e0; a0 += DD_NT) {
-                double ssum = 0.0;
-                for (int a1 = 0; a1 < e1; ++a1) ssum += w.mu[(r0 + a0) * nw1 + c0 + a1];
-                M5[a0] = ssum;
-            }
-            __syncthreads();
-            for (int y = tid; y < ny; y += DD_NT) {
-                const int y0 = y / ny1, y1 = y - y0 * ny1;
-                const double yc = w.yc0[y0];
-                double P = 0.0, C = 0.0, Q = 0.0, MCv = 0.0;
-                for (int a0 = 0; a0 < e0; ++a0) {
-                    const int x0 = r0 + a0;
-                    const double dd = w.xc0[x0] - yc;
-                    const double D0 = dd * dd;
-                    const double k0 = w.K0[(int64_t)x0 * ny0 + y0];
-                    const int64_t o = (int64_t)a0 * ny1 + y1;
-                    P += k0 * M1[o];
-                    C += k0 * (D0 * M1[o] + M2[o]);
-                    Q += k0 * M3[o];
-                    MCv += D0 * M5[a0] + M4[o];
-                }
+            // raw = e^{A + v} P in log form (no overflow of the scale alone);
+            // tc, tl as raw times the plan-weighted means of c and sc
+            if (P >= kTiny) {
                 const double bv = w.beta[y] / eps;
-                const double sc = exp(A + w.ty[y]);
-                raw[y] = sc * P;
-                tc[y] = sc * C;
-                tl[y] = sc * (Q / eps + bv * P - C / eps);
+                const double rv = exp(A + w.ty[y] + log(P));
+                raw[y] = rv;
+                tc[y] = rv * (C / P);
+                tl[y] = rv * ((Q / P) / eps + bv - (C / P) / eps);
                 mc[y] = MCv;
-            }
-        } else {
-            for (int y = tid; y < ny; y += DD_NT) {
-                const int y0 = y / ny1, y1 = y - y0 * ny1;
-                double P = 0.0, C = 0.0, T = 0.0, MCv = 0.0;
+            } else {
+                // exact per-entry evaluation (cells.py:357-374) where the
+                // factorised sum may have lost terms to underflow
+                double Pe = 0.0, Ce = 0.0, Te = 0.0, Me = 0.0;
                 for (int a0 = 0; a0 < e0; ++a0) {
                     const int x0 = r0 + a0;
                     const double dd0 = w.xc0[x0] - w.yc0[y0];
@@ -528,16 +505,16 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
                         const double cost = dd0 * dd0 + dd1 * dd1;
                         const double scv = w.alpha[x] / eps + w.beta[y] / eps + (-cost / eps);
                         const double pl = exp(scv + w.lmu[x] + w.lnu[y]);
-                        P += pl;
-                        C += pl * cost;
-                        T += pl * scv;
-                        MCv += cost * w.mu[x];
+                        Pe += pl;
+                        Ce += pl * cost;
+                        Te += pl * scv;
+                        Me += cost * w.mu[x];
                     }
                 }
-                raw[y] = P;
-                tc[y] = C;
-                tl[y] = T;
-                mc[y] = MCv;
+                raw[y] = Pe;
+                tc[y] = Ce;
+                tl[y] = Te;
+                mc[y] = Me;
             }
         }
         __syncthreads();
@@ -733,8 +710,9 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
             const double v = vals[y];
             const double fin = v >= b.trunc ? v : 0.0;
             const double r = raw[y];
-            const bool pos = r > 0;
-            const double f = pos ? fin / r : 0.0;
+            const double fr = r > 0 ? fin / r : 0.0;
+            const bool pos = r > 0 && isfinite(fr);
+            const double f = pos ? fr : 0.0;
             const double extra = pos ? 0.0 : fin;
             S1 += f * tc[y];
             S2 += extra * mc[y];
@@ -772,65 +750,61 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
         const double A = Ak[k];
         // f into ty (ty currently holds v = beta/eps + lnu; rebuild after)
         __syncthreads();
-        if (matrix) {
-            // gy[y] = exp(A + v[y]) f[y], staged in M3 region (size >= ny0*e1 needed for N1)
-            for (int y = tid; y < ny; y += DD_NT) {
-                const double v = vals[y];
-                const double fin = v >= b.trunc ? v : 0.0;
-                const double r = raw[y];
-                const double f = r > 0 ? fin / r : 0.0;
-                w.m[y] = f == 0.0 ? 0.0 : exp(A + w.beta[y] / eps + w.lnu[y]) * f;
-            }
-            __syncthreads();
-            for (int o = tid; o < ny0 * e1; o += DD_NT) {
-                const int y0 = o / e1, a1 = o - y0 * e1;
-                const int x1 = c0 + a1;
-                double sacc = 0.0;
-                for (int y1 = 0; y1 < ny1; ++y1)
-                    sacc = fma(w.m[(int64_t)y0 * ny1 + y1], w.K1[(int64_t)x1 * ny1 + y1], sacc);
-                M1[o] = sacc;
-            }
-            __syncthreads();
-            for (int t = tid; t < e0 * e1; t += DD_NT) {
-                const int a0 = t / e1, a1 = t - a0 * e1;
-                const int x0 = r0 + a0;
-                const int x = x0 * nw1 + (c0 + a1);
-                double sacc = 0.0;
-                for (int y0 = 0; y0 < ny0; ++y0)
-                    sacc = fma(w.K0[(int64_t)x0 * ny0 + y0], M1[(int64_t)y0 * e1 + a1], sacc);
-                double xm = exp(w.u[x] - A) * sacc;
-                if (SX != 0.0) xm = xm + w.mu[x] * (SX / mass);
-                xout[t] = w.mu[x] > 0 ? xm : 0.0;
-            }
-        } else {
-            for (int y = tid; y < ny; y += DD_NT) {
-                const double v = vals[y];
-                const double fin = v >= b.trunc ? v : 0.0;
-                const double r = raw[y];
-                w.m[y] = r > 0 ? fin / r : 0.0;
-            }
-            __syncthreads();
-            for (int t = tid; t < e0 * e1; t += DD_NT) {
-                const int a0 = t / e1, a1 = t - a0 * e1;
-                const int x0 = r0 + a0, x1 = c0 + a1;
-                const int x = x0 * nw1 + x1;
-                double sacc = 0.0;
-                if (w.mu[x] > 0) {
+        // gy[y] = exp(A + v[y] + log f[y] - G), G = max over y of the exponent
+        double gmax = kNegInf;
+        for (int y = tid; y < ny; y += DD_NT) {
+            const double v = vals[y];
+            const double fin = v >= b.trunc ? v : 0.0;
+            const double r = raw[y];
+            const double fr = r > 0 ? fin / r : 0.0;
+            const double f = (r > 0 && isfinite(fr)) ? fr : 0.0;
+            const double e = f > 0 ? A + w.beta[y] / eps + w.lnu[y] + log(f) : kNegInf;
+            w.m[y] = e;
+            gmax = fmax(gmax, e);
+        }
+        const double G = block_max(gmax, red);
+        for (int y = tid; y < ny; y += DD_NT) w.m[y] = isfinite(G) ? exp(w.m[y] - G) : 0.0;
+        __syncthreads();
+        for (int o = tid; o < ny0 * e1; o += DD_NT) {
+            const int y0 = o / e1, a1 = o - y0 * e1;
+            const int x1 = c0 + a1;
+            double sacc = 0.0;
+            for (int y1 = 0; y1 < ny1; ++y1)
+                sacc = fma(w.m[(int64_t)y0 * ny1 + y1], w.K1[(int64_t)x1 * ny1 + y1], sacc);
+            M1[o] = sacc;
+        }
+        __syncthreads();
+        for (int t = tid; t < e0 * e1; t += DD_NT) {
+            const int a0 = t / e1, a1 = t - a0 * e1;
+            const int x0 = r0 + a0;
+            const int x = x0 * nw1 + (c0 + a1);
+            double sacc = 0.0;
+            for (int y0 = 0; y0 < ny0; ++y0)
+                sacc = fma(w.K0[(int64_t)x0 * ny0 + y0], M1[(int64_t)y0 * e1 + a1], sacc);
+            double xm = 0.0;
+            if (w.mu[x] > 0) {
+                if (sacc >= kTiny) {
+                    xm = exp(w.u[x] - A + G + log(sacc));
+                } else {
+                    // exact: sum_y exp(sc + lmu + lnu) f[y]  (cells.py:436)
                     for (int y = 0; y < ny; ++y) {
-                        const double f = w.m[y];
+                        const double v = vals[y];
+                        const double fin = v >= b.trunc ? v : 0.0;
+                        const double r = raw[y];
+                        const double fr = r > 0 ? fin / r : 0.0;
+                        const double f = (r > 0 && isfinite(fr)) ? fr : 0.0;
                         if (f == 0.0) continue;
                         const int y0 = y / ny1, y1 = y - y0 * ny1;
                         const double dd0 = w.xc0[x0] - w.yc0[y0];
-                        const double dd1 = w.xc1[x1] - w.yc1[y1];
+                        const double dd1 = w.xc1[c0 + a1] - w.yc1[y1];
                         const double cost = dd0 * dd0 + dd1 * dd1;
                         const double scv = w.alpha[x] / eps + w.beta[y] / eps + (-cost / eps);
-                        sacc += exp(scv + w.lmu[x] + w.lnu[y]) * f;
+                        xm += exp(scv + w.lmu[x] + w.lnu[y]) * f;
                     }
                 }
-                double xm = sacc;
-                if (SX != 0.0) xm = xm + w.mu[x] * (SX / mass);
-                xout[t] = w.mu[x] > 0 ? xm : 0.0;
             }
+            if (SX != 0.0) xm = xm + w.mu[x] * (SX / mass);
+            xout[t] = w.mu[x] > 0 ? xm : 0.0;
         }
         __syncthreads();
     }
@@ -848,8 +822,8 @@ __global__ void __launch_bounds__(DD_NT) cell_solve_kernel(dd_geom g, dd_state s
         double* c2 = b.cstat2 + (int64_t)c * 4;
         c2[0] = (double)drift;
         c2[1] = trunc_total;
-        c2[2] = has_m ? 1.0 : 0.0;
-        c2[3] = matrix ? 1.0 : 0.0;
+        c2[2] = (double)t_loop;   // SM cycles spent in the Sinkhorn loop
+        c2[3] = nsteps;           // Newton evaluations over all nodes and iterations
     }
 }
 

@@ -120,7 +120,7 @@ __device__ __forceinline__ double kl_term(double rho, double sigma) {
 // Returns beta; *deg set when the node is degenerate (m == 0, z == -inf).
 __device__ __forceinline__ double newton_node(double z, double m, bool has_m, double beta0,
                                               double eps, double lam, double tol, int max_iters,
-                                              int* deg) {
+                                              int* deg, long long* steps = nullptr) {
     const double ratio = eps * lam / (eps + lam);
     const bool fz = z > kNegInf;
     if (!has_m || !(m > 0)) {
@@ -137,9 +137,25 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
     double hi = fmax(b1, b2) + lam;
     double b = fmin(fmax(beta0, lo), hi);  // np.clip
     for (int it = 0; it < max_iters; ++it) {
+        if (steps) ++*steps;
         const double w = b * inv_eps + z;
-        const double g = logaddexp(lm, w) + b * inv_lam;
-        const double gp = expit(w - lm) * inv_eps + inv_lam;
+        // logaddexp(lm, w) and expit(w - lm) from one exponential
+        double la, sig;
+        const double t = w - lm;
+        if (t > 0) {
+            const double e = exp(-t);
+            la = w + log1p(e);
+            sig = 1.0 / (1.0 + e);
+        } else if (t <= 0) {
+            const double e = exp(t);
+            la = (t == 0 ? w + 0.693147180559945309417232121458176568 : lm + log1p(e));
+            sig = e / (1.0 + e);
+        } else {
+            la = t;
+            sig = t;
+        }
+        const double g = la + b * inv_lam;
+        const double gp = sig * inv_eps + inv_lam;
         const double step = g / gp;
         const bool active = (fabs(g) > tol) || (fabs(step) > 4e-16 * (1.0 + fabs(b)));
         if (!active) break;

@@ -410,6 +410,153 @@ __global__ void __launch_bounds__(DD_NT) seed_duals_kernel(dd_geom g, dd_state s
     if (threadIdx.x == 0) s.d_has[j] = 1;
 }
 
+// Multiscale refinement of one fine basic cell j from its coarse parent
+// (SPEC multiscale.refine_plan): nu_j(yf) = f_j nu_i(yf/2) nu_f(yf)/nu_c(yf/2),
+// f_j = mu_f(X_j)/mu_c(X_i); truncated at `trunc`; product-plan fragments.
+struct RefineArgs {
+    const int32_t* parent;     // [n_fine] coarse cell id
+    const int32_t* cbox;       // coarse Y boxes
+    const double* cval;        // coarse slots
+    int64_t ccap;
+    const double* cmass;       // coarse basic masses
+    const double* nu_c;        // coarse nu grid
+    int32_t cny1;              // coarse Y dim 1
+    double trunc;
+    double* trunc_out;         // [n_fine]
+};
+
+__global__ void __launch_bounds__(DD_NT) refine_kernel(dd_geom g, dd_state s, RefineArgs a) {
+    __shared__ double red[DD_NW + 1];
+    __shared__ int redi[DD_NW + 1];
+    const int j = blockIdx.x;
+    const int i = a.parent[j];
+    const int32_t* cb = a.cbox + (int64_t)i * 4;
+    const double* cv = a.cval + (int64_t)i * a.ccap;
+    const double f = s.basic_mass[j] / a.cmass[i];
+    const int fo0 = 2 * cb[0], fe0 = 2 * cb[1], fo1 = 2 * cb[2], fe1 = 2 * cb[3];
+    const int n = fe0 * fe1;
+    // pass 0: bounding box and removed mass
+    int rmin = 0x7fffffff, rmax = -1, cmin = 0x7fffffff, cmax = -1;
+    double rem = 0.0;
+    for (int t = threadIdx.x; t < n; t += DD_NT) {
+        const int a0 = t / fe1, a1 = t - a0 * fe1;
+        const int yf0 = fo0 + a0, yf1 = fo1 + a1;
+        const int yc0 = yf0 >> 1, yc1 = yf1 >> 1;
+        const double vc = cv[(int64_t)(yc0 - cb[0]) * cb[3] + (yc1 - cb[2])];
+        const double v = f * vc * (s.nu[(int64_t)yf0 * g.ny1 + yf1] / a.nu_c[(int64_t)yc0 * a.cny1 + yc1]);
+        if (v >= a.trunc) {
+            rmin = min(rmin, a0); rmax = max(rmax, a0); cmin = min(cmin, a1); cmax = max(cmax, a1);
+        } else {
+            rem += v;
+        }
+    }
+    rmin = block_min_i(rmin, redi);
+    rmax = block_max_i(rmax, redi);
+    cmin = block_min_i(cmin, redi);
+    cmax = block_max_i(cmax, redi);
+    rem = block_sum(rem, red);
+    int ne0 = 0, ne1 = 0;
+    if (rmax >= 0) { ne0 = rmax - rmin + 1; ne1 = cmax - cmin + 1; }
+    double* out = s.yval + (int64_t)j * s.cap;
+    double mnu = 0.0, sy1a = 0.0, sy2a = 0.0, sy1b = 0.0, sy2b = 0.0, ent = 0.0;
+    for (int t = threadIdx.x; t < ne0 * ne1; t += DD_NT) {
+        const int a0 = t / ne1, a1 = t - a0 * ne1;
+        const int yf0 = fo0 + rmin + a0, yf1 = fo1 + cmin + a1;
+        const int yc0 = yf0 >> 1, yc1 = yf1 >> 1;
+        const double vc = cv[(int64_t)(yc0 - cb[0]) * cb[3] + (yc1 - cb[2])];
+        const double nu = s.nu[(int64_t)yf0 * g.ny1 + yf1];
+        double v = f * vc * (nu / a.nu_c[(int64_t)yc0 * a.cny1 + yc1]);
+        v = v >= a.trunc ? v : 0.0;
+        out[t] = v;
+        mnu += v;
+        const double ya = g.y_org0 + g.y_dx * (double)yf0;
+        const double yb = g.y_org1 + g.y_dx * (double)yf1;
+        sy1a += v * ya;
+        sy2a += v * (ya * ya);
+        sy1b += v * yb;
+        sy2b += v * (yb * yb);
+        ent += xlogy(v, v / nu);
+    }
+    mnu = block_sum(mnu, red);
+    sy1a = block_sum(sy1a, red);
+    sy2a = block_sum(sy2a, red);
+    sy1b = block_sum(sy1b, red);
+    sy2b = block_sum(sy2b, red);
+    ent = block_sum(ent, red);
+    const int32_t* bx = s.basic_xbox + (int64_t)j * 4;
+    const int bs = s.block0 * s.block1;
+    double mmu = 0.0, sx1a = 0.0, sx2a = 0.0, sx1b = 0.0, sx2b = 0.0;
+    for (int t = threadIdx.x; t < bs; t += DD_NT) {
+        const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+        const int r = bx[0] + a0, q = bx[2] + a1;
+        const double mu = s.mu[(int64_t)r * g.nx1 + q];
+        if (mu > 0) {
+            const double xa = g.x_org0 + g.x_dx * (double)r;
+            const double xb = g.x_org1 + g.x_dx * (double)q;
+            mmu += mu;
+            sx1a += mu * xa;
+            sx2a += mu * (xa * xa);
+            sx1b += mu * xb;
+            sx2b += mu * (xb * xb);
+        }
+    }
+    mmu = block_sum(mmu, red);
+    sx1a = block_sum(sx1a, red);
+    sx2a = block_sum(sx2a, red);
+    sx1b = block_sum(sx1b, red);
+    sx2b = block_sum(sx2b, red);
+    for (int t = threadIdx.x; t < bs; t += DD_NT) {
+        const int a0 = t / bx[3], a1 = t - a0 * bx[3];
+        const double mu = s.mu[(int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1)];
+        s.x_marg[(int64_t)j * bs + t] = mu > 0 ? mu * (mnu / mmu) : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        int32_t* ob = s.ybox + (int64_t)j * 4;
+        if (rmax >= 0) { ob[0] = fo0 + rmin; ob[1] = ne0; ob[2] = fo1 + cmin; ob[3] = ne1; }
+        else { ob[0] = 0; ob[1] = 0; ob[2] = 0; ob[3] = 0; }
+        a.trunc_out[j] = rem;
+        if (mnu == 0.0) {
+            s.transport[j] = 0.0;
+            s.kl[j] = mmu * g.nu_total;
+        } else {
+            double tr = sx2a * mnu - 2.0 * sx1a * sy1a + mmu * sy2a;
+            tr += sx2b * mnu - 2.0 * sx1b * sy1b + mmu * sy2b;
+            s.transport[j] = tr / mmu;
+            s.kl[j] = ent - mnu * log(mmu) - mnu + mmu * g.nu_total;
+        }
+    }
+}
+
+// Prolongation of a coarse cell-centred grid field to the fine grid (x2 per
+// axis): bilinear in the coarse node positions, constant beyond the outer
+// coarse centres.  Axes of length 1 (1D embedding) are copied.
+__global__ void prolong_kernel(int nf0, int nf1, int nc0, int nc1, const double* c, double* f) {
+    const int64_t n = (int64_t)nf0 * nf1;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(t / nf1), q = (int)(t - (int64_t)r * nf1);
+        int i0 = 0, i1 = 0, j0 = 0, j1 = 0;
+        double w0 = 0.0, w1 = 0.0;
+        if (nc0 > 1) {
+            const double p = 0.5 * (double)r - 0.25;   // coarse index of fine centre r
+            const double pc = fmin(fmax(p, 0.0), (double)(nc0 - 1));
+            i0 = min((int)floor(pc), nc0 - 2);
+            i1 = i0 + 1;
+            w0 = pc - (double)i0;
+        }
+        if (nc1 > 1) {
+            const double p = 0.5 * (double)q - 0.25;
+            const double pc = fmin(fmax(p, 0.0), (double)(nc1 - 1));
+            j0 = min((int)floor(pc), nc1 - 2);
+            j1 = j0 + 1;
+            w1 = pc - (double)j0;
+        }
+        const double c00 = c[(int64_t)i0 * nc1 + j0], c01 = c[(int64_t)i0 * nc1 + j1];
+        const double c10 = c[(int64_t)i1 * nc1 + j0], c11 = c[(int64_t)i1 * nc1 + j1];
+        f[t] = (1.0 - w0) * ((1.0 - w1) * c00 + w1 * c01) + w0 * ((1.0 - w1) * c10 + w1 * c11);
+    }
+}
+
 }  // namespace dd
 
 // ---- host wrappers ------------------------------------------------------------------
@@ -550,5 +697,23 @@ extern "C" int dd_seed_duals(const dd_geom* g, const dd_state* s, int n_comp, in
     if (n_comp <= 0) return 0;
     dd::seed_duals_kernel<<<n_comp, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, nw0, nw1, xbox, ybox,
                                                                       alpha, beta);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_refine(const dd_geom* g, const dd_state* s, const int32_t* parent,
+                         const int32_t* cbox, const double* cval, int64_t ccap, const double* cmass,
+                         const double* nu_c, int cny1, double trunc, double* trunc_out,
+                         void* stream) {
+    if (s->n_basic <= 0) return 0;
+    dd::RefineArgs a{parent, cbox, cval, ccap, cmass, nu_c, cny1, trunc, trunc_out};
+    dd::refine_kernel<<<s->n_basic, DD_NT, 0, (cudaStream_t)stream>>>(*g, *s, a);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd_prolong(int nf0, int nf1, int nc0, int nc1, const double* coarse, double* fine,
+                          void* stream) {
+    const int64_t n = (int64_t)nf0 * nf1;
+    dd::prolong_kernel<<<grid_blocks(n), DD_NT, 0, (cudaStream_t)stream>>>(nf0, nf1, nc0, nc1,
+                                                                          coarse, fine);
     return dd_set_error(cudaGetLastError());
 }

@@ -50,8 +50,12 @@ __all__ = [
 ]
 
 STRATEGY_KINDS = ("sequential", "safe", "fast", "swift", "opt", "staggered")
-SMEM_LIMIT = 220 * 1024   # dynamic shared memory budget per CTA (227 KB opt-in on sm_100a,
-                          # minus the solve kernel's ~3 KB of static shared memory)
+import os as _os
+
+# dynamic shared memory budget per CTA (227 KB opt-in on sm_100a minus the solve
+# kernel's ~3 KB of static shared memory); DD_FORCE_GLOBAL_WS=1 forces the
+# global-memory workspace path (used by the tests to cover it)
+SMEM_LIMIT = 0 if _os.environ.get("DD_FORCE_GLOBAL_WS") == "1" else 220 * 1024
 MAX_MEMBERS = 64
 
 
@@ -474,8 +478,8 @@ def _ws_total(nw0: int, nw1: int, ny0: np.ndarray, ny1: np.ndarray) -> np.ndarra
     """dd_cell_ws_size, vectorized (mirrors ws_layout in csrc/cell.cu)."""
     nx = nw0 * nw1
     ny = ny0 * ny1
-    ms = np.maximum(ny0 * nw1, nw0 * ny1) + nw0
-    return nw0 + nw1 + ny0 + ny1 + 6 * nx + 4 * ny + nw0 * ny0 + nw1 * ny1 + 5 * ms
+    ms = np.maximum(np.maximum(np.maximum(ny0 * nw1, nw0 * ny1), ny), nx) + nw0
+    return nw0 + nw1 + ny0 + ny1 + 7 * nx + 5 * ny + 2 * (nw0 * ny0 + nw1 * ny1) + 5 * ms
 
 
 class _Batch:
@@ -506,9 +510,13 @@ class _Batch:
         moff = np.concatenate([[0], np.cumsum(6 * nmem * ny)[:-1]]).astype(np.int64)
         xoff = np.concatenate([[0], np.cumsum(nmem * st.bs)[:-1]]).astype(np.int64)
         ws = _ws_total(pt.nw0, pt.nw1, ny0, ny1).astype(np.int64)
-        smem_bytes = int(ws.max()) * 8
-        smem_mode = smem_bytes <= SMEM_LIMIT
-        woff = np.concatenate([[0], np.cumsum(ws)[:-1]]).astype(np.int64)
+        fits = ws * 8 <= SMEM_LIMIT
+        # cells whose workspace fits run in shared memory (sized for the largest
+        # of them); the rest get global-arena slots
+        smem_bytes = int(ws[fits].max()) * 8 if fits.any() else 0
+        smem_mode = bool(fits.any())
+        gws = np.where(fits, 0, ws)
+        woff = np.concatenate([[0], np.cumsum(gws)[:-1]]).astype(np.int64)
         desc = np.zeros((n, 12), dtype=np.int32)
         desc[:, 0] = ids
         desc[:, 1:5] = pt.xbox[ids]
@@ -536,7 +544,7 @@ class _Batch:
         self.beta = B.get("beta", tot_y, f64)
         self.mdens = B.get("mdens", tot_y, f64)
         self.marena = B.get("marena", tot_m, f64)
-        self.work = B.get("work", 1 if smem_mode else int(ws.sum()), f64)
+        self.work = B.get("work", int(gws.sum()) + 1, f64)
         self.xarena = B.get("xarena", tot_mem * st.bs, f64)
         self.mbox = B.get("mbox", tot_mem * 4, i32)
         self.mstat = B.get("mstat", tot_mem * 4, f64)
@@ -828,10 +836,21 @@ class IterationStats:
     balance_target_miss: float = 0.0
     nu_j_drift_nodes: int = 0
     cell_iterations: int = 0
+    cell_flops: float = 0.0
+
+
+def cell_lse_flops(nw0: int, nw1: int, ny0, ny1):
+    """Algorithmic FLOPs of one Sinkhorn iteration of a cell: the four separable
+    contractions (2 per FMA) of the X and Y sweeps."""
+    nx = nw0 * nw1
+    return 2.0 * (ny0 * nw1 * ny1 + nx * ny0 + nw0 * ny1 * nw1 + ny0 * ny1 * nw0)
 
 
 def _absorb(stats: IterationStats, batch: _Batch) -> None:
     c1, c2 = batch.stats()
+    fl = cell_lse_flops(batch.pt.nw0, batch.pt.nw1, batch.ybox[:, 1].astype(np.float64),
+                        batch.ybox[:, 3].astype(np.float64))
+    stats.cell_flops += float((c1[:, 2] * fl).sum())
     stats.entry_gap += float(c1[:, 1].sum())
     stats.balance_fallbacks += int(c1[:, 6].sum())
     stats.newton_clamped = max(stats.newton_clamped, int(c1[:, 5].max(initial=0)))
@@ -975,7 +994,8 @@ def domdec_solve(problem: TransportProblem, partitions: Decomposition,
     timings = {"assemble": 0.0, "solve": 0.0, "score": 0.0, "commit": 0.0, "total": 0.0}
     diag = {"balance_fallbacks": 0, "safe_fallbacks": 0, "nonconverged_cells": 0,
             "newton_clamped": 0, "nu_minus_clamped": 0, "balance_target_miss": 0.0,
-            "nu_j_drift_nodes": 0, "cell_iterations": 0, "strategy": strategy.kind,
+            "nu_j_drift_nodes": 0, "cell_iterations": 0, "cell_flops": 0.0,
+            "strategy": strategy.kind,
             "leniency": strategy.leniency, "delta": config.delta}
     converged = False
     last_gap = float("inf")
@@ -1009,6 +1029,7 @@ def domdec_solve(problem: TransportProblem, partitions: Decomposition,
                     "nu_minus_clamped", "nu_j_drift_nodes"):
             diag[key] += getattr(stats, key)
         diag["cell_iterations"] += stats.cell_iterations
+        diag["cell_flops"] += stats.cell_flops
         diag["newton_clamped"] = max(diag["newton_clamped"], stats.newton_clamped)
         diag["balance_target_miss"] = max(diag["balance_target_miss"], stats.balance_target_miss)
         if last_gap / lam <= config.delta * mu_total:
