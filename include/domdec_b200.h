@@ -105,6 +105,7 @@ typedef struct dd_batch {
     int32_t newton_max_iters;
     double newton_tol;
     double trunc;
+    double* lnuw;              /* y arena: log nu on each cell window (kernel scratch) */
 } dd_batch;
 
 const char* dd_last_error(void);

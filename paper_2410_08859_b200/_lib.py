@@ -47,7 +47,7 @@ class Batch(C.Structure):
                 ("xarena", vp), ("mbox", vp), ("mstat", vp), ("cstat", vp), ("cstat2", vp),
                 ("smem_mode", i32), ("smem_bytes", i32),
                 ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
-                ("newton_tol", dbl), ("trunc", dbl)]
+                ("newton_tol", dbl), ("trunc", dbl), ("lnuw", vp)]
 
 
 _SIGS = {

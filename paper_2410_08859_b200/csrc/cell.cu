@@ -24,14 +24,16 @@ struct CellWin {
 // Workspace layout (doubles), identical on host and device.
 struct WsLayout {
     int64_t xc0, xc1, yc0, yc1;
-    int64_t alpha, u, L, mu, tx, lmu;
-    int64_t beta, lnu, m, ty;
-    int64_t wx, wy;
-    int64_t K0, K1, KT0, KT1, mid;
+    int64_t alpha, u, L, mu, tx, lmu, wx;
+    int64_t beta, ty, wy;
+    int64_t K0, K1, mid, rmax;
     int64_t midstride;
     int64_t total;
 };
 
+// Per-cell workspace: coordinates, 7 X-window arrays, 3 Y-window arrays (beta,
+// bv/z, sweep weights), the two per-axis kernel tables and the stage scratch.
+// The read-only Y arrays (log nu, background density m) stay in global memory.
 __host__ __device__ inline WsLayout ws_layout(int nw0, int nw1, int ny0, int ny1) {
     WsLayout w;
     const int64_t nx = (int64_t)nw0 * nw1, ny = (int64_t)ny0 * ny1;
@@ -46,34 +48,32 @@ __host__ __device__ inline WsLayout ws_layout(int nw0, int nw1, int ny0, int ny1
     w.mu = o; o += nx;
     w.tx = o; o += nx;
     w.lmu = o; o += nx;
-    w.beta = o; o += ny;
-    w.lnu = o; o += ny;
-    w.m = o; o += ny;
-    w.ty = o; o += ny;
     w.wx = o; o += nx;
+    w.beta = o; o += ny;
+    w.ty = o; o += ny;
     w.wy = o; o += ny;
     w.K0 = o; o += (int64_t)nw0 * ny0;
     w.K1 = o; o += (int64_t)nw1 * ny1;
-    w.KT0 = o; o += (int64_t)nw0 * ny0;
-    w.KT1 = o; o += (int64_t)nw1 * ny1;
     int64_t ms = (int64_t)ny0 * nw1;
     const int64_t ms2 = (int64_t)nw0 * ny1;
     if (ms2 > ms) ms = ms2;
-    if (ny > ms) ms = ny;  // stage-1 weights of the X sweep
-    if (nx > ms) ms = nx;  // stage-1 weights of the Y sweep
-    ms += nw0;  // row sums for the mc fragment
     w.midstride = ms;
     w.mid = o; o += 5 * ms;
+    int64_t rm = ny0 > ny1 ? ny0 : ny1;
+    if (nw0 > rm) rm = nw0;
+    if (nw1 > rm) rm = nw1;
+    w.rmax = o; o += rm;
     w.total = o;
     return w;
 }
 
 struct Ws {
     double *xc0, *xc1, *yc0, *yc1;
-    double *alpha, *u, *L, *mu, *tx, *lmu;
-    double *beta, *lnu, *m, *ty;
-    double *wx, *wy;
-    double *K0, *K1, *KT0, *KT1, *mid;
+    double *alpha, *u, *L, *mu, *tx, *lmu, *wx;
+    double *beta, *ty, *wy;
+    double *K0, *K1, *mid, *rmax;
+    const double* lnu;   // global: log nu on the window (contiguous copy)
+    double* m;           // global: background density on the window
     int64_t ms;
 };
 
@@ -81,11 +81,12 @@ __device__ inline Ws ws_bind(double* base, const WsLayout& l) {
     Ws w;
     w.xc0 = base + l.xc0; w.xc1 = base + l.xc1; w.yc0 = base + l.yc0; w.yc1 = base + l.yc1;
     w.alpha = base + l.alpha; w.u = base + l.u; w.L = base + l.L; w.mu = base + l.mu;
-    w.tx = base + l.tx; w.lmu = base + l.lmu;
-    w.beta = base + l.beta; w.lnu = base + l.lnu; w.m = base + l.m; w.ty = base + l.ty;
-    w.wx = base + l.wx; w.wy = base + l.wy;
-    w.K0 = base + l.K0; w.K1 = base + l.K1; w.KT0 = base + l.KT0; w.KT1 = base + l.KT1;
-    w.mid = base + l.mid;
+    w.tx = base + l.tx; w.lmu = base + l.lmu; w.wx = base + l.wx;
+    w.beta = base + l.beta; w.ty = base + l.ty; w.wy = base + l.wy;
+    w.K0 = base + l.K0; w.K1 = base + l.K1;
+    w.mid = base + l.mid; w.rmax = base + l.rmax;
+    w.lnu = nullptr;
+    w.m = nullptr;
     w.ms = l.midstride;
     return w;
 }
@@ -145,9 +146,9 @@ __device__ __forceinline__ double lse1d(const double* v, int64_t stride, int n, 
 // below kTiny may have lost its dominant terms to underflow and is recomputed
 // by the exact 1D log-sum-exp.  `wts` receives exp(in - rowmax) (R*Kn),
 // `rmax` the row maxima (R).
-__device__ void lse_stage(const double* in, int R, int Kn, const double* Kt, int O,
-                          const double* p, const double* q, double eps, double* wts, double* rmax,
-                          double* out, bool tr) {
+__device__ void lse_stage(const double* in, int R, int Kn, const double* Kt, int so, int sk,
+                          int O, const double* p, const double* q, double eps, double* wts,
+                          double* rmax, double* out, bool tr) {
     for (int r = threadIdx.x; r < R; r += DD_NT) {
         double m = kNegInf;
         for (int k = 0; k < Kn; ++k) m = fmax(m, in[(int64_t)r * Kn + k]);
@@ -168,16 +169,16 @@ __device__ void lse_stage(const double* in, int R, int Kn, const double* Kt, int
             res = kNegInf;
         } else {
             const double* wr = wts + (int64_t)r * Kn;
-            const double* kr = Kt + (int64_t)o * Kn;
+            const double* kr = Kt + (int64_t)o * so;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
             int k = 0;
             for (; k + 3 < Kn; k += 4) {
-                s0 = fma(wr[k], kr[k], s0);
-                s1 = fma(wr[k + 1], kr[k + 1], s1);
-                s2 = fma(wr[k + 2], kr[k + 2], s2);
-                s3 = fma(wr[k + 3], kr[k + 3], s3);
+                s0 = fma(wr[k], kr[(int64_t)k * sk], s0);
+                s1 = fma(wr[k + 1], kr[(int64_t)(k + 1) * sk], s1);
+                s2 = fma(wr[k + 2], kr[(int64_t)(k + 2) * sk], s2);
+                s3 = fma(wr[k + 3], kr[(int64_t)(k + 3) * sk], s3);
             }
-            for (; k < Kn; ++k) s0 = fma(wr[k], kr[k], s0);
+            for (; k < Kn; ++k) s0 = fma(wr[k], kr[(int64_t)k * sk], s0);
             const double s = (s0 + s1) + (s2 + s3);
             res = s >= kTiny ? log(s) + m : lse1d(in + (int64_t)r * Kn, 1, Kn, p[o], q, eps);
         }
@@ -189,23 +190,19 @@ __device__ void lse_stage(const double* in, int R, int Kn, const double* Kt, int
 
 // L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (left in ty).
 // Stage 1 reduces y1 per row y0 -> T[x1][y0] (transposed), stage 2 reduces y0
-// per x1 -> out[x0][x1] (transposed back).  Scratch: mid (5 slabs of ms).
+// per x1 -> out[x0][x1].  K1 is [x1][y1], K0 is [x0][y0].
 __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double* out, double* red) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny;
     for (int y = threadIdx.x; y < ny; y += DD_NT) w.ty[y] = w.beta[y] / eps + w.lnu[y];
     __syncthreads();
     double* T = w.mid;                  // [nw1][ny0]
-    double* W = w.mid + w.ms;           // weights
-    double* RM = w.mid + 2 * w.ms;      // row maxima
-    // K1 is stored [x1][y1]: row o = x1 of length ny1 — exactly Kt for stage 1
-    lse_stage(w.ty, ny0, ny1, w.K1, nw1, w.xc1, w.yc1, eps, W, RM, T, true);
-    // stage 2: rows x1 (length ny0) against K0 [x0][y0]
-    lse_stage(T, nw1, ny0, w.K0, nw0, w.xc0, w.yc0, eps, W, RM, out, true);
+    double* W = w.mid + w.ms;           // stage-2 weights
+    lse_stage(w.ty, ny0, ny1, w.K1, ny1, 1, nw1, w.xc1, w.yc1, eps, w.wy, w.rmax, T, true);
+    lse_stage(T, nw1, ny0, w.K0, ny0, 1, nw0, w.xc0, w.yc0, eps, W, w.rmax, out, true);
 }
 
 // z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu (left in tx).
-// Needs K tables transposed ([y][x]) — stored in wx/wy-sized slabs KT0/KT1.
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double* out, double* red) {
     const int ny0 = c.ye0, ny1 = c.ye1, nx = nw0 * nw1;
@@ -213,9 +210,8 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     __syncthreads();
     double* T = w.mid;                  // [ny1][nw0]
     double* W = w.mid + w.ms;
-    double* RM = w.mid + 2 * w.ms;
-    lse_stage(w.tx, nw0, nw1, w.KT1, ny1, w.yc1, w.xc1, eps, W, RM, T, true);
-    lse_stage(T, ny1, nw0, w.KT0, ny0, w.yc0, w.xc0, eps, W, RM, out, true);
+    lse_stage(w.tx, nw0, nw1, w.K1, 1, ny1, ny1, w.yc1, w.xc1, eps, w.wx, w.rmax, T, true);
+    lse_stage(T, ny1, nw0, w.K0, 1, ny0, ny0, w.yc0, w.xc0, eps, W, w.rmax, out, true);
 }
 
 // Value of a boxed marginal at absolute node (r, q); zero outside.
@@ -229,7 +225,7 @@ __device__ __forceinline__ double boxed_at(const int32_t* box, const double* val
 
 // ---- the solve kernel -----------------------------------------------------
 
-__global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
+__global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
     extern __shared__ double smem[];
     __shared__ double red[DD_NW + 1];
     __shared__ int redi[DD_NW + 1];
@@ -250,7 +246,9 @@ __global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_stat
     // launch's dynamic allocation, else its slot of the global arena
     const bool in_smem = b.smem_mode && lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes;
     double* base = in_smem ? smem : (b.work + off[2]);
-    const Ws w = ws_bind(base, lay);
+    Ws w = ws_bind(base, lay);
+    w.lnu = b.lnuw + off[0];
+    w.m = b.mdens + off[0];
     const double eps = g.eps, lam = g.lam;
     const double ratio = eps * lam / (eps + lam);
     const int tid = threadIdx.x;
@@ -293,7 +291,7 @@ __global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_stat
         const int r = cw.yo0 + y0, q = cw.yo1 + y1;
         const int64_t id = (int64_t)r * g.ny1 + q;
         const double nu = s.nu[id];
-        w.lnu[y] = s.log_nu[id];
+        b.lnuw[yoff + y] = s.log_nu[id];
         double cs = 0.0;
         for (int k = 0; k < nmem; ++k) {
             const int i = mem[k];
@@ -303,7 +301,6 @@ __global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_stat
         const double diff = pw - cs;
         if (diff < -1e-12 * fmax(pw, cs)) ++nclamp;
         const double mm = fmax(diff, 0.0) / nu;
-        w.m[y] = mm;
         b.mdens[yoff + y] = mm;
         if (mm != 0.0) anym = 1;
         w.beta[y] = has_dual ? boxed_at(dbox, dbeta, r, q) : 0.0;
@@ -322,16 +319,6 @@ __global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_stat
         w.K1[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps));
     }
     __syncthreads();
-    for (int o = tid; o < nw0 * ny0; o += DD_NT) {
-        const int y0 = o / nw0, x0 = o - y0 * nw0;
-        w.KT0[o] = w.K0[(int64_t)x0 * ny0 + y0];
-    }
-    for (int o = tid; o < nw1 * ny1; o += DD_NT) {
-        const int y1 = o / nw1, x1 = o - y1 * nw1;
-        w.KT1[o] = w.K1[(int64_t)x1 * ny1 + y1];
-    }
-    __syncthreads();
-
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
     const long long t_loop0 = clock64();
     long long newton_steps = 0;
@@ -759,18 +746,18 @@ __global__ void __launch_bounds__(DD_NT, 2) cell_solve_kernel(dd_geom g, dd_stat
             const double fr = r > 0 ? fin / r : 0.0;
             const double f = (r > 0 && isfinite(fr)) ? fr : 0.0;
             const double e = f > 0 ? A + w.beta[y] / eps + w.lnu[y] + log(f) : kNegInf;
-            w.m[y] = e;
+            w.wy[y] = e;
             gmax = fmax(gmax, e);
         }
         const double G = block_max(gmax, red);
-        for (int y = tid; y < ny; y += DD_NT) w.m[y] = isfinite(G) ? exp(w.m[y] - G) : 0.0;
+        for (int y = tid; y < ny; y += DD_NT) w.wy[y] = isfinite(G) ? exp(w.wy[y] - G) : 0.0;
         __syncthreads();
         for (int o = tid; o < ny0 * e1; o += DD_NT) {
             const int y0 = o / e1, a1 = o - y0 * e1;
             const int x1 = c0 + a1;
             double sacc = 0.0;
             for (int y1 = 0; y1 < ny1; ++y1)
-                sacc = fma(w.m[(int64_t)y0 * ny1 + y1], w.K1[(int64_t)x1 * ny1 + y1], sacc);
+                sacc = fma(w.wy[(int64_t)y0 * ny1 + y1], w.K1[(int64_t)x1 * ny1 + y1], sacc);
             M1[o] = sacc;
         }
         __syncthreads();

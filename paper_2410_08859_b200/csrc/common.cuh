@@ -5,7 +5,7 @@
 #include <math.h>
 #include <stdint.h>
 
-#define DD_NT 256
+#define DD_NT 512
 #define DD_NW (DD_NT / 32)
 
 namespace dd {

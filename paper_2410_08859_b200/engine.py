@@ -478,8 +478,9 @@ def _ws_total(nw0: int, nw1: int, ny0: np.ndarray, ny1: np.ndarray) -> np.ndarra
     """dd_cell_ws_size, vectorized (mirrors ws_layout in csrc/cell.cu)."""
     nx = nw0 * nw1
     ny = ny0 * ny1
-    ms = np.maximum(np.maximum(np.maximum(ny0 * nw1, nw0 * ny1), ny), nx) + nw0
-    return nw0 + nw1 + ny0 + ny1 + 7 * nx + 5 * ny + 2 * (nw0 * ny0 + nw1 * ny1) + 5 * ms
+    ms = np.maximum(ny0 * nw1, nw0 * ny1)
+    rm = np.maximum(np.maximum(ny0, ny1), max(nw0, nw1))
+    return nw0 + nw1 + ny0 + ny1 + 7 * nx + 3 * ny + nw0 * ny0 + nw1 * ny1 + 5 * ms + rm
 
 
 class _Batch:
@@ -543,6 +544,7 @@ class _Batch:
         self.alpha = B.get("alpha", n * pt.nw0 * pt.nw1, f64)
         self.beta = B.get("beta", tot_y, f64)
         self.mdens = B.get("mdens", tot_y, f64)
+        self.lnuw = B.get("lnuw", tot_y, f64)
         self.marena = B.get("marena", tot_m, f64)
         self.work = B.get("work", int(gws.sum()) + 1, f64)
         self.xarena = B.get("xarena", tot_mem * st.bs, f64)
@@ -562,7 +564,7 @@ class _Batch:
             cstat=self.cstat.data_ptr(), cstat2=self.cstat2.data_ptr(),
             smem_mode=1 if smem_mode else 0, smem_bytes=smem_bytes if smem_mode else 0,
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
-            newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold)
+            newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr())
         self.cfg = cfg
 
     def solve(self):
