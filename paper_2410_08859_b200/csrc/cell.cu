@@ -122,6 +122,10 @@ __device__ __forceinline__ double negsq(double a, double b, double eps) {
 // min(-c/eps) <= -700; both of its modes agree with this one to rounding).
 
 constexpr double kTiny = 1e-290;
+#ifdef DD_COUNT_FALLBACK
+__device__ unsigned long long g_fallbacks = 0;
+__device__ unsigned long long g_outputs = 0;
+#endif
 
 // Exact 1D log-sum-exp  log sum_k exp(v[k*stride] - (p - q[k])^2 / eps)  (two passes).
 __device__ __forceinline__ double lse1d(const double* v, int64_t stride, int n, double p,
@@ -140,78 +144,106 @@ __device__ __forceinline__ double lse1d(const double* v, int64_t stride, int n, 
 // One separable stage, in place of the reference's per-axis _lse
 // (sinkhorn.py:57-67 / 159-175):
 //   out[r][o] = log sum_k exp(in[r][k] - (p[o] - q[k])^2 / eps),  r < R, o < O, k < Kn,
-// with in row-major [R][Kn] and out row-major [R][O] (or [O][R] when tr).
-// Each row is shifted by its own max and contracted against the kernel table
-// Kt[o][k] = exp(-(p[o]-q[k])^2/eps) by FMAs; an output whose shifted sum is
-// below kTiny may have lost its dominant terms to underflow and is recomputed
-// by the exact 1D log-sum-exp.  `wts` receives exp(in - rowmax) (R*Kn),
-// `rmax` the row maxima (R).
-__device__ void lse_stage(const double* in, int R, int Kn, const double* Kt, int so, int sk,
-                          int O, const double* p, const double* q, double eps, double* wts,
-                          double* rmax, double* out, bool tr) {
-    for (int r = threadIdx.x; r < R; r += DD_NT) {
+// stored at out[o*R + r].  One warp per row: the warp takes the row max,
+// writes its shifted weights, then contracts them against the kernel table
+// Kt[o*so + k*sk] = exp(-(p[o]-q[k])^2/eps) with FMAs (a lane group per
+// output).  An output whose shifted sum is below kTiny may have lost its
+// dominant terms to underflow and is recomputed by the exact 1D
+// log-sum-exp.  PREP(r, row) may fill row r of `in` first (warp-private).
+// One block barrier at the end.
+template <class Prep>
+__device__ void lse_stage(double* in, int R, int Kn, const double* Kt, int so, int sk, int O,
+                          const double* p, const double* q, double eps, double* wts, double* out,
+                          Prep prep) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // lanes per output: largest power of two with O * g <= 32 (at most 8)
+    int g = 1;
+    while (g < 8 && O * g * 2 <= 32) g *= 2;
+    const int slots = 32 / g;
+    const int sub = lane % g, slot = lane / g;
+    for (int r = warp; r < R; r += DD_NW) {
+        double* ir = in + (int64_t)r * Kn;
+        prep(r, ir);
+        __syncwarp();
         double m = kNegInf;
-        for (int k = 0; k < Kn; ++k) m = fmax(m, in[(int64_t)r * Kn + k]);
-        rmax[r] = m;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < R * Kn; t += DD_NT) {
-        const int r = t / Kn;
-        const double m = rmax[r];
-        wts[t] = isfinite(m) ? exp(in[t] - m) : 0.0;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < R * O; t += DD_NT) {
-        const int r = t / O, o = t - r * O;
-        const double m = rmax[r];
-        double res;
-        if (!isfinite(m)) {
-            res = kNegInf;
-        } else {
-            const double* wr = wts + (int64_t)r * Kn;
-            const double* kr = Kt + (int64_t)o * so;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int k = 0;
-            for (; k + 3 < Kn; k += 4) {
-                s0 = fma(wr[k], kr[(int64_t)k * sk], s0);
-                s1 = fma(wr[k + 1], kr[(int64_t)(k + 1) * sk], s1);
-                s2 = fma(wr[k + 2], kr[(int64_t)(k + 2) * sk], s2);
-                s3 = fma(wr[k + 3], kr[(int64_t)(k + 3) * sk], s3);
+        for (int k = lane; k < Kn; k += 32) m = fmax(m, ir[k]);
+        m = warp_max_all(m);
+        double* wr = wts + (int64_t)r * Kn;
+        const bool fin = isfinite(m);
+        for (int k = lane; k < Kn; k += 32) wr[k] = fin ? exp(ir[k] - m) : 0.0;
+        __syncwarp();
+        for (int ob = 0; ob < O; ob += slots) {
+            const int o = ob + slot;
+            double s0 = 0.0, s1 = 0.0;
+            if (o < O && fin) {
+                const double* kr = Kt + (int64_t)o * so;
+                int k = sub;
+                for (; k + g < Kn; k += 2 * g) {
+                    s0 = fma(wr[k], kr[(int64_t)k * sk], s0);
+                    s1 = fma(wr[k + g], kr[(int64_t)(k + g) * sk], s1);
+                }
+                if (k < Kn) s0 = fma(wr[k], kr[(int64_t)k * sk], s0);
             }
-            for (; k < Kn; ++k) s0 = fma(wr[k], kr[(int64_t)k * sk], s0);
-            const double s = (s0 + s1) + (s2 + s3);
-            res = s >= kTiny ? log(s) + m : lse1d(in + (int64_t)r * Kn, 1, Kn, p[o], q, eps);
+            double sacc = s0 + s1;
+            for (int d = g / 2; d > 0; d >>= 1) sacc += __shfl_down_sync(0xffffffffu, sacc, d, g);
+            if (o < O && sub == 0) {
+                double res;
+                if (!fin) res = kNegInf;
+                else if (sacc >= kTiny) res = log(sacc) + m;
+                else res = lse1d(ir, 1, Kn, p[o], q, eps);
+                out[(int64_t)o * R + r] = res;
+            }
         }
-        if (tr) out[(int64_t)o * R + r] = res;
-        else out[t] = res;
+        __syncwarp();
     }
     __syncthreads();
 }
 
-// L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (left in ty).
-// Stage 1 reduces y1 per row y0 -> T[x1][y0] (transposed), stage 2 reduces y0
-// per x1 -> out[x0][x1].  K1 is [x1][y1], K0 is [x0][y0].
+struct NoPrep {
+    __device__ void operator()(int, double*) const {}
+};
+
+// L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (built row by row
+// into ty).  Stage 1 reduces y1 per row y0 -> T[x1][y0], stage 2 reduces y0 per
+// x1 -> out[x0][x1].  K1 is [x1][y1], K0 is [x0][y0].
 __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           double* out, double* red) {
-    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny;
-    for (int y = threadIdx.x; y < ny; y += DD_NT) w.ty[y] = w.beta[y] / eps + w.lnu[y];
-    __syncthreads();
+                           double* out) {
+    const int ny0 = c.ye0, ny1 = c.ye1;
     double* T = w.mid;                  // [nw1][ny0]
     double* W = w.mid + w.ms;           // stage-2 weights
-    lse_stage(w.ty, ny0, ny1, w.K1, ny1, 1, nw1, w.xc1, w.yc1, eps, w.wy, w.rmax, T, true);
-    lse_stage(T, nw1, ny0, w.K0, ny0, 1, nw0, w.xc0, w.yc0, eps, W, w.rmax, out, true);
+    const double* beta = w.beta;
+    const double* lnu = w.lnu;
+    auto prep = [=](int r, double* row) {
+        const int lane = threadIdx.x & 31;
+        for (int k = lane; k < ny1; k += 32) {
+            const int64_t y = (int64_t)r * ny1 + k;
+            row[k] = beta[y] / eps + lnu[y];
+        }
+    };
+    lse_stage(w.ty, ny0, ny1, w.K1, ny1, 1, nw1, w.xc1, w.yc1, eps, w.wy, T, prep);
+    lse_stage(T, nw1, ny0, w.K0, ny0, 1, nw0, w.xc0, w.yc0, eps, W, out, NoPrep());
 }
 
-// z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu (left in tx).
+// alpha = -ratio * L (row by row, fused), then
+// z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu (rows into tx).
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           double* out, double* red) {
-    const int ny0 = c.ye0, ny1 = c.ye1, nx = nw0 * nw1;
-    for (int x = threadIdx.x; x < nx; x += DD_NT) w.tx[x] = w.alpha[x] / eps + w.lmu[x];
-    __syncthreads();
+                           double ratio, double* out) {
+    const int ny0 = c.ye0, ny1 = c.ye1;
     double* T = w.mid;                  // [ny1][nw0]
     double* W = w.mid + w.ms;
-    lse_stage(w.tx, nw0, nw1, w.K1, 1, ny1, ny1, w.yc1, w.xc1, eps, w.wx, w.rmax, T, true);
-    lse_stage(T, ny1, nw0, w.K0, 1, ny0, ny0, w.yc0, w.xc0, eps, W, w.rmax, out, true);
+    double* alpha = w.alpha;
+    const double* L = w.L;
+    const double* lmu = w.lmu;
+    auto prep = [=](int r, double* row) {
+        const int lane = threadIdx.x & 31;
+        for (int k = lane; k < nw1; k += 32) {
+            const int x = r * nw1 + k;
+            if (ratio != 0.0) alpha[x] = -ratio * L[x];
+            row[k] = alpha[x] / eps + lmu[x];
+        }
+    };
+    lse_stage(w.tx, nw0, nw1, w.K1, 1, ny1, ny1, w.yc1, w.xc1, eps, w.wx, T, prep);
+    lse_stage(T, ny1, nw0, w.K0, 1, ny0, ny0, w.yc0, w.xc0, eps, W, out, NoPrep());
 }
 
 // Value of a boxed marginal at absolute node (r, q); zero outside.
@@ -327,8 +359,20 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
     double gap = __builtin_huge_val(), first_gap = 0.0;
     int iters = 0, newton_clamped = 0;
     const double inv_lam = 1.0 / lam;
+    __shared__ double red2[2 * DD_NW];
+    __shared__ int ndeg_sh[2];
+    if (tid < 2) ndeg_sh[tid] = 0;
+    int par = 0;
+#ifdef DD_PHASE_TIMING
+    long long ph[4] = {0, 0, 0, 0};
+    long long tp = clock64();
+#define DD_PH(i) do { __syncthreads(); long long tn = clock64(); ph[i] += tn - tp; tp = tn; } while (0)
+#else
+#define DD_PH(i) do {} while (0)
+#endif
     for (int k = 1; k <= b.max_iters; ++k) {
-        cell_lse_x(w, cw, nw0, nw1, eps, w.L, red);
+        cell_lse_x(w, cw, nw0, nw1, eps, w.L);
+        DD_PH(0);
         if (k >= 2) {
             double part = 0.0;
             for (int x = tid; x < nx; x += DD_NT) {
@@ -341,13 +385,15 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
                     part += px * (lr + a / lam) - px + ref;
                 }
             }
-            gap = lam * block_sum(part, red);
+            gap = lam * block_sum1(part, red2, par);
+            par ^= 1;
             if (!have_first) { first_gap = gap; have_first = true; }
             if (gap / lam <= thr) { converged = true; break; }
         }
-        for (int x = tid; x < nx; x += DD_NT) w.alpha[x] = -ratio * w.L[x];
-        __syncthreads();
-        cell_lse_y(w, cw, nw0, nw1, eps, w.ty, red);
+        DD_PH(1);
+        // alpha = -ratio L is fused into the Y sweep's row preparation
+        cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty);
+        DD_PH(2);
         int ndeg = 0;
         for (int y = tid; y < ny; y += DD_NT) {
             int dg = 0;
@@ -355,28 +401,23 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
                                     b.newton_max_iters, &dg, &newton_steps);
             ndeg += dg;
         }
-        const int nd = (int)block_sum((double)ndeg, red);
-        newton_clamped = max(newton_clamped, nd);
+        const int cur = k & 1;
+        if (ndeg) atomicAdd(&ndeg_sh[cur], ndeg);
+        __syncthreads();
+        // the previous iteration's count is final here (ordered by this barrier)
+        newton_clamped = max(newton_clamped, ndeg_sh[cur]);
+        if (tid == 0) ndeg_sh[cur ^ 1] = 0;
         iters = k;
+        DD_PH(3);
     }
-    (void)inv_lam;
-    if (!converged) {
-        cell_lse_x(w, cw, nw0, nw1, eps, w.L, red);
-        double part = 0.0;
-        for (int x = tid; x < nx; x += DD_NT) {
-            const double mu = w.mu[x];
-            if (mu > 0) {
-                const double a = w.alpha[x];
-                const double lr = a / eps + w.L[x];
-                const double px = mu * exp(lr);
-                const double ref = mu * exp(-a / lam);
-                part += px * (lr + a / lam) - px + ref;
-            }
-        }
-        gap = lam * block_sum(part, red);
-        if (!have_first) { first_gap = gap; have_first = true; }
-        converged = gap / lam <= thr;
+#ifdef DD_PHASE_TIMING
+    if (tid == 0) {
+        b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
+        b.cstat[(int64_t)c * 8 + 5] = (double)ph[1];
+        b.cstat[(int64_t)c * 8 + 6] = (double)ph[2];
+        b.cstat[(int64_t)c * 8 + 7] = (double)ph[3];
     }
+#endif
     const long long t_loop = clock64() - t_loop0;
     const double nsteps = block_sum((double)newton_steps, red);
     // outputs: duals
@@ -802,10 +843,12 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         cs[1] = first_gap;
         cs[2] = (double)iters;
         cs[3] = converged ? 1.0 : 0.0;
+#ifndef DD_PHASE_TIMING
         cs[4] = (double)n_clamped;
         cs[5] = (double)newton_clamped;
         cs[6] = (double)fallbacks;
         cs[7] = target_miss;
+#endif
         double* c2 = b.cstat2 + (int64_t)c * 4;
         c2[0] = (double)drift;
         c2[1] = trunc_total;
@@ -1252,3 +1295,11 @@ extern "C" int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy,
     dd::opt_set_kernel<<<1, DD_NT, 0, (cudaStream_t)stream>>>(*b, dy, c, dth, ycur, g->ny1);
     return dd_set_error(cudaGetLastError());
 }
+
+#ifdef DD_COUNT_FALLBACK
+extern "C" int dd_debug_fallbacks(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, dd::g_fallbacks, sizeof(unsigned long long));
+    cudaMemcpyFromSymbol(out + 1, dd::g_outputs, sizeof(unsigned long long));
+    return 0;
+}
+#endif

@@ -93,6 +93,27 @@ __device__ __forceinline__ int block_max_i(int v, int* red) {
     return red[DD_NW];
 }
 
+// Single-barrier deterministic block sum.  `red2` is __shared__ double[2*DD_NW];
+// successive calls must alternate `parity` (the next call's barrier orders the
+// re-use of a buffer).  Every thread sums the per-warp partials in warp order.
+__device__ __forceinline__ double block_sum1(double v, double* red2, int parity) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    double* r = red2 + parity * DD_NW;
+    if (lane == 0) r[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < DD_NW; ++k) t += r[k];
+    return t;
+}
+
+__device__ __forceinline__ double warp_max_all(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 // numpy.logaddexp semantics (npymath npy_logaddexp)
 __device__ __forceinline__ double logaddexp(double x, double y) {
     if (x == y) return x + 0.693147180559945309417232121458176568;
