@@ -206,8 +206,8 @@ struct NoPrep {
 // L[x] = log sum_y exp(bv[y] - c(x,y)/eps), bv = beta/eps + lnu (built row by row
 // into ty).  Stage 1 reduces y1 per row y0 -> T[x1][y0], stage 2 reduces y0 per
 // x1 -> out[x0][x1].  K1 is [x1][y1], K0 is [x0][y0].
-__device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           double* out) {
+__device__ void cell_lse_x_staged(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                                  double* out) {
     const int ny0 = c.ye0, ny1 = c.ye1;
     double* T = w.mid;                  // [nw1][ny0]
     double* W = w.mid + w.ms;           // stage-2 weights
@@ -226,8 +226,8 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
 
 // alpha = -ratio * L (row by row, fused), then
 // z[y] = log sum_x exp(av[x] - c(x,y)/eps), av = alpha/eps + lmu (rows into tx).
-__device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           double ratio, double* out) {
+__device__ void cell_lse_y_staged(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                                  double ratio, double* out) {
     const int ny0 = c.ye0, ny1 = c.ye1;
     double* T = w.mid;                  // [ny1][nw0]
     double* W = w.mid + w.ms;
@@ -244,6 +244,118 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     };
     lse_stage(w.tx, nw0, nw1, w.K1, 1, ny1, ny1, w.yc1, w.xc1, eps, w.wx, T, prep);
     lse_stage(T, ny1, nw0, w.K0, 1, ny0, ny0, w.yc0, w.xc0, eps, W, out, NoPrep());
+}
+
+// Fast path of both sweeps: one global max shift of the input vector and two
+// FMA contractions through the factorised kernel (the reference DenseKernel's
+// "matrix" evaluation, sinkhorn.py:91-130, done axis by axis).  If any output's
+// shifted sum is below kTiny it may have lost terms to underflow, and the
+// whole sweep is redone by the stage-wise stabilised path above, so every
+// output equals the log-domain value to rounding.
+struct SweepScratch {
+    double* redm;   // [2*DD_NW] block-max buffers
+    int* flag;      // shared underflow flag
+    int* par;       // block-max buffer parity
+};
+
+__device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                           double* out, SweepScratch sc) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    double lmax = kNegInf;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const double bv = w.beta[y] / eps + w.lnu[y];
+        w.ty[y] = bv;
+        lmax = fmax(lmax, bv);
+    }
+    if (threadIdx.x == 0) *sc.flag = 0;
+    double B = block_max1(lmax, sc.redm, *sc.par);
+    if (!isfinite(B)) B = 0.0;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) w.wy[y] = exp(w.ty[y] - B);
+    __syncthreads();
+    *sc.par ^= 1;
+    double* T = w.mid;   // [ny0][nw1]
+    for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
+        const int y0 = o / nw1, x1 = o - y0 * nw1;
+        const double* tr = w.wy + (int64_t)y0 * ny1;
+        const double* kr = w.K1 + (int64_t)x1 * ny1;
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < ny1; k += 2) {
+            s0 = fma(tr[k], kr[k], s0);
+            s1 = fma(tr[k + 1], kr[k + 1], s1);
+        }
+        if (k < ny1) s0 = fma(tr[k], kr[k], s0);
+        T[o] = s0 + s1;
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int o = threadIdx.x; o < nx; o += DD_NT) {
+        const int x0 = o / nw1, x1 = o - x0 * nw1;
+        const double* kr = w.K0 + (int64_t)x0 * ny0;
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < ny0; k += 2) {
+            s0 = fma(kr[k], T[(int64_t)k * nw1 + x1], s0);
+            s1 = fma(kr[k + 1], T[(int64_t)(k + 1) * nw1 + x1], s1);
+        }
+        if (k < ny0) s0 = fma(kr[k], T[(int64_t)k * nw1 + x1], s0);
+        const double sm = s0 + s1;
+        if (sm >= kTiny) out[o] = log(sm) + B;
+        else bad = 1;
+    }
+    if (bad) *sc.flag = 1;
+    __syncthreads();
+    if (*sc.flag) cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+}
+
+__device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                           double ratio, double* out, SweepScratch sc) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    double lmax = kNegInf;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) {
+        if (ratio != 0.0) w.alpha[x] = -ratio * w.L[x];
+        const double av = w.alpha[x] / eps + w.lmu[x];
+        w.tx[x] = av;
+        lmax = fmax(lmax, av);
+    }
+    if (threadIdx.x == 0) *sc.flag = 0;
+    double A = block_max1(lmax, sc.redm, *sc.par);
+    if (!isfinite(A)) A = 0.0;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) w.wx[x] = exp(w.tx[x] - A);
+    __syncthreads();
+    *sc.par ^= 1;
+    double* T = w.mid;   // [nw0][ny1]
+    for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
+        const int x0 = o / ny1, y1 = o - x0 * ny1;
+        const double* tr = w.wx + (int64_t)x0 * nw1;
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < nw1; k += 2) {
+            s0 = fma(tr[k], w.K1[(int64_t)k * ny1 + y1], s0);
+            s1 = fma(tr[k + 1], w.K1[(int64_t)(k + 1) * ny1 + y1], s1);
+        }
+        if (k < nw1) s0 = fma(tr[k], w.K1[(int64_t)k * ny1 + y1], s0);
+        T[o] = s0 + s1;
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int o = threadIdx.x; o < ny; o += DD_NT) {
+        const int y0 = o / ny1, y1 = o - y0 * ny1;
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+        for (; k + 1 < nw0; k += 2) {
+            s0 = fma(w.K0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+            s1 = fma(w.K0[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
+        }
+        if (k < nw0) s0 = fma(w.K0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+        const double sm = s0 + s1;
+        if (sm >= kTiny) out[o] = log(sm) + A;
+        else bad = 1;
+    }
+    if (bad) *sc.flag = 1;
+    __syncthreads();
+    // alpha is already updated; the staged redo must not apply the update twice
+    if (*sc.flag) cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
 }
 
 // Value of a boxed marginal at absolute node (r, q); zero outside.
@@ -360,6 +472,10 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
     int iters = 0, newton_clamped = 0;
     const double inv_lam = 1.0 / lam;
     __shared__ double red2[2 * DD_NW];
+    __shared__ double redm[2 * DD_NW];
+    __shared__ int sweep_flag;
+    int mpar = 0;
+    const SweepScratch sc{redm, &sweep_flag, &mpar};
     __shared__ int ndeg_sh[2];
     if (tid < 2) ndeg_sh[tid] = 0;
     int par = 0;
@@ -371,7 +487,7 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
 #define DD_PH(i) do {} while (0)
 #endif
     for (int k = 1; k <= b.max_iters; ++k) {
-        cell_lse_x(w, cw, nw0, nw1, eps, w.L);
+        cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
         DD_PH(0);
         if (k >= 2) {
             double part = 0.0;
@@ -392,7 +508,7 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         }
         DD_PH(1);
         // alpha = -ratio L is fused into the Y sweep's row preparation
-        cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty);
+        cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
         DD_PH(2);
         int ndeg = 0;
         for (int y = tid; y < ny; y += DD_NT) {
@@ -418,6 +534,26 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         b.cstat[(int64_t)c * 8 + 7] = (double)ph[3];
     }
 #endif
+    __syncthreads();
+    if (!converged) {
+        // cap reached: final X sweep and gap for the last (post-Y-step) pair
+        // (cells.py:341-348)
+        cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
+        double part = 0.0;
+        for (int x = tid; x < nx; x += DD_NT) {
+            const double mu = w.mu[x];
+            if (mu > 0) {
+                const double a = w.alpha[x];
+                const double lr = a / eps + w.L[x];
+                const double px = mu * exp(lr);
+                const double ref = mu * exp(-a / lam);
+                part += px * (lr + a / lam) - px + ref;
+            }
+        }
+        gap = lam * block_sum(part, red);
+        if (!have_first) { first_gap = gap; have_first = true; }
+        converged = gap / lam <= thr;
+    }
     const long long t_loop = clock64() - t_loop0;
     const double nsteps = block_sum((double)newton_steps, red);
     // outputs: duals

@@ -108,6 +108,19 @@ __device__ __forceinline__ double block_sum1(double v, double* red2, int parity)
     return t;
 }
 
+// Single-barrier block max (same double-buffer protocol as block_sum1).
+__device__ __forceinline__ double block_max1(double v, double* red2, int parity) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_max(v);
+    double* r = red2 + parity * DD_NW;
+    if (lane == 0) r[wid] = v;
+    __syncthreads();
+    double t = r[0];
+#pragma unroll
+    for (int k = 1; k < DD_NW; ++k) t = fmax(t, r[k]);
+    return t;
+}
+
 __device__ __forceinline__ double warp_max_all(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

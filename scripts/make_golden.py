@@ -76,6 +76,11 @@ CASES = [
          max_iters=10, warm=True, seed=6, uniform=False, nu_scale=1.3),
     dict(name="mix32_staggered", dims=(32, 32), s=4, lam=0.5, strategy="staggered", delta=1e-6,
          max_iters=6, warm=True, seed=7, uniform=False, nu_scale=0.8),
+    # cell iteration cap hit on every solve (non-converged cells, final recompute path)
+    dict(name="mix16_cellcap", dims=(16, 16), s=4, lam=1.0, strategy="staggered", delta=1e-7,
+         max_iters=4, warm=False, seed=8, uniform=False, nu_scale=1.2, cell_max_iters=7),
+    dict(name="toy1d_cellcap_swift", dims=(16,), s=2, lam=2.0, strategy="swift", delta=1e-8,
+         max_iters=5, warm=False, seed=9, uniform=False, cell_max_iters=3),
 ]
 
 
@@ -100,10 +105,12 @@ def run_case(eng, meas, c):
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         dec = eng.make_decomposition(prob.mu, c["s"])
-    cfg = eng.EngineConfig(delta=c["delta"], max_iters=c["max_iters"])
+    cell = eng.CellSolverConfig(max_iters=c.get("cell_max_iters", 10_000))
+    cfg = eng.EngineConfig(delta=c["delta"], max_iters=c["max_iters"], cell=cell)
     state = eng.warm_start_plan(prob, dec, delta=1e-3) if c["warm"] else None
     st, rep = eng.domdec_solve(prob, dec, eng.StrategyConfig(kind=c["strategy"]), cfg, state=state)
     out = dict(mu=mu, nu=nu, dx=dx, origin=np.array(origin), lam=c["lam"], eps=eps, s=c["s"],
+               cell_max_iters=c.get("cell_max_iters", 10_000),
                strategy=c["strategy"], delta=c["delta"], max_iters=c["max_iters"],
                warm=c["warm"])
     boxes, vals, offs = [], [], [0]

@@ -19,14 +19,16 @@ def problem_from_golden(g):
 
 def run_device(g):
     from paper_2410_08859_b200.decomposition import make_decomposition
-    from paper_2410_08859_b200.engine import (EngineConfig, StrategyConfig, domdec_solve,
-                                              warm_start_plan)
+    from paper_2410_08859_b200.engine import (CellSolverConfig, EngineConfig, StrategyConfig,
+                                              domdec_solve, warm_start_plan)
+    from _golden import cell_cap
 
     prob = problem_from_golden(g)
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         dec = make_decomposition(prob.mu, int(g["s"]))
-    cfg = EngineConfig(delta=float(g["delta"]), max_iters=int(g["max_iters"]))
+    cfg = EngineConfig(delta=float(g["delta"]), max_iters=int(g["max_iters"]),
+                       cell=CellSolverConfig(max_iters=cell_cap(g)))
     state = warm_start_plan(prob, dec, delta=1e-3) if bool(g["warm"]) else None
     st, rep = domdec_solve(prob, dec, StrategyConfig(kind=str(g["strategy"])), cfg, state=state)
     return prob, dec, st, rep

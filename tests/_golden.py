@@ -9,7 +9,12 @@ import numpy as np
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 ENGINE_CASES = ["toy1d_staggered", "toy1d_safe", "toy1d_swift", "toy1d_opt", "toy1d_sequential",
-                "toy1d_fast", "mix16_staggered", "mix16_warm", "mix32_staggered"]
+                "toy1d_fast", "mix16_staggered", "mix16_warm", "mix32_staggered", "mix16_cellcap",
+                "toy1d_cellcap_swift"]
+
+
+def cell_cap(g) -> int:
+    return int(g["cell_max_iters"]) if "cell_max_iters" in g else 10_000
 
 
 def load(name: str) -> dict:

@@ -9,9 +9,9 @@ import pytest
 
 from oracle import ref_lse
 from oracle.ref_problem import make_ctx
-from oracle.ref_sweep import EngCfg, StratCfg, solve, warm_state
+from oracle.ref_sweep import CellCfg, EngCfg, StratCfg, solve, warm_state
 
-from _golden import ENGINE_CASES, dense, load, ref_duals, ref_marginals, rel_err, scalar
+from _golden import ENGINE_CASES, cell_cap, dense, load, ref_duals, ref_marginals, rel_err, scalar
 
 
 def test_newton_grid_matches_reference():
@@ -46,7 +46,8 @@ def oracle_run(g):
     ctx = make_ctx(mu, nu, float(g["dx"]), tuple(g["origin"]), float(g["lam"]), float(g["eps"]),
                    int(g["s"]))
     st = warm_state(ctx, delta=1e-3) if bool(g["warm"]) else None
-    cfg = EngCfg(delta=float(g["delta"]), max_iters=int(g["max_iters"]))
+    cfg = EngCfg(delta=float(g["delta"]), max_iters=int(g["max_iters"]),
+                 cell=CellCfg(max_iters=cell_cap(g)))
     return ctx, solve(ctx, st, StratCfg(kind=str(g["strategy"])), cfg)
 
 
