@@ -118,6 +118,18 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank scalar across the process group (identity when not distributed)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def flush_l2(buf):
     buf.fill_(1.0)
 
@@ -237,11 +249,7 @@ def main():
             times.append(a.elapsed_time(b) / 1e3)
             reps.append(rep)
     launches = tracer.launches() // max(1, args.steps)
-    t_dev = float(np.max(times))
-    if world > 1:
-        tt = torch.tensor([t_dev], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_dev = float(tt.item())
+    t_dev = max_over_ranks(float(np.max(times)), device="cuda")
     # ---- end-to-end through the public API (host arrays in, host result out)
     e2e_times = []
     h2d = 0

@@ -81,6 +81,11 @@ CASES = [
          max_iters=4, warm=False, seed=8, uniform=False, nu_scale=1.2, cell_max_iters=7),
     dict(name="toy1d_cellcap_swift", dims=(16,), s=2, lam=2.0, strategy="swift", delta=1e-8,
          max_iters=5, warm=False, seed=9, uniform=False, cell_max_iters=3),
+    # zero-mass mu regions: dropped basic cells, padded composites, zero nodes inside cells
+    dict(name="mix16_zeros", dims=(16, 16), s=2, lam=1.0, strategy="staggered", delta=1e-6,
+         max_iters=8, warm=False, seed=10, uniform=False, zero_mu=True),
+    dict(name="mix16_zeros_warm_opt", dims=(16, 16), s=4, lam=0.7, strategy="opt", delta=1e-6,
+         max_iters=4, warm=True, seed=11, uniform=False, zero_mu=True, nu_scale=1.1),
 ]
 
 
@@ -97,6 +102,10 @@ def run_case(eng, meas, c):
     else:
         mu = _mixture(dims, dx, origin, rng, 3)
         nu = _mixture(dims, dx, origin, rng, 3) * c.get("nu_scale", 1.0)
+        if c.get("zero_mu"):
+            mu[4:8, 8:12] = 0.0            # a whole block (dropped basic cells)
+            mu[rng.uniform(size=dims) < 0.05] = 0.0   # scattered zero nodes
+            mu = mu / mu.sum()
     eps = 2.0 * dx * dx
     grid = meas.Grid(dims, dx=dx, origin=origin)
     prob = meas.TransportProblem(

@@ -10,7 +10,7 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 ENGINE_CASES = ["toy1d_staggered", "toy1d_safe", "toy1d_swift", "toy1d_opt", "toy1d_sequential",
                 "toy1d_fast", "mix16_staggered", "mix16_warm", "mix32_staggered", "mix16_cellcap",
-                "toy1d_cellcap_swift"]
+                "toy1d_cellcap_swift", "mix16_zeros", "mix16_zeros_warm_opt"]
 
 
 def cell_cap(g) -> int:
