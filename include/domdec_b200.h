@@ -213,6 +213,17 @@ int dd_refine(const dd_geom* g, const dd_state* s, const int32_t* parent, const 
               const double* cval, int64_t ccap, const double* cmass, const double* nu_c,
               int cny1, double trunc, double* trunc_out, void* stream);
 
+/* Dual-shaped refinement: as dd_refine, but each child's Y-marginal takes the
+ * shape of the diagonal-scaling plan of the (prolonged) fine duals alpha, beta
+ * restricted to the child block, over the parent's doubled box, scaled to the
+ * child's share of the parent mass.  tmp holds n_basic * tcap doubles (tcap >=
+ * 4 * coarse box size); max_fe1 = largest doubled box extent (either axis).  Requires
+ * block0 <= 8, block0*block1 <= 64. */
+int dd_refine_dual(const dd_geom* g, const dd_state* s, const int32_t* parent, const int32_t* cbox,
+                   const double* cval, int64_t ccap, const double* cmass, const double* alpha,
+                   const double* beta, double trunc, double* trunc_out, double* tmp, int64_t tcap,
+                   int max_fe1, void* stream);
+
 /* Bilinear prolongation of a cell-centred coarse field (nc0 x nc1) to the
  * x2 finer grid (nf0 x nf1); constant beyond the outer coarse centres. */
 int dd_prolong(int nf0, int nf1, int nc0, int nc1, const double* coarse, double* fine,

@@ -465,6 +465,9 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
     __syncthreads();
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
     const long long t_loop0 = clock64();
+#ifdef DD_NEWTON_STATS
+    int nst[4] = {0, 0, 0, 0};   // clips, bisections, max evals, nodes with >= 6 evals
+#endif
     long long newton_steps = 0;
     bool converged = false;
     bool have_first = false;
@@ -513,8 +516,13 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         int ndeg = 0;
         for (int y = tid; y < ny; y += DD_NT) {
             int dg = 0;
+#ifdef DD_NEWTON_STATS
+            w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
+                                    b.newton_max_iters, &dg, &newton_steps, nst);
+#else
             w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
                                     b.newton_max_iters, &dg, &newton_steps);
+#endif
             ndeg += dg;
         }
         const int cur = k & 1;
@@ -526,6 +534,20 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         iters = k;
         DD_PH(3);
     }
+#ifdef DD_NEWTON_STATS
+    {
+        const double a0 = block_sum((double)nst[0], red);
+        const double a1 = block_sum((double)nst[1], red);
+        const double a3 = block_sum((double)nst[3], red);
+        const double a2 = block_max((double)nst[2], red);
+        if (tid == 0) {
+            b.cstat[(int64_t)c * 8 + 4] = a0;
+            b.cstat[(int64_t)c * 8 + 5] = a1;
+            b.cstat[(int64_t)c * 8 + 6] = a2;
+            b.cstat[(int64_t)c * 8 + 7] = a3;
+        }
+    }
+#endif
 #ifdef DD_PHASE_TIMING
     if (tid == 0) {
         b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
@@ -979,7 +1001,7 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         cs[1] = first_gap;
         cs[2] = (double)iters;
         cs[3] = converged ? 1.0 : 0.0;
-#ifndef DD_PHASE_TIMING
+#if !defined(DD_PHASE_TIMING) && !defined(DD_NEWTON_STATS)
         cs[4] = (double)n_clamped;
         cs[5] = (double)newton_clamped;
         cs[6] = (double)fallbacks;

@@ -154,7 +154,8 @@ __device__ __forceinline__ double kl_term(double rho, double sigma) {
 // Returns beta; *deg set when the node is degenerate (m == 0, z == -inf).
 __device__ __forceinline__ double newton_node(double z, double m, bool has_m, double beta0,
                                               double eps, double lam, double tol, int max_iters,
-                                              int* deg, long long* steps = nullptr) {
+                                              int* deg, long long* steps = nullptr,
+                                              int* nstat = nullptr) {
     const double ratio = eps * lam / (eps + lam);
     const bool fz = z > kNegInf;
     if (!has_m || !(m > 0)) {
@@ -170,8 +171,11 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
     double lo = fmin(b1, b2) - lam;
     double hi = fmax(b1, b2) + lam;
     double b = fmin(fmax(beta0, lo), hi);  // np.clip
+    if (nstat && b != beta0) nstat[0] += 1;
+    int nev = 0;
     for (int it = 0; it < max_iters; ++it) {
         if (steps) ++*steps;
+        ++nev;
         const double w = b * inv_eps + z;
         // logaddexp(lm, w) and expit(w - lm) from one exponential
         double la, sig;
@@ -197,9 +201,16 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         if (!((nb > lo) && (nb < hi))) {
             if (g > 0) hi = fmin(hi, b);
             else lo = fmax(lo, b);
-            if ((nb <= lo) || (nb >= hi)) nb = 0.5 * (lo + hi);
+            if ((nb <= lo) || (nb >= hi)) {
+                nb = 0.5 * (lo + hi);
+                if (nstat) nstat[1] += 1;
+            }
         }
         b = nb;
+    }
+    if (nstat) {
+        nstat[2] = max(nstat[2], nev);
+        if (nev >= 6) nstat[3] += 1;
     }
     return b;
 }

@@ -12,10 +12,11 @@ grids refined x2 per level from ``n_coarsest`` up to the problem grid):
   on the finest level);
 * the coarsest level starts from ``warm_start_plan`` (global device Sinkhorn
   plus plan cut); every later level starts from ``refine_plan`` — each coarse
-  basic-cell Y-marginal split over its 2^d child cells by fine mu mass and,
-  within Y, over child nodes by fine nu mass (``dd_refine``), duals prolonged
-  bilinearly (``dd_prolong``; piecewise-constant potentials would put an
-  O(|grad beta| h / eps) error into the warm start);
+  basic-cell Y-marginal mass split over its 2^d child cells by fine mu mass,
+  duals prolonged bilinearly
+  (``dd_prolong``; piecewise-constant potentials would put an
+  O(|grad beta| h / eps) error into the warm start); child marginals are the
+  parent's split by fine mu (across children) and fine nu (across nodes);
 * each eps stage is one ``domdec_solve`` warm-started from the previous
   stage's plan, cell duals and certificate duals.
 
@@ -107,8 +108,20 @@ def eps_schedule(levels: list, eps_start: float, eps_final: float) -> list:
 
 
 def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
-                coarse_duals=None, trunc_threshold: float = 1e-15, dp=None) -> PlanState:
-    """Fine-level state from a solved coarse state (SPEC multiscale.refine_plan)."""
+                coarse_duals=None, trunc_threshold: float = 1e-15, dp=None,
+                shape: str = "split") -> PlanState:
+    """Fine-level state from a solved coarse state (SPEC multiscale.refine_plan).
+
+    Each child basic cell keeps its share f_j = mu(X_j)/mu(X_i) of the parent's
+    Y-marginal mass.  ``shape="split"`` (default) splits the parent marginal
+    over fine Y nodes by fine nu mass (``dd_refine``), which keeps the summed
+    children consistent with the coarse plan's Y-marginal.  ``shape="dual"``
+    shapes each child by the plan of the prolonged duals restricted to its
+    block (``dd_refine_dual``): tighter boxes, but the children no longer sum
+    to the coarse marginal and the first fine sweeps pay for it (measured: many
+    more cell iterations), so it is opt-in.  Both truncate at the threshold and
+    install product-plan fragments; duals are prolonged bilinearly.
+    """
     import torch
 
     cb = coarse.basic
@@ -128,24 +141,38 @@ def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
         raise ValueError("fine basic cell without a coarse parent")
     parent_d = torch.from_numpy(parent.astype(np.int32)).to(dp.device)
     trunc_out = torch.zeros(fb.n_cells, dtype=torch.float64, device=dp.device)
-    cny1 = coarse.dp.geom.ny1
-    _lib.check(_lib.lib().dd_refine(dp.geom, st.state_struct(), parent_d.data_ptr(),
-                                    coarse.ybox.data_ptr(), coarse.yval.data_ptr(), coarse.cap,
-                                    coarse.basic_mass.data_ptr(), coarse.dp.nu.data_ptr(), cny1,
-                                    float(trunc_threshold), trunc_out.data_ptr(),
-                                    _lib.stream_handle()))
-    st.sync_boxes()
-    st.truncated_mass = coarse.truncated_mass + float(trunc_out.sum().item())
+    g = dp.geom
+    L = _lib.lib()
+    fa = fbeta = None
     if coarse_duals is not None:
         ca, cbeta = coarse_duals
-        g = dp.geom
+        cg = coarse.dp.geom
         fa = dp.empty_x()
         fbeta = dp.empty_y()
-        cg = coarse.dp.geom
-        _lib.check(_lib.lib().dd_prolong(g.nx0, g.nx1, cg.nx0, cg.nx1, ca.data_ptr(),
-                                         fa.data_ptr(), _lib.stream_handle()))
-        _lib.check(_lib.lib().dd_prolong(g.ny0, g.ny1, cg.ny0, cg.ny1, cbeta.data_ptr(),
-                                         fbeta.data_ptr(), _lib.stream_handle()))
+        _lib.check(L.dd_prolong(g.nx0, g.nx1, cg.nx0, cg.nx1, ca.data_ptr(), fa.data_ptr(),
+                                _lib.stream_handle()))
+        _lib.check(L.dd_prolong(g.ny0, g.ny1, cg.ny0, cg.ny1, cbeta.data_ptr(), fbeta.data_ptr(),
+                                _lib.stream_handle()))
+    if shape == "dual" and fa is not None and st.block[0] <= 8 and st.bs <= 64:
+        tcap = 4 * cmax
+        tmp = torch.empty(fb.n_cells * tcap, dtype=torch.float64, device=dp.device)
+        max_fe = 2 * int(max(boxes[:, 1].max(initial=1), boxes[:, 3].max(initial=1)))
+        _lib.check(L.dd_refine_dual(dp.geom, st.state_struct(), parent_d.data_ptr(),
+                                    coarse.ybox.data_ptr(), coarse.yval.data_ptr(), coarse.cap,
+                                    coarse.basic_mass.data_ptr(), fa.data_ptr(), fbeta.data_ptr(),
+                                    float(trunc_threshold), trunc_out.data_ptr(), tmp.data_ptr(),
+                                    tcap, max_fe, _lib.stream_handle()))
+        torch.cuda.synchronize()
+        del tmp
+    else:
+        _lib.check(L.dd_refine(dp.geom, st.state_struct(), parent_d.data_ptr(),
+                               coarse.ybox.data_ptr(), coarse.yval.data_ptr(), coarse.cap,
+                               coarse.basic_mass.data_ptr(), coarse.dp.nu.data_ptr(),
+                               coarse.dp.geom.ny1, float(trunc_threshold), trunc_out.data_ptr(),
+                               _lib.stream_handle()))
+    st.sync_boxes()
+    st.truncated_mass = coarse.truncated_mass + float(trunc_out.sum().item())
+    if fa is not None:
         for part in fine_dec.composites:
             pt = _tables(part)
             yb = _member_boxes(st, pt, np.arange(pt.ncomp))
@@ -153,10 +180,9 @@ def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
             store.ensure(int((yb[:, 1].astype(np.int64) * yb[:, 3]).max(initial=1)))
             xb_d = torch.from_numpy(pt.xbox.ravel().copy()).to(dp.device)
             yb_d = torch.from_numpy(yb.ravel().copy()).to(dp.device)
-            _lib.check(_lib.lib().dd_seed_duals(dp.geom, st.state_struct(store), pt.ncomp, pt.nw0,
-                                               pt.nw1, xb_d.data_ptr(), yb_d.data_ptr(),
-                                               fa.data_ptr(), fbeta.data_ptr(),
-                                               _lib.stream_handle()))
+            _lib.check(L.dd_seed_duals(dp.geom, st.state_struct(store), pt.ncomp, pt.nw0, pt.nw1,
+                                       xb_d.data_ptr(), yb_d.data_ptr(), fa.data_ptr(),
+                                       fbeta.data_ptr(), _lib.stream_handle()))
         st.global_duals = (fa, fbeta)
     return st
 
