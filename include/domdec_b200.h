@@ -106,6 +106,7 @@ typedef struct dd_batch {
     double newton_tol;
     double trunc;
     double* lnuw;              /* y arena: log nu on each cell window (kernel scratch) */
+    double* lout;              /* [n_cells*nxw0*nxw1] final X sweep of cluster-solved cells */
 } dd_batch;
 
 const char* dd_last_error(void);
@@ -147,6 +148,21 @@ int dd_global_terms(int mode, int64_t n_x, int64_t n_y, const double* a, const d
 /* Cell batch: assemble windows, Sinkhorn to tolerance, split, balance,
  * truncate, fragments, x-marginals. */
 int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream);
+
+/* As dd_cell_solve, with the cells whose workspace does not fit shared memory
+ * (n_big of them) handled on stream_big, concurrently with the shared-memory
+ * cells on `stream` (joined back before return).  Of those, the n_clu cells
+ * listed in clu_ids (device int32; their desc flags bit 0 set) run their
+ * Sinkhorn loop on a thread-block cluster of clu_size CTAs (clu_smem bytes of
+ * shared memory each, rows of the Y window split across the cluster); every
+ * big cell then goes through the global-workspace kernel variant (max-L1
+ * carveout), epilogue only for the cluster-solved ones. */
+int dd_cell_solve2(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream,
+                   void* stream_big, int n_big, const int32_t* clu_ids, int n_clu, int clu_size,
+                   int clu_smem);
+
+/* Shared-memory doubles per CTA of the cluster variant. */
+int64_t dd_cell_cluster_ws(int nw0, int nw1, int ny0, int ny1, int clu_size);
 
 /* Blend scoring: per-cell dy windows (into dy arena at the y offsets) and
  * per-cell scalars cd[c*4] = t_delta, k_delta, d1_old, unused. */

@@ -20,6 +20,7 @@ EXPORTS = [
     "dd_cell_commit", "dd_assemble", "dd_energy_terms", "dd_product_init", "dd_cut_plan",
     "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
     "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong", "dd_refine_dual",
+    "dd_cell_solve2", "dd_cell_cluster_ws",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -47,7 +48,7 @@ class Batch(C.Structure):
                 ("xarena", vp), ("mbox", vp), ("mstat", vp), ("cstat", vp), ("cstat2", vp),
                 ("smem_mode", i32), ("smem_bytes", i32),
                 ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
-                ("newton_tol", dbl), ("trunc", dbl), ("lnuw", vp)]
+                ("newton_tol", dbl), ("trunc", dbl), ("lnuw", vp), ("lout", vp)]
 
 
 _SIGS = {
@@ -60,6 +61,9 @@ _SIGS = {
     "dd_global_terms": ([C.c_int, i64, i64, vp, vp, vp, vp, vp, vp, dbl, dbl, vp, vp, vp, vp],
                         C.c_int),
     "dd_cell_solve": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp], C.c_int),
+    "dd_cell_solve2": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, C.c_int, vp,
+                        C.c_int, C.c_int, C.c_int], C.c_int),
+    "dd_cell_cluster_ws": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], i64),
     "dd_cell_delta": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp], C.c_int),
     "dd_blend_energy": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp,
                          vp, vp], C.c_int),
@@ -113,7 +117,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
 # kernels each entry point launches (used for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "dd_grid_lse": 2, "dd_axpb": 1, "dd_newton_global": 1, "dd_newton_nodes": 1,
-    "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_delta": 1, "dd_blend_energy": 5,
+    "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_solve2": 3, "dd_cell_delta": 1, "dd_blend_energy": 5,
     "dd_cell_commit": 1, "dd_assemble": 1, "dd_energy_terms": 4, "dd_product_init": 1,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1, "dd_refine_dual": 1,
@@ -124,7 +128,7 @@ class Tracer:
     """Counts calls/kernel launches per entry point and times selected ones with
     CUDA events recorded on the launching (current) stream."""
 
-    def __init__(self, timed=("dd_cell_solve", "dd_grid_lse")):
+    def __init__(self, timed=("dd_cell_solve", "dd_cell_solve2", "dd_grid_lse")):
         self.timed = set(timed)
         self.calls: dict = {}
         self.events: dict = {}
@@ -157,7 +161,8 @@ class _Traced:
         fn = getattr(self._h, name)
         t = _tracer
         if t is None or not name.startswith("dd_") or name in ("dd_last_error", "dd_device_count",
-                                                               "dd_abi_version", "dd_cell_ws_size"):
+                                                               "dd_abi_version", "dd_cell_ws_size",
+                                                               "dd_cell_cluster_ws"):
             return fn
 
         def call(*args):

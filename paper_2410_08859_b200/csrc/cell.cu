@@ -10,6 +10,8 @@
 // the score fragments and X-marginals — the same outputs the reference
 // produces in cells.py:283-443.
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "domdec_b200.h"
 
@@ -369,6 +371,396 @@ __device__ __forceinline__ double boxed_at(const int32_t* box, const double* val
 
 // ---- the solve kernel -----------------------------------------------------
 
+// ---- cluster variant of the Sinkhorn loop for large Y windows -----------------
+//
+// One thread-block cluster per composite cell (north_star: "one CTA, or a
+// cluster for large composite cells").  The Y window's rows are split across
+// the cluster's CTAs (each keeps its rows of beta / bv / weights in shared
+// memory); the X-window state (alpha, L, mu) is replicated, and every CTA
+// performs the identical X-side arithmetic so stopping decisions agree
+// without communication.  Cross-CTA steps go through distributed shared
+// memory in fixed rank order (deterministic): the global max of bv, the
+// X-sweep's stage-2 partial sums over the row slices, and the gather of
+// stage-1 rows for the exact fallback.  The loop's outputs (alpha, beta, L,
+// stats) are written to the batch arenas; the single-CTA kernel then runs
+// the epilogue for these cells in epilogue-only mode.
+
+struct CluLayout {
+    int64_t xc0, xc1, yc0, yc1, alpha, L, mu, lmu, tx, wx, beta, ty, wy, K0, K1, T1, P, T2, W, G,
+        rmax, total;
+};
+
+__host__ __device__ inline CluLayout clu_layout(int nw0, int nw1, int ny0, int ny1, int rows) {
+    CluLayout l;
+    const int64_t nx = (int64_t)nw0 * nw1, nyl = (int64_t)rows * ny1;
+    int64_t o = 0;
+    l.xc0 = o; o += nw0;
+    l.xc1 = o; o += nw1;
+    l.yc0 = o; o += ny0;
+    l.yc1 = o; o += ny1;
+    l.alpha = o; o += nx;
+    l.L = o; o += nx;
+    l.mu = o; o += nx;
+    l.lmu = o; o += nx;
+    l.tx = o; o += nx;
+    l.wx = o; o += nx;
+    l.beta = o; o += nyl;
+    l.ty = o; o += nyl;
+    l.wy = o; o += nyl;
+    l.K0 = o; o += (int64_t)nw0 * ny0;
+    l.K1 = o; o += (int64_t)nw1 * ny1;
+    l.T1 = o; o += (int64_t)rows * nw1;       // X sweep stage 1, local rows ([x1][row] when staged)
+    l.P = o; o += 2 * nx;                     // double-buffered stage-2 partials
+    l.T2 = o; o += (int64_t)nw0 * ny1;        // Y sweep stage 1 (replicated)
+    int64_t wsz = (int64_t)nw1 * ny0;
+    if ((int64_t)ny1 * nw0 > wsz) wsz = (int64_t)ny1 * nw0;
+    if (nx > wsz) wsz = nx;
+    if (nyl > wsz) wsz = nyl;
+    l.W = o; o += wsz;                        // staged-stage weights
+    l.G = o; o += (int64_t)nw1 * ny0;         // gathered stage-1 rows for the staged X fallback
+    int64_t rm = ny0 > ny1 ? ny0 : ny1;
+    if (nw0 > rm) rm = nw0;
+    if (nw1 > rm) rm = nw1;
+    l.rmax = o; o += rm;
+    l.total = o;
+    return l;
+}
+
+__device__ __forceinline__ int clu_row0(int ny0, int C, int rank) {
+    return (int)(((int64_t)ny0 * rank) / C);
+}
+
+__global__ void __launch_bounds__(DD_NT, 1) cell_loop_cluster_kernel(dd_geom g, dd_state s,
+                                                                     dd_batch b,
+                                                                     const int32_t* ids) {
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cluster = cgx::this_cluster();
+    extern __shared__ double smem[];
+    __shared__ double red[DD_NW + 1];
+    __shared__ int redi[DD_NW + 1];
+    __shared__ double xslot[4];          // scalar exchange slots (double-buffered pairs)
+    __shared__ int flag_sh;
+
+    const int C = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int c = ids[blockIdx.x / C];
+    const int32_t* d = b.desc + (int64_t)c * 12;
+    const int64_t* off = b.offs + (int64_t)c * 4;
+    const int nw0 = b.nxw0, nw1 = b.nxw1;
+    const CellWin cw = load_win(d, nw0, nw1);
+    const int j = d[0];
+    const int nmem = d[9];
+    const int32_t* mem = b.members + d[10];
+    const int nx = cw.nx, ny0 = cw.ye0, ny1 = cw.ye1;
+    const int r0 = clu_row0(ny0, C, rank), r1 = clu_row0(ny0, C, rank + 1);
+    const int rows = r1 - r0;
+    const int rows_max = clu_row0(ny0, C, 1) + 1;   // upper bound used for the layout
+    const CluLayout lay = clu_layout(nw0, nw1, ny0, ny1, (ny0 + C - 1) / C + 1);
+    (void)rows_max;
+    double* xc0 = smem + lay.xc0;
+    double* xc1 = smem + lay.xc1;
+    double* yc0 = smem + lay.yc0;
+    double* yc1 = smem + lay.yc1;
+    double* alpha = smem + lay.alpha;
+    double* L = smem + lay.L;
+    double* mu = smem + lay.mu;
+    double* lmu = smem + lay.lmu;
+    double* tx = smem + lay.tx;
+    double* wx = smem + lay.wx;
+    double* beta = smem + lay.beta;
+    double* ty = smem + lay.ty;
+    double* wy = smem + lay.wy;
+    double* K0 = smem + lay.K0;
+    double* K1 = smem + lay.K1;
+    double* T1 = smem + lay.T1;
+    double* P = smem + lay.P;
+    double* T2 = smem + lay.T2;
+    double* W = smem + lay.W;
+    double* G = smem + lay.G;
+    const double eps = g.eps, lam = g.lam;
+    const double ratio = eps * lam / (eps + lam);
+    const int tid = threadIdx.x;
+    const int64_t yoff = off[0];
+    const int64_t ybase = yoff + (int64_t)r0 * ny1;   // this CTA's first node in the y arenas
+    const int nyl = rows * ny1;
+    const double* lnu = b.lnuw + ybase;
+    const double* mg = b.mdens + ybase;
+
+    // cluster helpers (fixed rank order => deterministic)
+    int spar = 0;
+    auto csum = [&](double v) -> double {
+        v = block_sum(v, red);
+        if (tid == 0) xslot[spar] = v;
+        cluster.sync();
+        double t = 0.0;
+        for (int r = 0; r < C; ++r) t += *cluster.map_shared_rank(&xslot[spar], r);
+        spar ^= 1;
+        return t;
+    };
+    auto cmax = [&](double v) -> double {
+        v = block_max(v, red);
+        if (tid == 0) xslot[2 + spar] = v;
+        cluster.sync();
+        double t = kNegInf;
+        for (int r = 0; r < C; ++r) t = fmax(t, *cluster.map_shared_rank(&xslot[2 + spar], r));
+        spar ^= 1;
+        return t;
+    };
+
+    for (int i = tid; i < nw0; i += DD_NT) xc0[i] = g.x_org0 + g.x_dx * (double)(cw.xo0 + i);
+    for (int i = tid; i < nw1; i += DD_NT) xc1[i] = g.x_org1 + g.x_dx * (double)(cw.xo1 + i);
+    for (int i = tid; i < ny0; i += DD_NT) yc0[i] = g.y_org0 + g.y_dx * (double)(cw.yo0 + i);
+    for (int i = tid; i < ny1; i += DD_NT) yc1[i] = g.y_org1 + g.y_dx * (double)(cw.yo1 + i);
+    const bool has_dual = s.d_has[j] != 0;
+    double musum_part = 0.0;
+    for (int x = tid; x < nx; x += DD_NT) {
+        const int x0 = x / nw1, x1 = x - x0 * nw1;
+        const int r = cw.xo0 + x0, q = cw.xo1 + x1;
+        double m = 0.0, lm = kNegInf;
+        if (r >= 0 && r < g.nx0 && q >= 0 && q < g.nx1) {
+            const int64_t id = (int64_t)r * g.nx1 + q;
+            m = s.mu[id];
+            lm = s.log_mu[id];
+        }
+        mu[x] = m;
+        lmu[x] = lm;
+        alpha[x] = has_dual ? s.d_alpha[(int64_t)j * nx + x] : 0.0;
+        musum_part += m;
+    }
+    const double musum = block_sum(musum_part, red);   // replicated, identical in every CTA
+    const double thr = b.delta * musum;
+    const int32_t* dbox = s.d_box + (int64_t)j * 4;
+    const double* dbeta = s.d_beta + (int64_t)j * s.d_cap;
+    int nclamp = 0, anym = 0;
+    for (int yl = tid; yl < nyl; yl += DD_NT) {
+        const int y0 = r0 + yl / ny1, y1 = yl % ny1;
+        const int rr = cw.yo0 + y0, q = cw.yo1 + y1;
+        const int64_t id = (int64_t)rr * g.ny1 + q;
+        const double nu = s.nu[id];
+        b.lnuw[ybase + yl] = s.log_nu[id];
+        double cs = 0.0;
+        for (int k = 0; k < nmem; ++k) {
+            const int i = mem[k];
+            cs += boxed_at(s.ybox + (int64_t)i * 4, s.yval + (int64_t)i * s.cap, rr, q);
+        }
+        const double pw = b.snapshot[id];
+        const double diff = pw - cs;
+        if (diff < -1e-12 * fmax(pw, cs)) ++nclamp;
+        const double mm = fmax(diff, 0.0) / nu;
+        b.mdens[ybase + yl] = mm;
+        if (mm != 0.0) anym = 1;
+        beta[yl] = has_dual ? boxed_at(dbox, dbeta, rr, q) : 0.0;
+    }
+    const double n_clamped = csum((double)nclamp);
+    const bool has_m = cmax((double)anym) > 0.0;
+    for (int o = tid; o < nw0 * ny0; o += DD_NT) {
+        const int x0 = o / ny0, y0 = o - x0 * ny0;
+        K0[o] = exp(negsq(xc0[x0], yc0[y0], eps));
+    }
+    for (int o = tid; o < nw1 * ny1; o += DD_NT) {
+        const int x1 = o / ny1, y1 = o - x1 * ny1;
+        K1[o] = exp(negsq(xc1[x1], yc1[y1], eps));
+    }
+    __syncthreads();
+
+    int ppar = 0;
+    // X sweep: L[x] = log sum_y exp(bv - c/eps), bv = beta/eps + lnu; rows split.
+    auto lse_x = [&]() {
+        double lmax = kNegInf;
+        for (int yl = tid; yl < nyl; yl += DD_NT) {
+            const double bv = beta[yl] / eps + lnu[yl];
+            ty[yl] = bv;
+            lmax = fmax(lmax, bv);
+        }
+        double B = cmax(lmax);
+        if (!isfinite(B)) B = 0.0;
+        for (int yl = tid; yl < nyl; yl += DD_NT) wy[yl] = exp(ty[yl] - B);
+        __syncthreads();
+        for (int o = tid; o < rows * nw1; o += DD_NT) {
+            const int rl = o / nw1, x1 = o - rl * nw1;
+            const double* tr = wy + (int64_t)rl * ny1;
+            const double* kr = K1 + (int64_t)x1 * ny1;
+            double s0 = 0.0, s1 = 0.0;
+            int k = 0;
+            for (; k + 1 < ny1; k += 2) {
+                s0 = fma(tr[k], kr[k], s0);
+                s1 = fma(tr[k + 1], kr[k + 1], s1);
+            }
+            if (k < ny1) s0 = fma(tr[k], kr[k], s0);
+            T1[o] = s0 + s1;
+        }
+        __syncthreads();
+        double* Pp = P + ppar * nx;
+        for (int x = tid; x < nx; x += DD_NT) {
+            const int x0 = x / nw1, x1 = x - x0 * nw1;
+            const double* kr = K0 + (int64_t)x0 * ny0 + r0;
+            double s0 = 0.0, s1 = 0.0;
+            int k = 0;
+            for (; k + 1 < rows; k += 2) {
+                s0 = fma(kr[k], T1[(int64_t)k * nw1 + x1], s0);
+                s1 = fma(kr[k + 1], T1[(int64_t)(k + 1) * nw1 + x1], s1);
+            }
+            if (k < rows) s0 = fma(kr[k], T1[(int64_t)k * nw1 + x1], s0);
+            Pp[x] = s0 + s1;
+        }
+        cluster.sync();
+        int bad = 0;
+        for (int x = tid; x < nx; x += DD_NT) {
+            double sm = 0.0;
+            for (int r = 0; r < C; ++r) sm += cluster.map_shared_rank(Pp, r)[x];
+            if (sm >= kTiny) L[x] = log(sm) + B;
+            else bad = 1;
+        }
+        ppar ^= 1;
+        if (tid == 0) flag_sh = 0;
+        __syncthreads();
+        if (bad) flag_sh = 1;
+        __syncthreads();
+        if (flag_sh) {   // identical in every CTA (replicated arithmetic)
+            // staged: stage 1 over own rows -> T1[x1][row], gather all rows -> G[x1][y0],
+            // stage 2 per x1 row -> L
+            lse_stage(ty, rows, ny1, K1, ny1, 1, nw1, xc1, yc1, eps, W, T1, NoPrep());
+            cluster.sync();
+            for (int t = tid; t < nw1 * ny0; t += DD_NT) {
+                const int x1 = t / ny0, y0 = t - x1 * ny0;
+                int r = 0;
+                while (r + 1 < C && y0 >= clu_row0(ny0, C, r + 1)) ++r;
+                const int rr0 = clu_row0(ny0, C, r), rrows = clu_row0(ny0, C, r + 1) - rr0;
+                G[t] = cluster.map_shared_rank(T1, r)[(int64_t)x1 * rrows + (y0 - rr0)];
+            }
+            cluster.sync();
+            lse_stage(G, nw1, ny0, K0, ny0, 1, nw0, xc0, yc0, eps, W, L, NoPrep());
+        }
+    };
+
+    bool converged = false, have_first = false;
+    double gap = __builtin_huge_val(), first_gap = 0.0;
+    int iters = 0, newton_clamped = 0;
+    long long newton_steps = 0;
+    const long long t0c = clock64();
+    for (int k = 1; k <= b.max_iters; ++k) {
+        lse_x();
+        if (k >= 2) {
+            double part = 0.0;
+            for (int x = tid; x < nx; x += DD_NT) {
+                const double m = mu[x];
+                if (m > 0) {
+                    const double a = alpha[x];
+                    const double lr = a / eps + L[x];
+                    const double px = m * exp(lr);
+                    const double ref = m * exp(-a / lam);
+                    part += px * (lr + a / lam) - px + ref;
+                }
+            }
+            gap = lam * block_sum(part, red);   // replicated
+            if (!have_first) { first_gap = gap; have_first = true; }
+            if (gap / lam <= thr) { converged = true; break; }
+        }
+        // Y sweep (replicated stage 1, own rows in stage 2), then Newton on own rows
+        double lmax = kNegInf;
+        for (int x = tid; x < nx; x += DD_NT) {
+            alpha[x] = -ratio * L[x];
+            const double av = alpha[x] / eps + lmu[x];
+            tx[x] = av;
+            lmax = fmax(lmax, av);
+        }
+        double A = block_max(lmax, red);
+        if (!isfinite(A)) A = 0.0;
+        for (int x = tid; x < nx; x += DD_NT) wx[x] = exp(tx[x] - A);
+        __syncthreads();
+        for (int o = tid; o < nw0 * ny1; o += DD_NT) {
+            const int x0 = o / ny1, y1 = o - x0 * ny1;
+            const double* tr = wx + (int64_t)x0 * nw1;
+            double s0 = 0.0, s1 = 0.0;
+            int kk = 0;
+            for (; kk + 1 < nw1; kk += 2) {
+                s0 = fma(tr[kk], K1[(int64_t)kk * ny1 + y1], s0);
+                s1 = fma(tr[kk + 1], K1[(int64_t)(kk + 1) * ny1 + y1], s1);
+            }
+            if (kk < nw1) s0 = fma(tr[kk], K1[(int64_t)kk * ny1 + y1], s0);
+            T2[o] = s0 + s1;
+        }
+        __syncthreads();
+        int bad = 0;
+        for (int yl = tid; yl < nyl; yl += DD_NT) {
+            const int y0 = r0 + yl / ny1, y1 = yl % ny1;
+            double s0 = 0.0, s1 = 0.0;
+            int kk = 0;
+            for (; kk + 1 < nw0; kk += 2) {
+                s0 = fma(K0[(int64_t)kk * ny0 + y0], T2[(int64_t)kk * ny1 + y1], s0);
+                s1 = fma(K0[(int64_t)(kk + 1) * ny0 + y0], T2[(int64_t)(kk + 1) * ny1 + y1], s1);
+            }
+            if (kk < nw0) s0 = fma(K0[(int64_t)kk * ny0 + y0], T2[(int64_t)kk * ny1 + y1], s0);
+            const double sm = s0 + s1;
+            if (sm >= kTiny) ty[yl] = log(sm) + A;
+            else bad = 1;
+        }
+        if (tid == 0) flag_sh = 0;
+        __syncthreads();
+        if (bad) flag_sh = 1;
+        __syncthreads();
+        if (flag_sh) {   // local: this CTA's rows only
+            lse_stage(tx, nw0, nw1, K1, 1, ny1, ny1, yc1, xc1, eps, W, T2, NoPrep());
+            lse_stage(T2, ny1, nw0, K0 + r0, 1, ny0, rows, yc0 + r0, xc0, eps, W, ty, NoPrep());
+        }
+        int ndeg = 0;
+        for (int yl = tid; yl < nyl; yl += DD_NT) {
+            int dg = 0;
+            beta[yl] = newton_node(ty[yl], mg[yl], has_m, beta[yl], eps, lam, b.newton_tol,
+                                   b.newton_max_iters, &dg, &newton_steps);
+            ndeg += dg;
+        }
+        newton_clamped = max(newton_clamped, (int)block_sum((double)ndeg, red));
+        iters = k;
+    }
+    __syncthreads();
+    if (!converged) {
+        lse_x();
+        double part = 0.0;
+        for (int x = tid; x < nx; x += DD_NT) {
+            const double m = mu[x];
+            if (m > 0) {
+                const double a = alpha[x];
+                const double lr = a / eps + L[x];
+                const double px = m * exp(lr);
+                const double ref = m * exp(-a / lam);
+                part += px * (lr + a / lam) - px + ref;
+            }
+        }
+        gap = lam * block_sum(part, red);
+        if (!have_first) { first_gap = gap; have_first = true; }
+        converged = gap / lam <= thr;
+    }
+    const double cyc = (double)(clock64() - t0c);
+    const double nst = csum((double)newton_steps);
+    const double ncl = csum((double)newton_clamped);
+    for (int yl = tid; yl < nyl; yl += DD_NT) b.beta[ybase + yl] = beta[yl];
+    if (rank == 0) {
+        for (int x = tid; x < nx; x += DD_NT) {
+            b.alpha[(int64_t)c * nx + x] = alpha[x];
+            b.lout[(int64_t)c * nx + x] = L[x];
+        }
+        if (tid == 0) {
+            double* cs = b.cstat + (int64_t)c * 8;
+            cs[0] = gap;
+            cs[1] = first_gap;
+            cs[2] = (double)iters;
+            cs[3] = converged ? 1.0 : 0.0;
+            cs[4] = n_clamped;
+            cs[5] = ncl;
+            double* c2 = b.cstat2 + (int64_t)c * 4;
+            c2[2] = cyc;
+            c2[3] = nst;
+        }
+    }
+    cluster.sync();   // keep every CTA's shared memory alive until remote reads are done
+}
+
+// kPass 0: cells whose workspace fits the launch's shared memory (others exit);
+// kPass 1: the remaining (large-window) cells, workspace in the global arena,
+//          compiled as a separate function so it can run with a max-L1
+//          carveout on a second stream, concurrently with pass 0.
+template <int kPass>
 __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
     extern __shared__ double smem[];
     __shared__ double red[DD_NW + 1];
@@ -389,6 +781,9 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
     // per-cell placement: shared memory when this cell's workspace fits the
     // launch's dynamic allocation, else its slot of the global arena
     const bool in_smem = b.smem_mode && lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes;
+    if (in_smem != (kPass == 0)) return;
+    // cells whose Sinkhorn loop ran in the cluster kernel: epilogue only
+    const bool epi = (d[11] & 1) != 0;
     double* base = in_smem ? smem : (b.work + off[2]);
     Ws w = ws_bind(base, lay);
     w.lnu = b.lnuw + off[0];
@@ -419,7 +814,9 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         }
         w.mu[x] = mu;
         w.lmu[x] = lmu;
-        w.alpha[x] = has_dual ? s.d_alpha[(int64_t)j * nx + x] : 0.0;
+        w.alpha[x] = epi ? b.alpha[(int64_t)c * nx + x]
+                         : (has_dual ? s.d_alpha[(int64_t)j * nx + x] : 0.0);
+        if (epi) w.L[x] = b.lout[(int64_t)c * nx + x];
         musum_part += mu;
     }
     const double musum = block_sum(musum_part, red);
@@ -447,9 +844,9 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         const double mm = fmax(diff, 0.0) / nu;
         b.mdens[yoff + y] = mm;
         if (mm != 0.0) anym = 1;
-        w.beta[y] = has_dual ? boxed_at(dbox, dbeta, r, q) : 0.0;
+        w.beta[y] = epi ? b.beta[yoff + y] : (has_dual ? boxed_at(dbox, dbeta, r, q) : 0.0);
     }
-    const int n_clamped = (int)block_sum((double)nclamp, red);
+    int n_clamped = (int)block_sum((double)nclamp, red);
     const bool has_m = block_max_i(anym, redi) != 0;
 
     // per-axis kernel tables K_a = exp(-(x_a - y_a)^2 / eps) (entries may underflow;
@@ -464,35 +861,116 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
     }
     __syncthreads();
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
-    const long long t_loop0 = clock64();
-#ifdef DD_NEWTON_STATS
-    int nst[4] = {0, 0, 0, 0};   // clips, bisections, max evals, nodes with >= 6 evals
-#endif
-    long long newton_steps = 0;
+    // ---- Sinkhorn loop (skipped for cells solved by the cluster kernel) ----
     bool converged = false;
     bool have_first = false;
     double gap = __builtin_huge_val(), first_gap = 0.0;
     int iters = 0, newton_clamped = 0;
-    const double inv_lam = 1.0 / lam;
-    __shared__ double red2[2 * DD_NW];
-    __shared__ double redm[2 * DD_NW];
-    __shared__ int sweep_flag;
-    int mpar = 0;
-    const SweepScratch sc{redm, &sweep_flag, &mpar};
-    __shared__ int ndeg_sh[2];
-    if (tid < 2) ndeg_sh[tid] = 0;
-    int par = 0;
-#ifdef DD_PHASE_TIMING
-    long long ph[4] = {0, 0, 0, 0};
-    long long tp = clock64();
-#define DD_PH(i) do { __syncthreads(); long long tn = clock64(); ph[i] += tn - tp; tp = tn; } while (0)
-#else
-#define DD_PH(i) do {} while (0)
-#endif
-    for (int k = 1; k <= b.max_iters; ++k) {
-        cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
-        DD_PH(0);
-        if (k >= 2) {
+    double t_loop_d = 0.0, nsteps = 0.0;
+    if (epi) {
+        const double* cs = b.cstat + (int64_t)c * 8;
+        gap = cs[0];
+        first_gap = cs[1];
+        iters = (int)cs[2];
+        converged = cs[3] != 0.0;
+        n_clamped = (int)cs[4];
+        newton_clamped = (int)cs[5];
+        t_loop_d = b.cstat2[(int64_t)c * 4 + 2];
+        nsteps = b.cstat2[(int64_t)c * 4 + 3];
+    } else {
+        const long long t_loop0 = clock64();
+    #ifdef DD_NEWTON_STATS
+        int nst[4] = {0, 0, 0, 0};   // clips, bisections, max evals, nodes with >= 6 evals
+    #endif
+        long long newton_steps = 0;
+        const double inv_lam = 1.0 / lam;
+        __shared__ double red2[2 * DD_NW];
+        __shared__ double redm[2 * DD_NW];
+        __shared__ int sweep_flag;
+        int mpar = 0;
+        const SweepScratch sc{redm, &sweep_flag, &mpar};
+        __shared__ int ndeg_sh[2];
+        if (tid < 2) ndeg_sh[tid] = 0;
+        int par = 0;
+    #ifdef DD_PHASE_TIMING
+        long long ph[4] = {0, 0, 0, 0};
+        long long tp = clock64();
+    #define DD_PH(i) do { __syncthreads(); long long tn = clock64(); ph[i] += tn - tp; tp = tn; } while (0)
+    #else
+    #define DD_PH(i) do {} while (0)
+    #endif
+        for (int k = 1; k <= b.max_iters; ++k) {
+            cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
+            DD_PH(0);
+            if (k >= 2) {
+                double part = 0.0;
+                for (int x = tid; x < nx; x += DD_NT) {
+                    const double mu = w.mu[x];
+                    if (mu > 0) {
+                        const double a = w.alpha[x];
+                        const double lr = a / eps + w.L[x];
+                        const double px = mu * exp(lr);
+                        const double ref = mu * exp(-a / lam);
+                        part += px * (lr + a / lam) - px + ref;
+                    }
+                }
+                gap = lam * block_sum1(part, red2, par);
+                par ^= 1;
+                if (!have_first) { first_gap = gap; have_first = true; }
+                if (gap / lam <= thr) { converged = true; break; }
+            }
+            DD_PH(1);
+            // alpha = -ratio L is fused into the Y sweep's row preparation
+            cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
+            DD_PH(2);
+            int ndeg = 0;
+            for (int y = tid; y < ny; y += DD_NT) {
+                int dg = 0;
+    #ifdef DD_NEWTON_STATS
+                w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
+                                        b.newton_max_iters, &dg, &newton_steps, nst);
+    #else
+                w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
+                                        b.newton_max_iters, &dg, &newton_steps);
+    #endif
+                ndeg += dg;
+            }
+            const int cur = k & 1;
+            if (ndeg) atomicAdd(&ndeg_sh[cur], ndeg);
+            __syncthreads();
+            // the previous iteration's count is final here (ordered by this barrier)
+            newton_clamped = max(newton_clamped, ndeg_sh[cur]);
+            if (tid == 0) ndeg_sh[cur ^ 1] = 0;
+            iters = k;
+            DD_PH(3);
+        }
+    #ifdef DD_NEWTON_STATS
+        {
+            const double a0 = block_sum((double)nst[0], red);
+            const double a1 = block_sum((double)nst[1], red);
+            const double a3 = block_sum((double)nst[3], red);
+            const double a2 = block_max((double)nst[2], red);
+            if (tid == 0) {
+                b.cstat[(int64_t)c * 8 + 4] = a0;
+                b.cstat[(int64_t)c * 8 + 5] = a1;
+                b.cstat[(int64_t)c * 8 + 6] = a2;
+                b.cstat[(int64_t)c * 8 + 7] = a3;
+            }
+        }
+    #endif
+    #ifdef DD_PHASE_TIMING
+        if (tid == 0) {
+            b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
+            b.cstat[(int64_t)c * 8 + 5] = (double)ph[1];
+            b.cstat[(int64_t)c * 8 + 6] = (double)ph[2];
+            b.cstat[(int64_t)c * 8 + 7] = (double)ph[3];
+        }
+    #endif
+        __syncthreads();
+        if (!converged) {
+            // cap reached: final X sweep and gap for the last (post-Y-step) pair
+            // (cells.py:341-348)
+            cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
             double part = 0.0;
             for (int x = tid; x < nx; x += DD_NT) {
                 const double mu = w.mu[x];
@@ -504,80 +982,15 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
                     part += px * (lr + a / lam) - px + ref;
                 }
             }
-            gap = lam * block_sum1(part, red2, par);
-            par ^= 1;
+            gap = lam * block_sum(part, red);
             if (!have_first) { first_gap = gap; have_first = true; }
-            if (gap / lam <= thr) { converged = true; break; }
+            converged = gap / lam <= thr;
         }
-        DD_PH(1);
-        // alpha = -ratio L is fused into the Y sweep's row preparation
-        cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
-        DD_PH(2);
-        int ndeg = 0;
-        for (int y = tid; y < ny; y += DD_NT) {
-            int dg = 0;
-#ifdef DD_NEWTON_STATS
-            w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
-                                    b.newton_max_iters, &dg, &newton_steps, nst);
-#else
-            w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
-                                    b.newton_max_iters, &dg, &newton_steps);
-#endif
-            ndeg += dg;
-        }
-        const int cur = k & 1;
-        if (ndeg) atomicAdd(&ndeg_sh[cur], ndeg);
-        __syncthreads();
-        // the previous iteration's count is final here (ordered by this barrier)
-        newton_clamped = max(newton_clamped, ndeg_sh[cur]);
-        if (tid == 0) ndeg_sh[cur ^ 1] = 0;
-        iters = k;
-        DD_PH(3);
+
+        t_loop_d = (double)(clock64() - t_loop0);
+        nsteps = block_sum((double)newton_steps, red);
     }
-#ifdef DD_NEWTON_STATS
-    {
-        const double a0 = block_sum((double)nst[0], red);
-        const double a1 = block_sum((double)nst[1], red);
-        const double a3 = block_sum((double)nst[3], red);
-        const double a2 = block_max((double)nst[2], red);
-        if (tid == 0) {
-            b.cstat[(int64_t)c * 8 + 4] = a0;
-            b.cstat[(int64_t)c * 8 + 5] = a1;
-            b.cstat[(int64_t)c * 8 + 6] = a2;
-            b.cstat[(int64_t)c * 8 + 7] = a3;
-        }
-    }
-#endif
-#ifdef DD_PHASE_TIMING
-    if (tid == 0) {
-        b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
-        b.cstat[(int64_t)c * 8 + 5] = (double)ph[1];
-        b.cstat[(int64_t)c * 8 + 6] = (double)ph[2];
-        b.cstat[(int64_t)c * 8 + 7] = (double)ph[3];
-    }
-#endif
-    __syncthreads();
-    if (!converged) {
-        // cap reached: final X sweep and gap for the last (post-Y-step) pair
-        // (cells.py:341-348)
-        cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
-        double part = 0.0;
-        for (int x = tid; x < nx; x += DD_NT) {
-            const double mu = w.mu[x];
-            if (mu > 0) {
-                const double a = w.alpha[x];
-                const double lr = a / eps + w.L[x];
-                const double px = mu * exp(lr);
-                const double ref = mu * exp(-a / lam);
-                part += px * (lr + a / lam) - px + ref;
-            }
-        }
-        gap = lam * block_sum(part, red);
-        if (!have_first) { first_gap = gap; have_first = true; }
-        converged = gap / lam <= thr;
-    }
-    const long long t_loop = clock64() - t_loop0;
-    const double nsteps = block_sum((double)newton_steps, red);
+
     // outputs: duals
     for (int x = tid; x < nx; x += DD_NT) b.alpha[(int64_t)c * nx + x] = w.alpha[x];
     for (int y = tid; y < ny; y += DD_NT) b.beta[yoff + y] = w.beta[y];
@@ -1010,7 +1423,7 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         double* c2 = b.cstat2 + (int64_t)c * 4;
         c2[0] = (double)drift;
         c2[1] = trunc_total;
-        c2[2] = (double)t_loop;   // SM cycles spent in the Sinkhorn loop
+        c2[2] = t_loop_d;         // SM cycles spent in the Sinkhorn loop
         c2[3] = nsteps;           // Newton evaluations over all nodes and iterations
     }
 }
@@ -1364,28 +1777,115 @@ extern "C" int64_t dd_cell_ws_size(int nw0, int nw1, int ny0, int ny1) {
     return dd::ws_layout(nw0, nw1, ny0, ny1).total;
 }
 
-extern "C" int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream) {
-    if (b->n_cells <= 0) return 0;
-    cudaStream_t st = (cudaStream_t)stream;
+static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch* b,
+                             cudaStream_t st, cudaStream_t st_big, int n_big,
+                             const int32_t* clu_ids, int n_clu, int clu_size, int clu_smem) {
     const int smem = b->smem_mode ? b->smem_bytes : 0;
     static thread_local int configured = -1;
+    static thread_local bool big_configured = false;
+    static thread_local int clu_configured = -1;
     if (smem > configured) {
         // opt in to the full per-block budget minus the kernel's static shared memory
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel);
+        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel<0>);
         if (e != cudaSuccess) return dd_set_error(e);
         const int avail = optin - (int)fa.sharedSizeBytes;
         if (smem > avail) return dd_set_error(cudaErrorInvalidValue);
-        e = cudaFuncSetAttribute(dd::cell_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 avail);
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
         if (e != cudaSuccess) return dd_set_error(e);
         configured = avail;
     }
-    dd::cell_solve_kernel<<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+    if (!big_configured) {
+        cudaError_t e = cudaFuncSetAttribute(dd::cell_solve_kernel<1>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxL1);
+        if (e != cudaSuccess) return dd_set_error(e);
+        big_configured = true;
+    }
+    if (n_clu > 0 && clu_smem > clu_configured) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa;
+        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_loop_cluster_kernel);
+        if (e != cudaSuccess) return dd_set_error(e);
+        const int avail = optin - (int)fa.sharedSizeBytes;
+        if (clu_smem > avail) return dd_set_error(cudaErrorInvalidValue);
+        e = cudaFuncSetAttribute(dd::cell_loop_cluster_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
+        if (e != cudaSuccess) return dd_set_error(e);
+        e = cudaFuncSetAttribute(dd::cell_loop_cluster_kernel,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return dd_set_error(e);
+        clu_configured = avail;
+    }
+    auto launch_big = [&](cudaStream_t sb) -> cudaError_t {
+        if (n_clu > 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(n_clu * clu_size), 1, 1);
+            cfg.blockDim = dim3(DD_NT, 1, 1);
+            cfg.dynamicSmemBytes = (size_t)clu_smem;
+            cfg.stream = sb;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)clu_size;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, dd::cell_loop_cluster_kernel, *g, *s, *b,
+                                               clu_ids);
+            if (e != cudaSuccess) return e;
+        }
+        dd::cell_solve_kernel<1><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
+        return cudaGetLastError();
+    };
+    if (n_big > 0 && st_big != nullptr && st_big != st) {
+        // big cells on the side stream, ordered after everything already on st and
+        // joined back before anything enqueued on st afterwards
+        static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+        if (!ev_fork) {
+            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+        }
+        cudaEventRecord(ev_fork, st);
+        cudaStreamWaitEvent(st_big, ev_fork, 0);
+        cudaError_t e = launch_big(st_big);
+        if (e != cudaSuccess) return dd_set_error(e);
+        if (b->smem_mode) dd::cell_solve_kernel<0><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return dd_set_error(e);
+        cudaEventRecord(ev_join, st_big);
+        cudaStreamWaitEvent(st, ev_join, 0);
+        return dd_set_error(cudaGetLastError());
+    }
+    if (b->smem_mode) dd::cell_solve_kernel<0><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+    if (n_big > 0) {
+        cudaError_t e = launch_big(st);
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
     return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int64_t dd_cell_cluster_ws(int nw0, int nw1, int ny0, int ny1, int clu_size) {
+    return dd::clu_layout(nw0, nw1, ny0, ny1, (ny0 + clu_size - 1) / clu_size + 1).total;
+}
+
+extern "C" int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream) {
+    if (b->n_cells <= 0) return 0;
+    return cell_solve_launch(g, s, b, (cudaStream_t)stream, nullptr, 1, nullptr, 0, 1, 0);
+}
+
+extern "C" int dd_cell_solve2(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream,
+                              void* stream_big, int n_big, const int32_t* clu_ids, int n_clu,
+                              int clu_size, int clu_smem) {
+    if (b->n_cells <= 0) return 0;
+    return cell_solve_launch(g, s, b, (cudaStream_t)stream, (cudaStream_t)stream_big, n_big,
+                             clu_ids, n_clu, clu_size, clu_smem);
 }
 
 extern "C" int dd_cell_delta(const dd_geom* g, const dd_state* s, const dd_batch* b, double* dy,

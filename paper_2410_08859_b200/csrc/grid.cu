@@ -345,13 +345,15 @@ __global__ void __launch_bounds__(DD_NT) cut_plan_kernel(dd_geom g, dd_state s,
     rmax = block_max_i(rmax, redi);
     cmin = block_min_i(cmin, redi);
     cmax = block_max_i(cmax, redi);
-    for (int k = 0; k < bs; ++k) {
-        const double v = block_sum(k < nxn ? xacc[k] : 0.0, red);
-        if (threadIdx.x == 0) s.x_marg[(int64_t)i * bs + k] = 0.0;
-        __syncthreads();
-        if (threadIdx.x == 0 && k < nxn) s.x_marg[(int64_t)i * bs + xs_t[k]] = v;
-        __syncthreads();
+    // zero the block first: retained nodes are a subsequence, so zeroing slot k
+    // while scattering xs_t[k] >= k would wipe earlier writes
+    for (int k = threadIdx.x; k < bs; k += DD_NT) s.x_marg[(int64_t)i * bs + k] = 0.0;
+    __syncthreads();
+    for (int k = 0; k < nxn; ++k) {
+        const double v = block_sum(xacc[k], red);
+        if (threadIdx.x == 0) s.x_marg[(int64_t)i * bs + xs_t[k]] = v;
     }
+    __syncthreads();
     int ne0 = 0, ne1 = 0;
     if (rmax >= 0) { ne0 = rmax - rmin + 1; ne1 = cmax - cmin + 1; }
     if (threadIdx.x == 0) {

@@ -56,6 +56,23 @@ import os as _os
 # kernel's ~3 KB of static shared memory); DD_FORCE_GLOBAL_WS=1 forces the
 # global-memory workspace path (used by the tests to cover it)
 SMEM_LIMIT = 0 if _os.environ.get("DD_FORCE_GLOBAL_WS") == "1" else 220 * 1024
+CLUSTER_SMEM = 220 * 1024
+CLUSTER_SIZES = (2, 4, 8, 16)
+# test switches: DD_FORCE_CLUSTER=C runs every cell through the cluster kernel
+# with C CTAs; DD_NO_CLUSTER=1 keeps large cells on the single-CTA global path
+_FORCE_CLUSTER = int(_os.environ.get("DD_FORCE_CLUSTER", "0") or 0)
+_NO_CLUSTER = _os.environ.get("DD_NO_CLUSTER") == "1"
+
+
+def _cluster_ws(nw0: int, nw1: int, ny0: np.ndarray, ny1: np.ndarray, C: int) -> np.ndarray:
+    """dd_cell_cluster_ws, vectorized (mirrors clu_layout in csrc/cell.cu)."""
+    nx = nw0 * nw1
+    rows = (ny0 + C - 1) // C + 1
+    nyl = rows * ny1
+    wsz = np.maximum(np.maximum(np.maximum(nw1 * ny0, ny1 * nw0), nx), nyl)
+    rm = np.maximum(np.maximum(ny0, ny1), max(nw0, nw1))
+    return (nw0 + nw1 + ny0 + ny1 + 6 * nx + 3 * nyl + nw0 * ny0 + nw1 * ny1 + rows * nw1
+            + 2 * nx + nw0 * ny1 + wsz + nw1 * ny0 + rm)
 MAX_MEMBERS = 64
 
 
@@ -461,6 +478,24 @@ def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta:
 
 
 _TABLE_CACHE: dict = {}
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device):
+    """Second stream for the large-window cells of a batch (one per device)."""
+    import torch
+
+    key = str(device)
+    s = _SIDE_STREAMS.get(key)
+    if s is None:
+        s = torch.cuda.Stream(device=device)
+        _SIDE_STREAMS[key] = s
+    return s
+
+
+def C_void(v):
+    import ctypes
+    return ctypes.c_void_p(v)
 
 
 def _tables(part: CompositePartition) -> _PartTables:
@@ -512,11 +547,30 @@ class _Batch:
         xoff = np.concatenate([[0], np.cumsum(nmem * st.bs)[:-1]]).astype(np.int64)
         ws = _ws_total(pt.nw0, pt.nw1, ny0, ny1).astype(np.int64)
         fits = ws * 8 <= SMEM_LIMIT
+        if _FORCE_CLUSTER:
+            fits = np.zeros_like(fits)
         # cells whose workspace fits run in shared memory (sized for the largest
         # of them); the rest get global-arena slots
         smem_bytes = int(ws[fits].max()) * 8 if fits.any() else 0
         smem_mode = bool(fits.any())
         gws = np.where(fits, 0, ws)
+        self.n_big = int((~fits).sum())
+        # large cells: Sinkhorn loop on a thread-block cluster when one fits
+        big = ~fits
+        clu = np.zeros(n, dtype=bool)
+        self.clu_size = 1
+        self.clu_smem = 0
+        if big.any() and not _NO_CLUSTER:
+            sizes = (_FORCE_CLUSTER,) if _FORCE_CLUSTER else CLUSTER_SIZES
+            for C in sizes:
+                cws = _cluster_ws(pt.nw0, pt.nw1, ny0, ny1, C) * 8
+                ok = big & (cws <= CLUSTER_SMEM) & (ny0 >= C)
+                if ok.any() and (ok == big).all() or C == sizes[-1]:
+                    clu = ok
+                    self.clu_size = C
+                    self.clu_smem = int(cws[ok].max()) if ok.any() else 0
+                    break
+        self.n_clu = int(clu.sum())
         woff = np.concatenate([[0], np.cumsum(gws)[:-1]]).astype(np.int64)
         desc = np.zeros((n, 12), dtype=np.int32)
         desc[:, 0] = ids
@@ -524,6 +578,7 @@ class _Batch:
         desc[:, 5:9] = yb
         desc[:, 9] = nmem
         desc[:, 10] = membase
+        desc[:, 11] = clu.astype(np.int32)
         offs = np.stack([yoff, moff, woff, xoff], axis=1).astype(np.int64)
         mflat = np.concatenate(members).astype(np.int32) if n else np.zeros(0, np.int32)
         self.mflat = mflat
@@ -545,6 +600,10 @@ class _Batch:
         self.beta = B.get("beta", tot_y, f64)
         self.mdens = B.get("mdens", tot_y, f64)
         self.lnuw = B.get("lnuw", tot_y, f64)
+        self.lout = B.get("lout", n * pt.nw0 * pt.nw1, f64)
+        clu_ids = np.flatnonzero(clu).astype(np.int32)
+        self.clu_ids = (torch.from_numpy(clu_ids).to(dev) if len(clu_ids)
+                        else B.get("clu_ids", 1, i32))
         self.marena = B.get("marena", tot_m, f64)
         self.work = B.get("work", int(gws.sum()) + 1, f64)
         self.xarena = B.get("xarena", tot_mem * st.bs, f64)
@@ -564,13 +623,20 @@ class _Batch:
             cstat=self.cstat.data_ptr(), cstat2=self.cstat2.data_ptr(),
             smem_mode=1 if smem_mode else 0, smem_bytes=smem_bytes if smem_mode else 0,
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
-            newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr())
+            newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
+            lout=self.lout.data_ptr())
         self.cfg = cfg
 
     def solve(self):
+        import torch
+
         st = self.st
-        _lib.check(_lib.lib().dd_cell_solve(st.dp.geom, st.state_struct(self.store), self.batch,
-                                            _lib.stream_handle()))
+        n_big = int(self.n_big)
+        side = C_void(_side_stream(st.dp.device).cuda_stream) if n_big else None
+        _lib.check(_lib.lib().dd_cell_solve2(st.dp.geom, st.state_struct(self.store), self.batch,
+                                             _lib.stream_handle(), side, n_big,
+                                             self.clu_ids.data_ptr(), self.n_clu, self.clu_size,
+                                             self.clu_smem))
 
     def stats(self):
         c1 = self.cstat[:self.n * 8].view(self.n, 8).cpu().numpy()

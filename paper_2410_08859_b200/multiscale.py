@@ -81,8 +81,11 @@ def build_pyramid(mu: GridMeasure, nu: GridMeasure, n_min: int) -> list:
     return levels
 
 
-def eps_schedule(levels: list, eps_start: float, eps_final: float) -> list:
-    """Per level, the eps values it solves (halving ladder eps_start -> eps_final)."""
+def eps_schedule(levels: list, eps_start: float, eps_final: float, final_stages: int = 1) -> list:
+    """Per level, the eps values it solves (halving ladder eps_start -> eps_final).
+
+    The last ``final_stages`` ladder values always run on the finest level.
+    """
     ladder = []
     e = float(eps_start)
     while e > eps_final * (1.0 + 1e-12):
@@ -91,7 +94,7 @@ def eps_schedule(levels: list, eps_start: float, eps_final: float) -> list:
     ladder.append(float(eps_final))
     per = [[] for _ in levels]
     for k, e in enumerate(ladder):
-        if k == len(ladder) - 1:
+        if k >= len(ladder) - max(1, final_stages):
             per[-1].append(e)
             continue
         idx = len(levels) - 1
@@ -204,7 +207,8 @@ def _with_eps(lv: Level, lam_div, eps: float) -> TransportProblem:
 def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int, eps_start: float,
                      eps_final: float | None = None, strategy: StrategyConfig = StrategyConfig(),
                      config: EngineConfig = EngineConfig(), warm_delta: float = 1e-3,
-                     warm_max_iters: int = 20_000, progress=None, levels: list | None = None):
+                     warm_max_iters: int = 20_000, progress=None, levels: list | None = None,
+                     final_stages: int = 1):
     """Solve ``problem`` coarse-to-fine; returns (fine PlanState, MultiscaleReport).
 
     ``levels`` may carry a pre-built (and device-staged) pyramid from
@@ -214,7 +218,7 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
     eps_final = problem.eps if eps_final is None else eps_final
     if levels is None:
         levels = build_pyramid(problem.mu, problem.nu, n_coarsest)
-    sched = eps_schedule(levels, eps_start, eps_final)
+    sched = eps_schedule(levels, eps_start, eps_final, final_stages)
     rep = MultiscaleReport(converged=True)
     state = None
     duals = None

@@ -7,6 +7,7 @@ from paper_2410_08859_b200.problems import config_problem_arrays
 import paper_2410_08859_b200.engine as E
 import paper_2410_08859_b200.multiscale as M
 idx, level, iters_at_level = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+final_stages = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 mu, nu, dx, org, cfg = config_problem_arrays(idx, seed=0)
 h2 = dx*dx
 grid = Grid(mu.shape, dx, org)
@@ -36,4 +37,4 @@ def dd(problem, dec, strategy, config, state=None, evaluator=None):
         raise SystemExit(0)
     return st, r
 M.domdec_solve = dd
-M.multiscale_solve(prob, cfg["cell"], cfg["coarsest"], cfg["eps_start_h2"]*h2)
+M.multiscale_solve(prob, cfg["cell"], cfg["coarsest"], cfg["eps_start_h2"]*h2, final_stages=final_stages)

@@ -49,3 +49,13 @@ def test_product_path_refuses_without_device():
         pytest.skip("a device is visible")
     with pytest.raises(_lib.LibraryError):
         _lib.lib()
+
+
+def test_cluster_workspace_layout_matches_python_mirror():
+    from paper_2410_08859_b200 import _lib
+    from paper_2410_08859_b200.engine import _cluster_ws
+
+    h = _lib.load()
+    for nw0, nw1, ny0, ny1, c in [(16, 16, 140, 150, 8), (8, 8, 30, 40, 2), (16, 16, 33, 17, 16)]:
+        assert h.dd_cell_cluster_ws(nw0, nw1, ny0, ny1, c) == int(
+            _cluster_ws(nw0, nw1, np.array([ny0]), np.array([ny1]), c)[0])
