@@ -206,6 +206,10 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
                 if (nstat) nstat[1] += 1;
             }
         }
+        // fixed point of the iteration (the step is below half an ulp of b): every
+        // further pass of the reference loop recomputes the same g and step and
+        // leaves b unchanged until max_iters, so stopping here returns the same b
+        if (nb == b) break;
         b = nb;
     }
     if (nstat) {
