@@ -151,15 +151,17 @@ int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* 
 
 /* As dd_cell_solve, with the cells whose workspace does not fit shared memory
  * (n_big of them) handled on stream_big, concurrently with the shared-memory
- * cells on `stream` (joined back before return).  Of those, the n_clu cells
- * listed in clu_ids (device int32; their desc flags bit 0 set) run their
- * Sinkhorn loop on a thread-block cluster of clu_size CTAs (clu_smem bytes of
- * shared memory each, rows of the Y window split across the cluster); every
- * big cell then goes through the global-workspace kernel variant (max-L1
- * carveout), epilogue only for the cluster-solved ones. */
+ * cells on `stream` (joined back before return).  Of those, the cells listed
+ * in clu_ids (device int32; their desc flags bit 0 set) run their Sinkhorn
+ * loop on thread-block clusters, rows of the Y window split across the
+ * cluster: host arrays goff[n_groups+1], gsize[n_groups], gsmem[n_groups]
+ * give, per launch group, the slice of clu_ids, the cluster size (2..16) and
+ * the shared memory per CTA.  Every big cell then goes through the
+ * global-workspace kernel variant (max-L1 carveout), epilogue only for the
+ * cluster-solved ones. */
 int dd_cell_solve2(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream,
-                   void* stream_big, int n_big, const int32_t* clu_ids, int n_clu, int clu_size,
-                   int clu_smem);
+                   void* stream_big, int n_big, const int32_t* clu_ids, int n_groups,
+                   const int32_t* goff, const int32_t* gsize, const int32_t* gsmem);
 
 /* Shared-memory doubles per CTA of the cluster variant. */
 int64_t dd_cell_cluster_ws(int nw0, int nw1, int ny0, int ny1, int clu_size);

@@ -62,7 +62,7 @@ _SIGS = {
                         C.c_int),
     "dd_cell_solve": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp], C.c_int),
     "dd_cell_solve2": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, C.c_int, vp,
-                        C.c_int, C.c_int, C.c_int], C.c_int),
+                        C.c_int, vp, vp, vp], C.c_int),
     "dd_cell_cluster_ws": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], i64),
     "dd_cell_delta": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp], C.c_int),
     "dd_blend_energy": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp,

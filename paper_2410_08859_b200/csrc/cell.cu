@@ -1777,13 +1777,36 @@ extern "C" int64_t dd_cell_ws_size(int nw0, int nw1, int ny0, int ny1) {
     return dd::ws_layout(nw0, nw1, ny0, ny1).total;
 }
 
+static int cluster_configure(int clu_smem) {
+    static thread_local int clu_configured = -1;
+    if (clu_smem <= clu_configured) return 0;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_loop_cluster_kernel);
+    if (e != cudaSuccess) return dd_set_error(e);
+    const int avail = optin - (int)fa.sharedSizeBytes;
+    if (clu_smem > avail) return dd_set_error(cudaErrorInvalidValue);
+    e = cudaFuncSetAttribute(dd::cell_loop_cluster_kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
+    if (e != cudaSuccess) return dd_set_error(e);
+    e = cudaFuncSetAttribute(dd::cell_loop_cluster_kernel,
+                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return dd_set_error(e);
+    clu_configured = avail;
+    return 0;
+}
+
+// groups: n_groups cluster launches; group k covers clu_ids[goff[k] .. goff[k+1])
+// with cluster size gsize[k] and gsmem[k] bytes of shared memory per CTA.
 static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch* b,
                              cudaStream_t st, cudaStream_t st_big, int n_big,
-                             const int32_t* clu_ids, int n_clu, int clu_size, int clu_smem) {
+                             const int32_t* clu_ids, int n_groups, const int32_t* goff,
+                             const int32_t* gsize, const int32_t* gsmem) {
     const int smem = b->smem_mode ? b->smem_bytes : 0;
     static thread_local int configured = -1;
     static thread_local bool big_configured = false;
-    static thread_local int clu_configured = -1;
     if (smem > configured) {
         // opt in to the full per-block budget minus the kernel's static shared memory
         int dev = 0, optin = 0;
@@ -1806,39 +1829,28 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
         if (e != cudaSuccess) return dd_set_error(e);
         big_configured = true;
     }
-    if (n_clu > 0 && clu_smem > clu_configured) {
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_loop_cluster_kernel);
-        if (e != cudaSuccess) return dd_set_error(e);
-        const int avail = optin - (int)fa.sharedSizeBytes;
-        if (clu_smem > avail) return dd_set_error(cudaErrorInvalidValue);
-        e = cudaFuncSetAttribute(dd::cell_loop_cluster_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
-        if (e != cudaSuccess) return dd_set_error(e);
-        e = cudaFuncSetAttribute(dd::cell_loop_cluster_kernel,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return dd_set_error(e);
-        clu_configured = avail;
+    for (int k = 0; k < n_groups; ++k) {
+        const int rc = cluster_configure(gsmem[k]);
+        if (rc) return rc;
     }
     auto launch_big = [&](cudaStream_t sb) -> cudaError_t {
-        if (n_clu > 0) {
+        for (int k = 0; k < n_groups; ++k) {
+            const int ncl = goff[k + 1] - goff[k];
+            if (ncl <= 0) continue;
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)(n_clu * clu_size), 1, 1);
+            cfg.gridDim = dim3((unsigned)(ncl * gsize[k]), 1, 1);
             cfg.blockDim = dim3(DD_NT, 1, 1);
-            cfg.dynamicSmemBytes = (size_t)clu_smem;
+            cfg.dynamicSmemBytes = (size_t)gsmem[k];
             cfg.stream = sb;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = (unsigned)clu_size;
+            attr[0].val.clusterDim.x = (unsigned)gsize[k];
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             cudaError_t e = cudaLaunchKernelEx(&cfg, dd::cell_loop_cluster_kernel, *g, *s, *b,
-                                               clu_ids);
+                                               clu_ids + goff[k]);
             if (e != cudaSuccess) return e;
         }
         dd::cell_solve_kernel<1><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
@@ -1877,15 +1889,16 @@ extern "C" int64_t dd_cell_cluster_ws(int nw0, int nw1, int ny0, int ny1, int cl
 
 extern "C" int dd_cell_solve(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream) {
     if (b->n_cells <= 0) return 0;
-    return cell_solve_launch(g, s, b, (cudaStream_t)stream, nullptr, 1, nullptr, 0, 1, 0);
+    return cell_solve_launch(g, s, b, (cudaStream_t)stream, nullptr, 1, nullptr, 0, nullptr,
+                             nullptr, nullptr);
 }
 
 extern "C" int dd_cell_solve2(const dd_geom* g, const dd_state* s, const dd_batch* b, void* stream,
-                              void* stream_big, int n_big, const int32_t* clu_ids, int n_clu,
-                              int clu_size, int clu_smem) {
+                              void* stream_big, int n_big, const int32_t* clu_ids, int n_groups,
+                              const int32_t* goff, const int32_t* gsize, const int32_t* gsmem) {
     if (b->n_cells <= 0) return 0;
     return cell_solve_launch(g, s, b, (cudaStream_t)stream, (cudaStream_t)stream_big, n_big,
-                             clu_ids, n_clu, clu_size, clu_smem);
+                             clu_ids, n_groups, goff, gsize, gsmem);
 }
 
 extern "C" int dd_cell_delta(const dd_geom* g, const dd_state* s, const dd_batch* b, double* dy,

@@ -555,21 +555,26 @@ class _Batch:
         smem_mode = bool(fits.any())
         gws = np.where(fits, 0, ws)
         self.n_big = int((~fits).sum())
-        # large cells: Sinkhorn loop on a thread-block cluster when one fits
+        # large cells: Sinkhorn loop on a thread-block cluster, each cell on the
+        # smallest cluster (2, 4, 8, 16 CTAs) whose per-CTA workspace fits;
+        # one launch per cluster size
         big = ~fits
         clu = np.zeros(n, dtype=bool)
-        self.clu_size = 1
-        self.clu_smem = 0
+        csize = np.zeros(n, dtype=np.int64)
+        csmem = np.zeros(n, dtype=np.int64)
         if big.any() and not _NO_CLUSTER:
             sizes = (_FORCE_CLUSTER,) if _FORCE_CLUSTER else CLUSTER_SIZES
             for C in sizes:
                 cws = _cluster_ws(pt.nw0, pt.nw1, ny0, ny1, C) * 8
-                ok = big & (cws <= CLUSTER_SMEM) & (ny0 >= C)
-                if ok.any() and (ok == big).all() or C == sizes[-1]:
-                    clu = ok
-                    self.clu_size = C
-                    self.clu_smem = int(cws[ok].max()) if ok.any() else 0
-                    break
+                ok = big & ~clu & (cws <= CLUSTER_SMEM) & (ny0 >= C)
+                csize[ok] = C
+                csmem[ok] = cws[ok]
+                clu |= ok
+        groups = []
+        for C in sorted(set(csize[clu].tolist())):
+            sel = np.flatnonzero(clu & (csize == C))
+            groups.append((int(C), sel, int(csmem[sel].max())))
+        self.clu_groups = groups
         self.n_clu = int(clu.sum())
         woff = np.concatenate([[0], np.cumsum(gws)[:-1]]).astype(np.int64)
         desc = np.zeros((n, 12), dtype=np.int32)
@@ -601,9 +606,17 @@ class _Batch:
         self.mdens = B.get("mdens", tot_y, f64)
         self.lnuw = B.get("lnuw", tot_y, f64)
         self.lout = B.get("lout", n * pt.nw0 * pt.nw1, f64)
-        clu_ids = np.flatnonzero(clu).astype(np.int32)
+        clu_ids = (np.concatenate([sel for _, sel, _ in groups]).astype(np.int32) if groups
+                   else np.zeros(0, np.int32))
         self.clu_ids = (torch.from_numpy(clu_ids).to(dev) if len(clu_ids)
                         else B.get("clu_ids", 1, i32))
+        import ctypes
+        ng = len(groups)
+        goff = np.concatenate([[0], np.cumsum([len(sel) for _, sel, _ in groups])]).astype(np.int32)
+        self.clu_n_groups = ng
+        self.clu_goff = (ctypes.c_int32 * (ng + 1))(*goff.tolist())
+        self.clu_gsize = (ctypes.c_int32 * max(1, ng))(*[C for C, _, _ in groups])
+        self.clu_gsmem = (ctypes.c_int32 * max(1, ng))(*[m for _, _, m in groups])
         self.marena = B.get("marena", tot_m, f64)
         self.work = B.get("work", int(gws.sum()) + 1, f64)
         self.xarena = B.get("xarena", tot_mem * st.bs, f64)
@@ -635,8 +648,8 @@ class _Batch:
         side = C_void(_side_stream(st.dp.device).cuda_stream) if n_big else None
         _lib.check(_lib.lib().dd_cell_solve2(st.dp.geom, st.state_struct(self.store), self.batch,
                                              _lib.stream_handle(), side, n_big,
-                                             self.clu_ids.data_ptr(), self.n_clu, self.clu_size,
-                                             self.clu_smem))
+                                             self.clu_ids.data_ptr(), self.clu_n_groups,
+                                             self.clu_goff, self.clu_gsize, self.clu_gsmem))
 
     def stats(self):
         c1 = self.cstat[:self.n * 8].view(self.n, 8).cpu().numpy()

@@ -18,7 +18,7 @@ for mode in (0, 2):
     pt = E._tables(dec.composites[0])
     snap = st.assemble_device()
     bt = E._Batch(st, pt, pt.batches[0], snap, E.EngineConfig(delta=float(g["delta"])).cell_config())
-    print("mode", mode, "n_clu", bt.n_clu, "clu_size", bt.clu_size, "n_big", bt.n_big, "smem", bt.batch.smem_mode)
+    print("mode", mode, "n_clu", bt.n_clu, "groups", [(C, len(sel)) for C, sel, _ in bt.clu_groups], "n_big", bt.n_big, "smem", bt.batch.smem_mode)
     bt.solve()
     torch.cuda.synchronize()
     c1, c2 = bt.stats()
