@@ -163,6 +163,9 @@ int dd_cell_solve2(const dd_geom* g, const dd_state* s, const dd_batch* b, void*
                    void* stream_big, int n_big, const int32_t* clu_ids, int n_groups,
                    const int32_t* goff, const int32_t* gsize, const int32_t* gsmem);
 
+/* Minimum resident cell CTAs per SM the library was built for (1 or 2). */
+int dd_cell_min_blocks(void);
+
 /* Shared-memory doubles per CTA of the cluster variant. */
 int64_t dd_cell_cluster_ws(int nw0, int nw1, int ny0, int ny1, int clu_size);
 

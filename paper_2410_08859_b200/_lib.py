@@ -12,7 +12,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdomdec_b200.so")
+# DD_LIB_PATH selects an alternative build of the same library (debug/profiling variants)
+LIB_PATH = os.environ.get("DD_LIB_PATH") or os.path.join(_HERE, "libdomdec_b200.so")
 
 EXPORTS = [
     "dd_last_error", "dd_device_count", "dd_abi_version", "dd_grid_lse", "dd_axpb",
@@ -20,7 +21,7 @@ EXPORTS = [
     "dd_cell_commit", "dd_assemble", "dd_energy_terms", "dd_product_init", "dd_cut_plan",
     "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
     "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong", "dd_refine_dual",
-    "dd_cell_solve2", "dd_cell_cluster_ws",
+    "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -64,6 +65,7 @@ _SIGS = {
     "dd_cell_solve2": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, C.c_int, vp,
                         C.c_int, vp, vp, vp], C.c_int),
     "dd_cell_cluster_ws": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int], i64),
+    "dd_cell_min_blocks": ([], C.c_int),
     "dd_cell_delta": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp], C.c_int),
     "dd_blend_energy": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp,
                          vp, vp], C.c_int),
@@ -162,7 +164,8 @@ class _Traced:
         t = _tracer
         if t is None or not name.startswith("dd_") or name in ("dd_last_error", "dd_device_count",
                                                                "dd_abi_version", "dd_cell_ws_size",
-                                                               "dd_cell_cluster_ws"):
+                                                               "dd_cell_cluster_ws",
+                                                               "dd_cell_min_blocks"):
             return fn
 
         def call(*args):

@@ -15,6 +15,12 @@
 #include "common.cuh"
 #include "domdec_b200.h"
 
+// minimum resident cell CTAs per SM (2 caps registers at 64 so two 512-thread
+// cell CTAs can share an SM; the host then halves the shared-memory budget)
+#ifndef DD_CELL_MIN_BLOCKS
+#define DD_CELL_MIN_BLOCKS 1
+#endif
+
 namespace dd {
 
 struct CellWin {
@@ -430,7 +436,7 @@ __device__ __forceinline__ int clu_row0(int ny0, int C, int rank) {
     return (int)(((int64_t)ny0 * rank) / C);
 }
 
-__global__ void __launch_bounds__(DD_NT, 1) cell_loop_cluster_kernel(dd_geom g, dd_state s,
+__global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_kernel(dd_geom g, dd_state s,
                                                                      dd_batch b,
                                                                      const int32_t* ids) {
     namespace cgx = cooperative_groups;
@@ -454,9 +460,8 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_loop_cluster_kernel(dd_geom g, 
     const int nx = cw.nx, ny0 = cw.ye0, ny1 = cw.ye1;
     const int r0 = clu_row0(ny0, C, rank), r1 = clu_row0(ny0, C, rank + 1);
     const int rows = r1 - r0;
-    const int rows_max = clu_row0(ny0, C, 1) + 1;   // upper bound used for the layout
+    // layout sized for the largest row slice (identical in every CTA of the cluster)
     const CluLayout lay = clu_layout(nw0, nw1, ny0, ny1, (ny0 + C - 1) / C + 1);
-    (void)rows_max;
     double* xc0 = smem + lay.xc0;
     double* xc1 = smem + lay.xc1;
     double* yc0 = smem + lay.yc0;
@@ -761,11 +766,11 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_loop_cluster_kernel(dd_geom g, 
 //          compiled as a separate function so it can run with a max-L1
 //          carveout on a second stream, concurrently with pass 0.
 template <int kPass>
-__global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
+__global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
+    cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
     extern __shared__ double smem[];
     __shared__ double red[DD_NW + 1];
     __shared__ int redi[DD_NW + 1];
-    __shared__ double sh_sc[16];
     __shared__ int sh_flag[4];
 
     const int c = blockIdx.x;
@@ -883,7 +888,6 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
         int nst[4] = {0, 0, 0, 0};   // clips, bisections, max evals, nodes with >= 6 evals
     #endif
         long long newton_steps = 0;
-        const double inv_lam = 1.0 / lam;
         __shared__ double red2[2 * DD_NW];
         __shared__ double redm[2 * DD_NW];
         __shared__ int sweep_flag;
@@ -926,13 +930,34 @@ __global__ void __launch_bounds__(DD_NT, 1) cell_solve_kernel(dd_geom g, dd_stat
             int ndeg = 0;
             for (int y = tid; y < ny; y += DD_NT) {
                 int dg = 0;
-    #ifdef DD_NEWTON_STATS
+#if defined(DD_NEWTON_STATS)
                 w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
                                         b.newton_max_iters, &dg, &newton_steps, nst);
-    #else
+#elif defined(DD_NEWTON_PAIR)
+                const int y2 = y + DD_NT;
+                if (y2 < ny) {
+                    NewtonState sa, sb;
+                    double oa = 0.0, ob = 0.0;
+                    newton_init(sa, w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, &oa, &dg);
+                    newton_init(sb, w.ty[y2], w.m[y2], has_m, w.beta[y2], eps, lam, &ob, &dg);
+                    const double ie = 1.0 / eps, il = 1.0 / lam;
+                    while (!(sa.done && sb.done)) {
+                        newton_step(sa, ie, il, b.newton_tol, b.newton_max_iters, &oa,
+                                    &newton_steps);
+                        newton_step(sb, ie, il, b.newton_tol, b.newton_max_iters, &ob,
+                                    &newton_steps);
+                    }
+                    w.beta[y] = oa;
+                    w.beta[y2] = ob;
+                    y += DD_NT;   // the loop's own increment then skips past y2
+                } else {
+                    w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam,
+                                            b.newton_tol, b.newton_max_iters, &dg, &newton_steps);
+                }
+#else
                 w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
                                         b.newton_max_iters, &dg, &newton_steps);
-    #endif
+#endif
                 ndeg += dg;
             }
             const int cur = k & 1;
@@ -1974,3 +1999,5 @@ extern "C" int dd_debug_fallbacks(unsigned long long* out) {
     return 0;
 }
 #endif
+
+extern "C" int dd_cell_min_blocks(void) { return DD_CELL_MIN_BLOCKS; }

@@ -55,8 +55,17 @@ import os as _os
 # dynamic shared memory budget per CTA (227 KB opt-in on sm_100a minus the solve
 # kernel's ~3 KB of static shared memory); DD_FORCE_GLOBAL_WS=1 forces the
 # global-memory workspace path (used by the tests to cover it)
-SMEM_LIMIT = 0 if _os.environ.get("DD_FORCE_GLOBAL_WS") == "1" else 220 * 1024
-CLUSTER_SMEM = 220 * 1024
+def _occupancy() -> int:
+    try:
+        h = _lib.load()
+        return int(h.dd_cell_min_blocks())
+    except Exception:
+        return 1
+
+
+_OCC = _occupancy()
+SMEM_LIMIT = 0 if _os.environ.get("DD_FORCE_GLOBAL_WS") == "1" else (220 * 1024) // _OCC - 1024 * (_OCC - 1)
+CLUSTER_SMEM = (220 * 1024) // _OCC - 1024 * (_OCC - 1)
 CLUSTER_SIZES = (2, 4, 8, 16)
 # test switches: DD_FORCE_CLUSTER=C runs every cell through the cluster kernel
 # with C CTAs; DD_NO_CLUSTER=1 keeps large cells on the single-CTA global path
