@@ -107,6 +107,8 @@ typedef struct dd_batch {
     double trunc;
     double* lnuw;              /* y arena: log nu on each cell window (kernel scratch) */
     double* lout;              /* [n_cells*nxw0*nxw1] final X sweep of cluster-solved cells */
+    int32_t skip_stagnant;     /* 1: end a cell's loop at the cap as soon as an iteration
+                                  reproduces beta bitwise (exactly equivalent) */
 } dd_batch;
 
 const char* dd_last_error(void);

@@ -49,7 +49,8 @@ class Batch(C.Structure):
                 ("xarena", vp), ("mbox", vp), ("mstat", vp), ("cstat", vp), ("cstat2", vp),
                 ("smem_mode", i32), ("smem_bytes", i32),
                 ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
-                ("newton_tol", dbl), ("trunc", dbl), ("lnuw", vp), ("lout", vp)]
+                ("newton_tol", dbl), ("trunc", dbl), ("lnuw", vp), ("lout", vp),
+                ("skip_stagnant", i32)]
 
 
 _SIGS = {

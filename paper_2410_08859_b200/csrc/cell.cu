@@ -709,14 +709,25 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
             lse_stage(T2, ny1, nw0, K0 + r0, 1, ny0, rows, yc0 + r0, xc0, eps, W, ty, NoPrep());
         }
         int ndeg = 0;
+        int moved = 0;
         for (int yl = tid; yl < nyl; yl += DD_NT) {
             int dg = 0;
-            beta[yl] = newton_node(ty[yl], mg[yl], has_m, beta[yl], eps, lam, b.newton_tol,
-                                   b.newton_max_iters, &dg, &newton_steps);
+            const double ob = beta[yl];
+            const double nb = newton_node(ty[yl], mg[yl], has_m, ob, eps, lam, b.newton_tol,
+                                          b.newton_max_iters, &dg, &newton_steps);
+            moved |= (nb != ob) ? 1 : 0;
+            beta[yl] = nb;
             ndeg += dg;
         }
         newton_clamped = max(newton_clamped, (int)block_sum((double)ndeg, red));
         iters = k;
+        if (b.skip_stagnant && k >= 2) {
+            // cluster-wide: did any node's beta change?  (see the single-CTA kernel)
+            if (cmax((double)moved) == 0.0) {
+                iters = b.max_iters;
+                break;
+            }
+        }
     }
     __syncthreads();
     if (!converged) {
@@ -894,7 +905,8 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         int mpar = 0;
         const SweepScratch sc{redm, &sweep_flag, &mpar};
         __shared__ int ndeg_sh[2];
-        if (tid < 2) ndeg_sh[tid] = 0;
+        __shared__ int moved_sh[2];
+        if (tid < 2) { ndeg_sh[tid] = 0; moved_sh[tid] = 0; }
         int par = 0;
     #ifdef DD_PHASE_TIMING
         long long ph[4] = {0, 0, 0, 0};
@@ -928,12 +940,15 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
             cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
             DD_PH(2);
             int ndeg = 0;
+            bool moved = false;
             for (int y = tid; y < ny; y += DD_NT) {
                 int dg = 0;
 #if defined(DD_NEWTON_STATS)
+                moved = true;   // diagnostic build: no stagnation shortcut
                 w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
                                         b.newton_max_iters, &dg, &newton_steps, nst);
 #elif defined(DD_NEWTON_PAIR)
+                moved = true;   // variant build: no stagnation shortcut
                 const int y2 = y + DD_NT;
                 if (y2 < ny) {
                     NewtonState sa, sb;
@@ -955,19 +970,34 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
                                             b.newton_tol, b.newton_max_iters, &dg, &newton_steps);
                 }
 #else
-                w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
-                                        b.newton_max_iters, &dg, &newton_steps);
+                {
+                    const double ob = w.beta[y];
+                    const double nb = newton_node(w.ty[y], w.m[y], has_m, ob, eps, lam,
+                                                  b.newton_tol, b.newton_max_iters, &dg,
+                                                  &newton_steps);
+                    moved |= (nb != ob);
+                    w.beta[y] = nb;
+                }
 #endif
                 ndeg += dg;
             }
             const int cur = k & 1;
             if (ndeg) atomicAdd(&ndeg_sh[cur], ndeg);
+            if (moved) moved_sh[cur] = 1;
             __syncthreads();
             // the previous iteration's count is final here (ordered by this barrier)
             newton_clamped = max(newton_clamped, ndeg_sh[cur]);
-            if (tid == 0) ndeg_sh[cur ^ 1] = 0;
+            const bool any_moved = moved_sh[cur] != 0;
+            if (tid == 0) { ndeg_sh[cur ^ 1] = 0; moved_sh[cur ^ 1] = 0; }
             iters = k;
             DD_PH(3);
+            if (!any_moved && k >= 2 && b.skip_stagnant) {
+                // beta reproduced itself bitwise: every later iteration recomputes the
+                // same L, alpha, z and beta and fails the same gap test, so the loop
+                // would end at the cap in exactly this state (cells.py:320-348)
+                iters = b.max_iters;
+                break;
+            }
         }
     #ifdef DD_NEWTON_STATS
         {

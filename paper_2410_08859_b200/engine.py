@@ -646,7 +646,7 @@ class _Batch:
             smem_mode=1 if smem_mode else 0, smem_bytes=smem_bytes if smem_mode else 0,
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
-            lout=self.lout.data_ptr())
+            lout=self.lout.data_ptr(), skip_stagnant=0 if _os.environ.get("DD_NO_SKIP") == "1" else 1)
         self.cfg = cfg
 
     def solve(self):
