@@ -46,7 +46,8 @@ __all__ = [
     "Decomposition", "make_decomposition", "ScoreBreakdown", "CellDuals", "PlanState",
     "initial_plan_state", "warm_start_plan", "BlendScorer", "get_weights_safe",
     "get_weights_swift", "get_weights_opt", "StitchedGapEvaluator", "IterationStats",
-    "iteration_sequential", "iteration_parallel", "domdec_solve",
+    "iteration_sequential", "iteration_parallel", "domdec_solve", "ShardSpec", "set_shard",
+    "clear_shard",
 ]
 
 STRATEGY_KINDS = ("sequential", "safe", "fast", "swift", "opt", "staggered")
@@ -316,6 +317,8 @@ class PlanState:
         out = out if out is not None else self.dp.empty_y()
         _lib.check(_lib.lib().dd_assemble(self.dp.geom, self.state_struct(), out.data_ptr(),
                                           _lib.stream_handle()))
+        if _SHARD is not None and _SHARD.world > 1:
+            _SHARD.broadcast(out[:self.dp.ny])
         return out
 
     def energy_terms(self, y) -> np.ndarray:
@@ -486,6 +489,78 @@ def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta:
     return st
 
 
+class ShardSpec:
+    """Cell-sharded execution over a torch.distributed process group.
+
+    Every rank holds the full plan state and runs the identical control flow;
+    only the cell solves of each batch are partitioned (cost-balanced by window
+    size).  Each rank solves its own cells, the solve's output arenas (zero for
+    cells owned elsewhere) are summed across ranks (adding zeros is exact), and
+    everything downstream proceeds identically everywhere.  The two kernels
+    that accumulate with float atomics (the Y-marginal assembly and the blend
+    scatter) are not bitwise reproducible, so the assembled Y-marginal and the
+    weight decision are taken from rank 0 and broadcast; every other step is
+    deterministic, which keeps the ranks' states, window layouts and control
+    flow identical.
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def all_reduce_sum(self, t) -> None:
+        import torch.distributed as dist
+
+        if self.nccl:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        else:   # gloo: reduce through host memory
+            c = t.cpu()
+            dist.all_reduce(c, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(c)
+
+    def broadcast(self, t) -> None:
+        """Rank 0's values to every rank (in place)."""
+        import torch.distributed as dist
+
+        src = dist.get_global_rank(self.group, 0) if self.group is not None else 0
+        if self.nccl:
+            dist.broadcast(t, src=src, group=self.group)
+        else:
+            c = t.cpu()
+            dist.broadcast(c, src=src, group=self.group)
+            t.copy_(c)
+
+    def owners(self, cost: np.ndarray) -> np.ndarray:
+        """Greedy longest-processing-time assignment (deterministic on every rank)."""
+        order = np.argsort(-cost, kind="stable")
+        load = np.zeros(self.world)
+        own = np.empty(len(cost), dtype=np.int64)
+        for c in order:
+            r = int(np.argmin(load))
+            own[c] = r
+            load[r] += cost[c]
+        return own
+
+
+_SHARD: ShardSpec | None = None
+
+
+def set_shard(group=None) -> ShardSpec:
+    """Shard the cell solves of every batch over ``group`` (default: WORLD)."""
+    global _SHARD
+    _SHARD = ShardSpec(group)
+    return _SHARD
+
+
+def clear_shard() -> None:
+    global _SHARD
+    _SHARD = None
+
+
 _TABLE_CACHE: dict = {}
 _SIDE_STREAMS: dict = {}
 
@@ -579,6 +654,14 @@ class _Batch:
                 csize[ok] = C
                 csmem[ok] = cws[ok]
                 clu |= ok
+        # sharded solve: cells owned by other ranks are skipped (desc flag bit 1)
+        owned = np.ones(n, dtype=bool)
+        self.shard = _SHARD if (_SHARD is not None and _SHARD.world > 1) else None
+        if self.shard is not None:
+            cost = (ny.astype(np.float64) + 1.0) * (pt.nw0 * pt.nw1)
+            owned = self.shard.owners(cost) == self.shard.rank
+            clu &= owned
+        self.owned = owned
         groups = []
         for C in sorted(set(csize[clu].tolist())):
             sel = np.flatnonzero(clu & (csize == C))
@@ -592,7 +675,7 @@ class _Batch:
         desc[:, 5:9] = yb
         desc[:, 9] = nmem
         desc[:, 10] = membase
-        desc[:, 11] = clu.astype(np.int32)
+        desc[:, 11] = clu.astype(np.int32) | np.where(owned, 0, 2).astype(np.int32)
         offs = np.stack([yoff, moff, woff, xoff], axis=1).astype(np.int64)
         mflat = np.concatenate(members).astype(np.int32) if n else np.zeros(0, np.int32)
         self.mflat = mflat
@@ -634,6 +717,7 @@ class _Batch:
         self.cstat = B.get("cstat", n * 8, f64)
         self.cstat2 = B.get("cstat2", n * 4, f64)
         self.dy = None
+        self.tot = dict(y=tot_y, m=tot_m, mem=tot_mem)
         self.yoff = yoff
         self.snapshot = snapshot
         self.batch = _lib.Batch(
@@ -655,10 +739,23 @@ class _Batch:
         st = self.st
         n_big = int(self.n_big)
         side = C_void(_side_stream(st.dp.device).cuda_stream) if n_big else None
+        outs = None
+        if self.shard is not None:
+            n, nx, t = self.n, self.pt.nw0 * self.pt.nw1, self.tot
+            outs = [self.alpha[:n * nx], self.beta[:t["y"]], self.mdens[:t["y"]],
+                    self.lnuw[:t["y"]], self.marena[:t["m"]], self.xarena[:t["mem"] * st.bs],
+                    self.mbox[:t["mem"] * 4], self.mstat[:t["mem"] * 4], self.cstat[:n * 8],
+                    self.cstat2[:n * 4], self.lout[:n * nx]]
+            for o in outs:
+                o.zero_()
         _lib.check(_lib.lib().dd_cell_solve2(st.dp.geom, st.state_struct(self.store), self.batch,
                                              _lib.stream_handle(), side, n_big,
                                              self.clu_ids.data_ptr(), self.clu_n_groups,
                                              self.clu_goff, self.clu_gsize, self.clu_gsmem))
+        if outs is not None:
+            # every rank contributes its own cells (zeros elsewhere): exact sum
+            for o in outs:
+                self.shard.all_reduce_sum(o)
 
     def stats(self):
         c1 = self.cstat[:self.n * 8].view(self.n, 8).cpu().numpy()
@@ -1045,6 +1142,19 @@ def iteration_parallel(plan: PlanState, part: CompositePartition, strategy: Stra
                 theta = np.full(kb, 1.0 / kb)
                 actions.append("safe-fallback")
                 stats.safe_fallbacks += 1
+        if bt.shard is not None:
+            # one decision for all ranks (the blend energies use float atomics)
+            import torch
+            th = torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64)).to(plan.dp.device)
+            bt.shard.broadcast(th)
+            theta = th.cpu().numpy()
+            if strategy.kind == "staggered":
+                greedy = bool(np.all(theta == 1.0))
+                if actions[-1] == "safe-fallback" and greedy:
+                    stats.safe_fallbacks -= 1
+                if actions[-1] == "greedy" and not greedy:
+                    stats.safe_fallbacks += 1
+                actions[-1] = "greedy" if greedy else "safe-fallback"
         stats.score_time += time.perf_counter() - t0
         t0 = time.perf_counter()
         e = bt.commit(theta, ag, None)
