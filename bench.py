@@ -182,7 +182,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        # DD_DIST_BACKEND=gloo: functional multi-rank runs on fewer GPUs than ranks
+        backend = os.environ.get("DD_DIST_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
+        dist.init_process_group(backend)
     prob, cfg, eps_start = problem(args.config, args.seed)
     config_desc = {"workload": f"{args.config}: BASELINE configs[{CONFIGS[args.config]}] "
                                f"{prob.mu.grid.dims[0]}x{prob.mu.grid.dims[1]} multiscale "
@@ -223,7 +225,7 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     from paper_2410_08859_b200 import _lib
     from paper_2410_08859_b200.multiscale import build_pyramid, stage_pyramid
     if world > 1:
@@ -259,8 +261,9 @@ def main():
             reps.append(rep)
     launches = tracer.launches() // max(1, args.steps)
     # per-step time = the K timed steps' device time / K (max over ranks)
-    t_dev = max_over_ranks(float(np.sum(times)) / len(times), device="cuda")
-    t_max_step = max_over_ranks(float(np.max(times)), device="cuda")
+    red_dev = "cuda" if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu"
+    t_dev = max_over_ranks(float(np.sum(times)) / len(times), device=red_dev)
+    t_max_step = max_over_ranks(float(np.max(times)), device=red_dev)
     # ---- end-to-end through the public API (host arrays in, host result out)
     e2e_times = []
     h2d = 0
