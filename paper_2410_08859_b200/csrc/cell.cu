@@ -264,6 +264,10 @@ struct SweepScratch {
     double* redm;   // [2*DD_NW] block-max buffers
     int* flag;      // shared underflow flag
     int* par;       // block-max buffer parity
+#ifdef DD_PHASE_TIMING
+    long long* fb_cycles;   // [2] cycles spent in the staged fallback (X, Y)
+    int* fb_count;          // [2] number of fallback sweeps (X, Y)
+#endif
 };
 
 __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
@@ -313,7 +317,16 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     }
     if (bad) *sc.flag = 1;
     __syncthreads();
-    if (*sc.flag) cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+    if (*sc.flag) {
+#ifdef DD_PHASE_TIMING
+        const long long t0 = clock64();
+#endif
+        cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+#ifdef DD_PHASE_TIMING
+        sc.fb_cycles[0] += clock64() - t0;
+        sc.fb_count[0] += 1;
+#endif
+    }
 }
 
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
@@ -363,7 +376,16 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     if (bad) *sc.flag = 1;
     __syncthreads();
     // alpha is already updated; the staged redo must not apply the update twice
-    if (*sc.flag) cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
+    if (*sc.flag) {
+#ifdef DD_PHASE_TIMING
+        const long long t0 = clock64();
+#endif
+        cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
+#ifdef DD_PHASE_TIMING
+        sc.fb_cycles[1] += clock64() - t0;
+        sc.fb_count[1] += 1;
+#endif
+    }
 }
 
 // Value of a boxed marginal at absolute node (r, q); zero outside.
@@ -904,7 +926,13 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         __shared__ double redm[2 * DD_NW];
         __shared__ int sweep_flag;
         int mpar = 0;
+#ifdef DD_PHASE_TIMING
+        long long fbc[2] = {0, 0};
+        int fbn[2] = {0, 0};
+        const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn};
+#else
         const SweepScratch sc{redm, &sweep_flag, &mpar};
+#endif
         __shared__ int ndeg_sh[2];
         __shared__ int moved_sh[2];
         if (tid < 2) { ndeg_sh[tid] = 0; moved_sh[tid] = 0; }
@@ -1016,6 +1044,8 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     #endif
     #ifdef DD_PHASE_TIMING
         if (tid == 0) {
+            b.cstat2[(int64_t)c * 4 + 0] = (double)fbc[0] + (double)fbc[1];
+            b.cstat2[(int64_t)c * 4 + 1] = (double)fbn[0] * 1e6 + (double)fbn[1];
             b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
             b.cstat[(int64_t)c * 8 + 5] = (double)ph[1];
             b.cstat[(int64_t)c * 8 + 6] = (double)ph[2];
