@@ -166,10 +166,24 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
     if (!fz) return -lam * log(m);
     const double inv_eps = 1.0 / eps, inv_lam = 1.0 / lam;
     const double lm = log(m);
-    const double b1 = -lam * logaddexp(lm, z);
     const double b2 = -ratio * z;
-    double lo = fmin(b1, b2) - lam;
-    double hi = fmax(b1, b2) + lam;
+    // Safeguard bracket, evaluated lazily.  The computed logaddexp(lm, z) lies in
+    // [M, M + 0.7] with M = max(lm, z) (its log1p term is in [0, ln 2]), so
+    //   lo <= loU = min(-lam M, b2) - lam   and   hi >= hiL = max(-lam (M + 0.7), b2) + lam
+    // in floating point (each operation is monotone).  While beta0 and every iterate
+    // stay inside (loU, hiL) the exact bracket cannot change the result, so its two
+    // transcendentals are only paid when a value reaches the conservative edge.
+    const double M = fmax(lm, z);
+    double lo = fmin(-lam * M, b2) - lam;
+    double hi = fmax(-lam * (M + 0.7), b2) + lam;
+    bool exact = false;
+    auto make_exact = [&]() {
+        const double b1 = -lam * logaddexp(lm, z);
+        lo = fmin(b1, b2) - lam;
+        hi = fmax(b1, b2) + lam;
+        exact = true;
+    };
+    if (!((beta0 > lo) && (beta0 < hi))) make_exact();
     double b = fmin(fmax(beta0, lo), hi);  // np.clip
     if (nstat && b != beta0) nstat[0] += 1;
     int nev = 0;
@@ -193,11 +207,13 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
             sig = t;
         }
         const double g = la + b * inv_lam;
+        if (g == 0.0) break;   // step 0: inactive (avoids the division's slow path)
         const double gp = sig * inv_eps + inv_lam;
         const double step = g / gp;
         const bool active = (fabs(g) > tol) || (fabs(step) > 4e-16 * (1.0 + fabs(b)));
         if (!active) break;
         double nb = b - step;
+        if (!exact && !((nb > lo) && (nb < hi))) make_exact();
         if (!((nb > lo) && (nb < hi))) {
             if (g > 0) hi = fmin(hi, b);
             else lo = fmax(lo, b);

@@ -2,7 +2,7 @@ import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np
 from paper_2410_08859_b200 import _lib
-_lib.LIB_PATH = os.path.join(os.getcwd(), "build_dbg", "libdomdec_b200.so")
+_lib.LIB_PATH = os.environ.get("DD_DBG_LIB", os.path.join(os.getcwd(), "build_dbg", "libdomdec_b200.so"))
 _lib.load(_lib.LIB_PATH)
 from paper_2410_08859_b200 import DivergenceSpec, Grid, GridMeasure, TransportProblem
 from paper_2410_08859_b200.problems import config_problem_arrays

@@ -3,13 +3,13 @@ import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np
 from paper_2410_08859_b200 import _lib
-_lib.load(os.path.join(os.getcwd(), "build_dbg", "libdomdec_b200.so"))
+_lib.load(os.environ.get("DD_DBG_LIB", os.path.join(os.getcwd(), "build_dbg", "libdomdec_b200.so")))
 from paper_2410_08859_b200 import DivergenceSpec, Grid, GridMeasure, TransportProblem
 from paper_2410_08859_b200.problems import config_problem_arrays
 import paper_2410_08859_b200.engine as E
 import paper_2410_08859_b200.multiscale as M
 level = int(sys.argv[1])
-mu, nu, dx, org, cfg = config_problem_arrays(2, seed=0)
+mu, nu, dx, org, cfg = config_problem_arrays(int(sys.argv[2]) if len(sys.argv) > 2 else 2, seed=0)
 h2 = dx * dx
 grid = Grid(mu.shape, dx, org)
 prob = TransportProblem(GridMeasure(grid, mu), GridMeasure(grid, nu), DivergenceSpec(cfg["lam"]), 2 * h2)
