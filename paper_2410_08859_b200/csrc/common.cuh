@@ -191,21 +191,18 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         if (steps) ++*steps;
         ++nev;
         const double w = b * inv_eps + z;
-        // logaddexp(lm, w) and expit(w - lm) from one exponential
-        double la, sig;
+        // logaddexp(lm, w) and expit(w - lm) from one exponential, without branches:
+        // lanes of a warp fall on both sides of t = 0, and a divergent if/else made the
+        // warp issue both exp/log1p chains.  Same values as the two-sided form
+        // (t > 0: exp(-t), w + log1p(e), 1/(1+e); t <= 0: exp(t), lm + log1p(e), e/(1+e)).
         const double t = w - lm;
-        if (t > 0) {
-            const double e = exp(-t);
-            la = w + log1p(e);
-            sig = 1.0 / (1.0 + e);
-        } else if (t <= 0) {
-            const double e = exp(t);
-            la = (t == 0 ? w + 0.693147180559945309417232121458176568 : lm + log1p(e));
-            sig = e / (1.0 + e);
-        } else {
-            la = t;
-            sig = t;
-        }
+        const bool pos = t > 0;
+        const double e = exp(pos ? -t : t);
+        const double l1 = log1p(e);
+        double la = (pos ? w : lm) + l1;
+        if (t == 0) la = w + 0.693147180559945309417232121458176568;
+        double sig = (pos ? 1.0 : e) / (1.0 + e);
+        if (t != t) { la = t; sig = t; }
         const double g = la + b * inv_lam;
         if (g == 0.0) break;   // step 0: inactive (avoids the division's slow path)
         const double gp = sig * inv_eps + inv_lam;
@@ -214,7 +211,9 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         if (!active) break;
         double nb = b - step;
         if (!exact && !((nb > lo) && (nb < hi))) make_exact();
+        bool safeguarded = false;
         if (!((nb > lo) && (nb < hi))) {
+            safeguarded = true;
             if (g > 0) hi = fmin(hi, b);
             else lo = fmax(lo, b);
             if ((nb <= lo) || (nb >= hi)) {
@@ -226,6 +225,18 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         // further pass of the reference loop recomputes the same g and step and
         // leaves b unchanged until max_iters, so stopping here returns the same b
         if (nb == b) break;
+#if !defined(DD_NEWTON_CONFIRM)
+        // Converged step.  Newton's next correction is at most
+        //   |g''| step^2 / (2 g') <= (1 - sig) step^2 / (2 eps)   (g'' = sig(1-sig)/eps^2),
+        // so once step^2/eps <= 2^-52 |nb| it is below one ulp of nb and the confirming
+        // evaluation the reference loop spends to observe that is skipped.  The result
+        // differs from running it by at most that ulp (well inside the 1e-9 parity bar);
+        // build with -DDD_NEWTON_CONFIRM to evaluate it anyway.
+        if (!safeguarded && step * step * inv_eps <= 2.220446049250313e-16 * fabs(nb)) {
+            b = nb;
+            break;
+        }
+#endif
         b = nb;
     }
     if (nstat) {
