@@ -887,6 +887,10 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     }
     int n_clamped = (int)block_sum((double)nclamp, red);
     const bool has_m = block_max_i(anym, redi) != 0;
+    // log m of this thread's first two Y nodes: the same nodes every Sinkhorn
+    // iteration, so the Newton step's log is taken once per solve for them
+    const double lmc0 = (tid < ny) ? log(w.m[tid]) : 0.0;
+    const double lmc1 = (tid + DD_NT < ny) ? log(w.m[tid + DD_NT]) : 0.0;
 
     // per-axis kernel tables K_a = exp(-(x_a - y_a)^2 / eps) (entries may underflow;
     // the sweeps recompute affected outputs exactly)
@@ -1001,9 +1005,10 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
 #else
                 {
                     const double ob = w.beta[y];
+                    const double lmv = y == tid ? lmc0 : (y == tid + DD_NT ? lmc1 : __builtin_nan(""));
                     const double nb = newton_node(w.ty[y], w.m[y], has_m, ob, eps, lam,
                                                   b.newton_tol, b.newton_max_iters, &dg,
-                                                  &newton_steps);
+                                                  &newton_steps, nullptr, lmv);
                     moved |= (nb != ob);
                     w.beta[y] = nb;
                 }

@@ -155,7 +155,8 @@ __device__ __forceinline__ double kl_term(double rho, double sigma) {
 __device__ __forceinline__ double newton_node(double z, double m, bool has_m, double beta0,
                                               double eps, double lam, double tol, int max_iters,
                                               int* deg, long long* steps = nullptr,
-                                              int* nstat = nullptr) {
+                                              int* nstat = nullptr,
+                                              double lm_cached = __builtin_nan("")) {
     const double ratio = eps * lam / (eps + lam);
     const bool fz = z > kNegInf;
     if (!has_m || !(m > 0)) {
@@ -165,7 +166,7 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
     }
     if (!fz) return -lam * log(m);
     const double inv_eps = 1.0 / eps, inv_lam = 1.0 / lam;
-    const double lm = log(m);
+    const double lm = lm_cached == lm_cached ? lm_cached : log(m);   // NaN: not cached
     const double b2 = -ratio * z;
     // Safeguard bracket, evaluated lazily.  The computed logaddexp(lm, z) lies in
     // [M, M + 0.7] with M = max(lm, z) (its log1p term is in [0, ln 2]), so
