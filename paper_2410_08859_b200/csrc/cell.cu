@@ -274,7 +274,21 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
                            double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
     double lmax = kNegInf;
-    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+    int y = threadIdx.x;
+    // four nodes per pass: all loads issue before the first store (the arrays are
+    // distinct, which the compiler cannot prove through the workspace pointers)
+    for (; y + 3 * DD_NT < ny; y += 4 * DD_NT) {
+        double bt[4], ln[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { bt[j] = w.beta[y + j * DD_NT]; ln[j] = w.lnu[y + j * DD_NT]; }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double bv = bt[j] / eps + ln[j];
+            w.ty[y + j * DD_NT] = bv;
+            lmax = fmax(lmax, bv);
+        }
+    }
+    for (; y < ny; y += DD_NT) {
         const double bv = w.beta[y] / eps + w.lnu[y];
         w.ty[y] = bv;
         lmax = fmax(lmax, bv);
@@ -282,7 +296,15 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     if (threadIdx.x == 0) *sc.flag = 0;
     double B = block_max1(lmax, sc.redm, *sc.par);
     if (!isfinite(B)) B = 0.0;
-    for (int y = threadIdx.x; y < ny; y += DD_NT) w.wy[y] = exp(w.ty[y] - B);
+    y = threadIdx.x;
+    for (; y + 3 * DD_NT < ny; y += 4 * DD_NT) {
+        double tv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tv[j] = w.ty[y + j * DD_NT];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w.wy[y + j * DD_NT] = exp(tv[j] - B);
+    }
+    for (; y < ny; y += DD_NT) w.wy[y] = exp(w.ty[y] - B);
     __syncthreads();
     *sc.par ^= 1;
     double* T = w.mid;   // [ny0][nw1]
