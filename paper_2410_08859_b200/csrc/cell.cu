@@ -268,11 +268,32 @@ struct SweepScratch {
     long long* fb_cycles;   // [2] cycles spent in the staged fallback (X, Y)
     int* fb_count;          // [2] number of fallback sweeps (X, Y)
 #endif
+#ifdef DD_SWEEP_TIMING
+    long long* sub;         // [4] X-sweep sub-phases: prologue+max, exp, stage 1, stage 2
+#endif
 };
+#ifdef DD_SWEEP_TIMING
+#define DD_SUB_(i) do { __syncthreads(); const long long tn_ = clock64(); sc.sub[i] += tn_ - ts_; ts_ = tn_; } while (0)
+#else
+#define DD_SUB_(i) do {} while (0)
+#endif
+#if defined(DD_SWEEP_TIMING) && DD_SWEEP_TIMING == 1
+#define DD_SUBX(i) DD_SUB_(i)
+#else
+#define DD_SUBX(i) do {} while (0)
+#endif
+#if defined(DD_SWEEP_TIMING) && DD_SWEEP_TIMING == 2
+#define DD_SUBY(i) DD_SUB_(i)
+#else
+#define DD_SUBY(i) do {} while (0)
+#endif
 
 __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+#ifdef DD_SWEEP_TIMING
+    long long ts_ = clock64();
+#endif
     double lmax = kNegInf;
     int y = threadIdx.x;
     // four nodes per pass: all loads issue before the first store (the arrays are
@@ -304,8 +325,10 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
 #pragma unroll
         for (int j = 0; j < 4; ++j) w.wy[y + j * DD_NT] = exp(tv[j] - B);
     }
+    DD_SUBX(0);
     for (; y < ny; y += DD_NT) w.wy[y] = exp(w.ty[y] - B);
     __syncthreads();
+    DD_SUBX(1);
     *sc.par ^= 1;
     double* T = w.mid;   // [ny0][nw1]
     for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
@@ -313,15 +336,30 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         const double* tr = w.wy + (int64_t)y0 * ny1;
         const double* kr = w.K1 + (int64_t)x1 * ny1;
         double s0 = 0.0, s1 = 0.0;
-        int k = 0;
-        for (; k + 1 < ny1; k += 2) {
-            s0 = fma(tr[k], kr[k], s0);
-            s1 = fma(tr[k + 1], kr[k + 1], s1);
+        if (ny1 & 1) {
+            // K1 rows are an odd number of doubles apart: the lanes' rows hit distinct banks
+            int k = 0;
+            for (; k + 1 < ny1; k += 2) {
+                s0 = fma(tr[k], kr[k], s0);
+                s1 = fma(tr[k + 1], kr[k + 1], s1);
+            }
+            if (k < ny1) s0 = fma(tr[k], kr[k], s0);
+        } else {
+            // even row stride: lanes reading the same k of different K1 rows would share
+            // banks (up to 16-way).  Each row starts at k = x1 instead, which makes the
+            // effective stride ny1 + 1 (odd).  Only the summation order changes.
+            int k = ny1 > 0 ? x1 % ny1 : 0;
+            for (int j = 0; j < ny1; j += 2) {
+                const int k1 = k + 1 == ny1 ? 0 : k + 1;
+                s0 = fma(tr[k], kr[k], s0);
+                s1 = fma(tr[k1], kr[k1], s1);
+                k = k1 + 1 == ny1 ? 0 : k1 + 1;
+            }
         }
-        if (k < ny1) s0 = fma(tr[k], kr[k], s0);
         T[o] = s0 + s1;
     }
     __syncthreads();
+    DD_SUBX(2);
     int bad = 0;
     for (int o = threadIdx.x; o < nx; o += DD_NT) {
         const int x0 = o / nw1, x1 = o - x0 * nw1;
@@ -339,6 +377,7 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     }
     if (bad) *sc.flag = 1;
     __syncthreads();
+    DD_SUBX(3);
     if (*sc.flag) {
 #ifdef DD_PHASE_TIMING
         const long long t0 = clock64();
@@ -354,6 +393,9 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double ratio, double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+#ifdef DD_SWEEP_TIMING
+    long long ts_ = clock64();
+#endif
     double lmax = kNegInf;
     for (int x = threadIdx.x; x < nx; x += DD_NT) {
         if (ratio != 0.0) w.alpha[x] = -ratio * w.L[x];
@@ -364,8 +406,10 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     if (threadIdx.x == 0) *sc.flag = 0;
     double A = block_max1(lmax, sc.redm, *sc.par);
     if (!isfinite(A)) A = 0.0;
+    DD_SUBY(0);
     for (int x = threadIdx.x; x < nx; x += DD_NT) w.wx[x] = exp(w.tx[x] - A);
     __syncthreads();
+    DD_SUBY(1);
     *sc.par ^= 1;
     double* T = w.mid;   // [nw0][ny1]
     for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
@@ -381,6 +425,7 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         T[o] = s0 + s1;
     }
     __syncthreads();
+    DD_SUBY(2);
     int bad = 0;
     for (int o = threadIdx.x; o < ny; o += DD_NT) {
         const int y0 = o / ny1, y1 = o - y0 * ny1;
@@ -397,6 +442,7 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     }
     if (bad) *sc.flag = 1;
     __syncthreads();
+    DD_SUBY(3);
     // alpha is already updated; the staged redo must not apply the update twice
     if (*sc.flag) {
 #ifdef DD_PHASE_TIMING
@@ -952,7 +998,12 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         __shared__ double redm[2 * DD_NW];
         __shared__ int sweep_flag;
         int mpar = 0;
-#ifdef DD_PHASE_TIMING
+#if defined(DD_SWEEP_TIMING)
+        long long fbc[2] = {0, 0};
+        int fbn[2] = {0, 0};
+        long long subc[4] = {0, 0, 0, 0};
+        const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn, subc};
+#elif defined(DD_PHASE_TIMING)
         long long fbc[2] = {0, 0};
         int fbn[2] = {0, 0};
         const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn};
@@ -1073,10 +1124,15 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         if (tid == 0) {
             b.cstat2[(int64_t)c * 4 + 0] = (double)fbc[0] + (double)fbc[1];
             b.cstat2[(int64_t)c * 4 + 1] = (double)fbn[0] * 1e6 + (double)fbn[1];
+#ifdef DD_SWEEP_TIMING
+            // X-sweep sub-phases in place of the loop phases
+            for (int q = 0; q < 4; ++q) b.cstat[(int64_t)c * 8 + 4 + q] = (double)subc[q];
+#else
             b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
             b.cstat[(int64_t)c * 8 + 5] = (double)ph[1];
             b.cstat[(int64_t)c * 8 + 6] = (double)ph[2];
             b.cstat[(int64_t)c * 8 + 7] = (double)ph[3];
+#endif
         }
     #endif
         __syncthreads();

@@ -29,7 +29,7 @@ def solve(self):
             ph = c1[sel, 4:8] / it[sel, None]
             fbx = np.floor(c2[sel, 1] / 1e6) / it[sel]
             fby = (c2[sel, 1] % 1e6) / it[sel]
-            print(f"{name}: n={sel.sum()} ny med={np.median(ny[sel]):.0f} cycles/iter med: lse_x={np.median(ph[:,0]):.0f} gap={np.median(ph[:,1]):.0f} lse_y={np.median(ph[:,2]):.0f} newton={np.median(ph[:,3]):.0f} "
+            print(f"{name}: n={sel.sum()} ny med={np.median(ny[sel]):.0f} ny0 med={np.median(self.ybox[sel,1]):.0f} ny1 med={np.median(self.ybox[sel,3]):.0f} cycles/iter med: lse_x={np.median(ph[:,0]):.0f} gap={np.median(ph[:,1]):.0f} lse_y={np.median(ph[:,2]):.0f} newton={np.median(ph[:,3]):.0f} "
                   f"fallback frac x={np.median(fbx):.2f} y={np.median(fby):.2f} fallback cyc/iter={np.median(c2[sel,0]/it[sel]):.0f}", flush=True)
         raise SystemExit(0)
 E._Batch.solve = solve
