@@ -284,6 +284,8 @@ struct SweepScratch {
 #endif
 #if defined(DD_SWEEP_TIMING) && DD_SWEEP_TIMING == 2
 #define DD_SUBY(i) DD_SUB_(i)
+#elif defined(DD_SWEEP_BARRIERS)
+#define DD_SUBY(i) __syncthreads()
 #else
 #define DD_SUBY(i) do {} while (0)
 #endif
@@ -331,13 +333,18 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     DD_SUBX(1);
     *sc.par ^= 1;
     double* T = w.mid;   // [ny0][nw1]
+    // A warp reads the same k of up to min(nw1, 16) K1 rows, ny1 doubles apart.  They
+    // share banks when gcd(ny1, 16) * min(nw1, 16) > 16; then every row starts at its
+    // own offset instead (below).
+    const int low = ny1 & -ny1;
+    const bool rotate = ny1 > 0 && (low < 16 ? low : 16) * (nw1 < 16 ? nw1 : 16) > 16;
     for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
         const int y0 = o / nw1, x1 = o - y0 * nw1;
         const double* tr = w.wy + (int64_t)y0 * ny1;
         const double* kr = w.K1 + (int64_t)x1 * ny1;
         double s0 = 0.0, s1 = 0.0;
-        if (ny1 & 1) {
-            // K1 rows are an odd number of doubles apart: the lanes' rows hit distinct banks
+        if (!rotate) {
+            // conflict-free row stride (e.g. ny1 odd)
             int k = 0;
             for (; k + 1 < ny1; k += 2) {
                 s0 = fma(tr[k], kr[k], s0);
@@ -345,10 +352,9 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
             }
             if (k < ny1) s0 = fma(tr[k], kr[k], s0);
         } else {
-            // even row stride: lanes reading the same k of different K1 rows would share
-            // banks (up to 16-way).  Each row starts at k = x1 instead, which makes the
-            // effective stride ny1 + 1 (odd).  Only the summation order changes.
-            int k = ny1 > 0 ? x1 % ny1 : 0;
+            // Each row starts at k = x1, which makes the effective stride ny1 + 1 (odd:
+            // rotate implies ny1 even).  Only the summation order changes.
+            int k = x1 % ny1;
             for (int j = 0; j < ny1; j += 2) {
                 const int k1 = k + 1 == ny1 ? 0 : k + 1;
                 s0 = fma(tr[k], kr[k], s0);
@@ -1125,7 +1131,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
             b.cstat2[(int64_t)c * 4 + 0] = (double)fbc[0] + (double)fbc[1];
             b.cstat2[(int64_t)c * 4 + 1] = (double)fbn[0] * 1e6 + (double)fbn[1];
 #ifdef DD_SWEEP_TIMING
-            // X-sweep sub-phases in place of the loop phases
+            // sweep sub-phases in place of the loop phases
             for (int q = 0; q < 4; ++q) b.cstat[(int64_t)c * 8 + 4 + q] = (double)subc[q];
 #else
             b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
