@@ -1596,8 +1596,10 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         cs[7] = target_miss;
 #endif
         double* c2 = b.cstat2 + (int64_t)c * 4;
-        c2[0] = (double)drift;
+#if !defined(DD_PHASE_TIMING)
+        c2[0] = (double)drift;    // (phase-timing builds keep the sweep-fallback stats here)
         c2[1] = trunc_total;
+#endif
         c2[2] = t_loop_d;         // SM cycles spent in the Sinkhorn loop
         c2[3] = nsteps;           // Newton evaluations over all nodes and iterations
     }
