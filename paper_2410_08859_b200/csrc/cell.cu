@@ -266,7 +266,7 @@ struct SweepScratch {
     int* par;       // block-max buffer parity
 #ifdef DD_PHASE_TIMING
     long long* fb_cycles;   // [2] cycles spent in the staged fallback (X, Y)
-    int* fb_count;          // [2] number of fallback sweeps (X, Y)
+    int* fb_count;          // [4] shared: fallback sweeps (X, Y), underflowed outputs (X, Y)
 #endif
 #ifdef DD_SWEEP_TIMING
     long long* sub;         // [4] X-sweep sub-phases: prologue+max, exp, stage 1, stage 2
@@ -379,9 +379,12 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         if (k < ny0) s0 = fma(kr[k], T[(int64_t)k * nw1 + x1], s0);
         const double sm = s0 + s1;
         if (sm >= kTiny) out[o] = log(sm) + B;
-        else bad = 1;
+        else ++bad;
     }
     if (bad) *sc.flag = 1;
+#ifdef DD_PHASE_TIMING
+    if (bad) atomicAdd(&sc.fb_count[2 + 0], bad);   // outputs that underflowed
+#endif
     __syncthreads();
     DD_SUBX(3);
     if (*sc.flag) {
@@ -391,7 +394,7 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         cell_lse_x_staged(w, c, nw0, nw1, eps, out);
 #ifdef DD_PHASE_TIMING
         sc.fb_cycles[0] += clock64() - t0;
-        sc.fb_count[0] += 1;
+        if (threadIdx.x == 0) sc.fb_count[0] += 1;
 #endif
     }
 }
@@ -444,9 +447,12 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         if (k < nw0) s0 = fma(w.K0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
         const double sm = s0 + s1;
         if (sm >= kTiny) out[o] = log(sm) + A;
-        else bad = 1;
+        else ++bad;
     }
     if (bad) *sc.flag = 1;
+#ifdef DD_PHASE_TIMING
+    if (bad) atomicAdd(&sc.fb_count[2 + 1], bad);   // outputs that underflowed
+#endif
     __syncthreads();
     DD_SUBY(3);
     // alpha is already updated; the staged redo must not apply the update twice
@@ -457,7 +463,7 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
 #ifdef DD_PHASE_TIMING
         sc.fb_cycles[1] += clock64() - t0;
-        sc.fb_count[1] += 1;
+        if (threadIdx.x == 0) sc.fb_count[1] += 1;
 #endif
     }
 }
@@ -1006,12 +1012,14 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         int mpar = 0;
 #if defined(DD_SWEEP_TIMING)
         long long fbc[2] = {0, 0};
-        int fbn[2] = {0, 0};
+        __shared__ int fbn[4];
+        if (tid < 4) fbn[tid] = 0;
         long long subc[4] = {0, 0, 0, 0};
         const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn, subc};
 #elif defined(DD_PHASE_TIMING)
         long long fbc[2] = {0, 0};
-        int fbn[2] = {0, 0};
+        __shared__ int fbn[4];
+        if (tid < 4) fbn[tid] = 0;
         const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn};
 #else
         const SweepScratch sc{redm, &sweep_flag, &mpar};
@@ -1128,7 +1136,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     #endif
     #ifdef DD_PHASE_TIMING
         if (tid == 0) {
-            b.cstat2[(int64_t)c * 4 + 0] = (double)fbc[0] + (double)fbc[1];
+            b.cstat2[(int64_t)c * 4 + 0] = (double)fbn[3];   // underflowed Y-sweep outputs
             b.cstat2[(int64_t)c * 4 + 1] = (double)fbn[0] * 1e6 + (double)fbn[1];
 #ifdef DD_SWEEP_TIMING
             // sweep sub-phases in place of the loop phases
