@@ -35,6 +35,7 @@ struct WsLayout {
     int64_t alpha, u, L, mu, tx, lmu, wx;
     int64_t beta, ty, wy;
     int64_t K0, K1, mid, rmax;
+    int64_t K0y, K1y, c0, c1;
     int64_t midstride;
     int64_t total;
 };
@@ -71,6 +72,12 @@ __host__ __device__ inline WsLayout ws_layout(int nw0, int nw1, int ny0, int ny1
     if (nw0 > rm) rm = nw0;
     if (nw1 > rm) rm = nw1;
     w.rmax = o; o += rm;
+    // Y-sweep tables normalised per Y coordinate (column max 1) and the removed
+    // log factors c_a[y_a] = max_x -(x_a - y_a)^2 / eps
+    w.K0y = o; o += (int64_t)nw0 * ny0;
+    w.K1y = o; o += (int64_t)nw1 * ny1;
+    w.c0 = o; o += ny0;
+    w.c1 = o; o += ny1;
     w.total = o;
     return w;
 }
@@ -80,6 +87,7 @@ struct Ws {
     double *alpha, *u, *L, *mu, *tx, *lmu, *wx;
     double *beta, *ty, *wy;
     double *K0, *K1, *mid, *rmax;
+    double *K0y, *K1y, *c0, *c1;
     const double* lnu;   // global: log nu on the window (contiguous copy)
     double* m;           // global: background density on the window
     int64_t ms;
@@ -93,6 +101,7 @@ __device__ inline Ws ws_bind(double* base, const WsLayout& l) {
     w.beta = base + l.beta; w.ty = base + l.ty; w.wy = base + l.wy;
     w.K0 = base + l.K0; w.K1 = base + l.K1;
     w.mid = base + l.mid; w.rmax = base + l.rmax;
+    w.K0y = base + l.K0y; w.K1y = base + l.K1y; w.c0 = base + l.c0; w.c1 = base + l.c1;
     w.lnu = nullptr;
     w.m = nullptr;
     w.ms = l.midstride;
@@ -427,10 +436,10 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         double s0 = 0.0, s1 = 0.0;
         int k = 0;
         for (; k + 1 < nw1; k += 2) {
-            s0 = fma(tr[k], w.K1[(int64_t)k * ny1 + y1], s0);
-            s1 = fma(tr[k + 1], w.K1[(int64_t)(k + 1) * ny1 + y1], s1);
+            s0 = fma(tr[k], w.K1y[(int64_t)k * ny1 + y1], s0);
+            s1 = fma(tr[k + 1], w.K1y[(int64_t)(k + 1) * ny1 + y1], s1);
         }
-        if (k < nw1) s0 = fma(tr[k], w.K1[(int64_t)k * ny1 + y1], s0);
+        if (k < nw1) s0 = fma(tr[k], w.K1y[(int64_t)k * ny1 + y1], s0);
         T[o] = s0 + s1;
     }
     __syncthreads();
@@ -441,12 +450,12 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         double s0 = 0.0, s1 = 0.0;
         int k = 0;
         for (; k + 1 < nw0; k += 2) {
-            s0 = fma(w.K0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
-            s1 = fma(w.K0[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
+            s0 = fma(w.K0y[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+            s1 = fma(w.K0y[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
         }
-        if (k < nw0) s0 = fma(w.K0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+        if (k < nw0) s0 = fma(w.K0y[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
         const double sm = s0 + s1;
-        if (sm >= kTiny) out[o] = log(sm) + A;
+        if (sm >= kTiny) out[o] = log(sm) + A + (w.c0[y0] + w.c1[y1]);
         else ++bad;
     }
     if (bad) *sc.flag = 1;
@@ -981,6 +990,28 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     for (int o = tid; o < nw1 * ny1; o += DD_NT) {
         const int x1 = o / ny1, y1 = o - x1 * ny1;
         w.K1[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps));
+    }
+    // Y-sweep tables: each Y coordinate's column divided by its largest entry, so
+    // far Y nodes do not underflow to zero geometrically (the factor returns in the
+    // log domain: out = log(sum) + A + c0[y0] + c1[y1])
+    for (int y0 = tid; y0 < ny0; y0 += DD_NT) {
+        double cm = kNegInf;
+        for (int x0 = 0; x0 < nw0; ++x0) cm = fmax(cm, negsq(w.xc0[x0], w.yc0[y0], eps));
+        w.c0[y0] = cm;
+    }
+    for (int y1 = tid; y1 < ny1; y1 += DD_NT) {
+        double cm = kNegInf;
+        for (int x1 = 0; x1 < nw1; ++x1) cm = fmax(cm, negsq(w.xc1[x1], w.yc1[y1], eps));
+        w.c1[y1] = cm;
+    }
+    __syncthreads();
+    for (int o = tid; o < nw0 * ny0; o += DD_NT) {
+        const int x0 = o / ny0, y0 = o - x0 * ny0;
+        w.K0y[o] = exp(negsq(w.xc0[x0], w.yc0[y0], eps) - w.c0[y0]);
+    }
+    for (int o = tid; o < nw1 * ny1; o += DD_NT) {
+        const int x1 = o / ny1, y1 = o - x1 * ny1;
+        w.K1y[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps) - w.c1[y1]);
     }
     __syncthreads();
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----

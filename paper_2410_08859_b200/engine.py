@@ -599,7 +599,8 @@ def _ws_total(nw0: int, nw1: int, ny0: np.ndarray, ny1: np.ndarray) -> np.ndarra
     ny = ny0 * ny1
     ms = np.maximum(ny0 * nw1, nw0 * ny1)
     rm = np.maximum(np.maximum(ny0, ny1), max(nw0, nw1))
-    return nw0 + nw1 + ny0 + ny1 + 7 * nx + 3 * ny + nw0 * ny0 + nw1 * ny1 + 5 * ms + rm
+    return (nw0 + nw1 + ny0 + ny1 + 7 * nx + 3 * ny + nw0 * ny0 + nw1 * ny1 + 5 * ms + rm
+            + nw0 * ny0 + nw1 * ny1 + ny0 + ny1)   # Y-sweep normalised tables, c0, c1
 
 
 class _Batch:
