@@ -264,7 +264,9 @@ __device__ void cell_lse_y_staged(const Ws& w, const CellWin& c, int nw0, int nw
 }
 
 // Fast path of both sweeps: one global max shift of the input vector and two
-// FMA contractions through the factorised kernel (the reference DenseKernel's
+// FMA contractions through the factorised kernel, using the Y-normalised tables
+// K_a^y = K_a exp(-c_a(y_a)) (the X sweep adds c0 + c1 to its Y input, the Y sweep
+// adds them to its outputs) (the reference DenseKernel's
 // "matrix" evaluation, sinkhorn.py:91-130, done axis by axis).  If any output's
 // shifted sum is below kTiny it may have lost terms to underflow, and the
 // whole sweep is redone by the stage-wise stabilised path above, so every
@@ -315,13 +317,15 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         for (int j = 0; j < 4; ++j) { bt[j] = w.beta[y + j * DD_NT]; ln[j] = w.lnu[y + j * DD_NT]; }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const double bv = bt[j] / eps + ln[j];
-            w.ty[y + j * DD_NT] = bv;
+            const int yy = y + j * DD_NT, y0 = yy / ny1;
+            const double bv = bt[j] / eps + ln[j] + (w.c0[y0] + w.c1[yy - y0 * ny1]);
+            w.ty[yy] = bv;
             lmax = fmax(lmax, bv);
         }
     }
     for (; y < ny; y += DD_NT) {
-        const double bv = w.beta[y] / eps + w.lnu[y];
+        const int y0 = y / ny1;
+        const double bv = w.beta[y] / eps + w.lnu[y] + (w.c0[y0] + w.c1[y - y0 * ny1]);
         w.ty[y] = bv;
         lmax = fmax(lmax, bv);
     }
@@ -350,7 +354,7 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
         const int y0 = o / nw1, x1 = o - y0 * nw1;
         const double* tr = w.wy + (int64_t)y0 * ny1;
-        const double* kr = w.K1 + (int64_t)x1 * ny1;
+        const double* kr = w.K1y + (int64_t)x1 * ny1;
         double s0 = 0.0, s1 = 0.0;
         if (!rotate) {
             // conflict-free row stride (e.g. ny1 odd)
@@ -378,7 +382,7 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     int bad = 0;
     for (int o = threadIdx.x; o < nx; o += DD_NT) {
         const int x0 = o / nw1, x1 = o - x0 * nw1;
-        const double* kr = w.K0 + (int64_t)x0 * ny0;
+        const double* kr = w.K0y + (int64_t)x0 * ny0;
         double s0 = 0.0, s1 = 0.0;
         int k = 0;
         for (; k + 1 < ny0; k += 2) {

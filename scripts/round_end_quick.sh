@@ -6,4 +6,4 @@ DD_FORCE_GLOBAL_WS=1 timeout 200 python -m pytest tests/test_gpu_parity.py -q 2>
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
 timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/f3_bench.log 2>&1; tail -1 gpurun_out/f3_bench.log | cut -c1-160
 DD_DBG_LIB=$PWD/build_dbg/libdomdec_b200.so timeout 400 python scripts/probe_phase_level.py 256 1 2>&1 | grep cycles
-DD_DBG_LIB=$PWD/build_dbg/libdomdec_b200.so timeout 400 python scripts/probe_phase_level.py 1024 2 2>&1 | grep capped
+DD_DBG_LIB=$PWD/build_dbg/libdomdec_b200.so timeout 400 python scripts/probe_phase_level.py 1024 2 2>&1 | grep cycles
