@@ -2,30 +2,37 @@
 """Benchmark: converged multiscale unbalanced domdec solve on B200.
 
 One "step" is one full converged solve of a BASELINE.json configuration.
-Default ``ms_256`` = configs[1] (256^2, 5-Gaussian mixtures, lambda = 0.5, eps
-annealed 64h^2 -> 2h^2 over the 32^2 -> 256^2 pyramid, 4x4 basic cells, fp64,
-staggered strategy, delta = 2e-5), which finishes in seconds; ``--config
-ms_1024`` runs configs[2] (the 1024^2 headline, several minutes per solve in
-this round).  The metric is the solve time in seconds (lower is better).
+Default ``ms_1024`` = configs[2], the metric's own config (1024^2, 8-Gaussian
+mixtures + 1e-5 floor, masses 1.0 / 1.5, lambda = 1, eps annealed 256h^2 ->
+2h^2 over the 64^2 -> 1024^2 pyramid, 8x8 basic cells with 2x2 composites,
+fp64, staggered strategy, delta = 2e-5), solved with the SPEC / paper §4.3.1
+multiscale protocol (global Sinkhorn at delta/4 below layer 8, domdec from
+512^2).  ``--config ms_256`` runs configs[1].  The metric is the solve time in
+seconds (lower is better).
 
 * ``value``  — device-timed solve (CUDA events on the launching stream) with the
   pyramid already resident in HBM; L2 is flushed (256 MiB write) before each step.
-* ``e2e``    — the same solve through the public API from pinned host arrays:
-  host->device copy of every pyramid level and device->host read of the result
-  (basic-cell marginals, duals, objective) inside the timed region.
+* ``e2e``    — the same solve through the public API from host arrays: the
+  host->device copy of every pyramid level and the device->host read of the
+  result (basic-cell marginals, duals) inside the timed region.
 * ``roofline`` — the dominant kernel (``dd_cell_solve``): algorithmic FP64
   FLOPs of its separable contractions per launch / mean launch time (CUDA
-  events), against the nominal FP64 peak (no FP64 entry in MEASURED_PEAKS.json);
-  its HBM traffic is reported next to it.
-* ``cpu_baseline`` — the CPU oracle (a restatement of the reference algorithm)
-  timed on the coarsest stage of the same workload and extrapolated to the
-  whole solve by the ratio of algorithmic cell-sweep FLOPs (both arms run the
-  same iteration sequence).
+  events), against the FP64 DFMA peak measured on B200
+  (``profiles/fp64_peak.json``, scripts/micro/fp64_peak.cu); DRAM traffic per
+  launch and FP64-pipe utilisation from the committed ncu capture.
+* ``cpu_baseline`` — the reference algorithm (the CPU oracle restatement) on a
+  bounded sample of the same workload: complete composite-cell subproblems
+  recorded from the 1024^2 stage (``tests/golden/ms1024_cells.npz``), solved
+  process-parallel over all host cores with a bounded cell iteration cap; the
+  measured time is reported together with its scaling to the whole solve by
+  algorithmic cell-sweep work (labelled as a scaled estimate).
+* ``--impl reference`` — that same CPU sample, timed per step on the host
+  cores; ``value`` is the measured seconds of one sample (what ran), the scaled
+  whole-solve estimate is a separate labelled field.
 
 Multi-GPU (``--gpus N`` under torchrun): every batch's cell solves are
 partitioned across the ranks (cost-balanced) and the solve outputs summed
-with NCCL, so all ranks solve the same problem together (strong scaling);
-value is the max over ranks.
+with NCCL (strong scaling); value is the max over ranks.
 """
 
 from __future__ import annotations
@@ -44,16 +51,17 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 CONFIGS = {"pr1_64": 0, "ms_256": 1, "ms_1024": 2, "ms_2048": 3}
-FP64_PEAK_TFLOPS = 40.0   # B200 nominal FP64 (vector); not measured on this pool
+FP64_NOMINAL_TFLOPS = 40.0   # B200 datasheet FP64 (fallback when no measurement is committed)
+SAMPLE_CAP = 100             # cell iteration cap of the CPU sample
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=os.environ.get("DD_BENCH_CONFIG", "ms_256"),
+    ap.add_argument("--config", default=os.environ.get("DD_BENCH_CONFIG", "ms_1024"),
                     choices=sorted(CONFIGS))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=1, help="run the CPU baseline sample")
@@ -154,23 +162,33 @@ def fetch_result(st):
     return d2h
 
 
-def cpu_sample(prob, cfg, eps_start):
-    """Oracle (reference algorithm restated in numpy) on the coarsest stage."""
-    from oracle.ref_problem import make_ctx
-    from oracle.ref_sweep import EngCfg, StratCfg, solve, warm_state
-    from paper_2410_08859_b200.multiscale import build_pyramid, eps_schedule
+def cpu_sample(workers=None):
+    """Oracle solves of the recorded 1024^2 cell sample (bounded cap), all host cores."""
+    from oracle.cell_sample import run_sample, sample_flops
 
-    levels = build_pyramid(prob.mu, prob.nu, cfg["coarsest"])
-    sched = eps_schedule(levels, eps_start, prob.eps)
-    lv = levels[0]
-    eps = sched[0][0]
-    t0 = time.perf_counter()
-    ctx = make_ctx(lv.mu, lv.nu, lv.grid.dx, lv.grid.origin, prob.div.lam, eps, cfg["cell"])
-    st = warm_state(ctx, delta=1e-3)
-    _, rep, _ = solve(ctx, st, StratCfg("staggered"), EngCfg())
-    t = time.perf_counter() - t0
-    return t, rep, f"coarsest stage {lv.grid.dims[0]}^2 at eps={eps / (prob.mu.grid.dx ** 2):g}h^2 " \
-                   f"(warm start + staggered domdec to delta=2e-5)"
+    wall, iters, cores, d, probs = run_sample(SAMPLE_CAP, workers)
+    fl = sample_flops(probs, iters, int(d["nw0"]), int(d["nw1"]))
+    desc = (f"{len(probs)} complete composite-cell subproblems of the first staggered batch of "
+            f"the 1024^2 stage (tests/golden/ms1024_cells.npz), oracle cell solver (reference "
+            f"cells.py restated), cell cap {SAMPLE_CAP}: {int(iters.sum())} cell iterations, "
+            f"{fl:.3e} algorithmic FLOPs, {wall:.2f} s on {cores} processes")
+    return wall, fl, cores, desc, d
+
+
+def _peak():
+    """Measured FP64 DFMA peak (profiles/fp64_peak.json) or the datasheet fallback."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return float(d["tflops"]), f"measured FP64 DFMA peak on B200 ({d.get('how', '')})"
+    except Exception:
+        return FP64_NOMINAL_TFLOPS, "B200 datasheet FP64 (no measured FP64 peak committed)"
+
+
+def _ncu_profile():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_cell_solve.json")))
+    except Exception:
+        return None
 
 
 def main():
@@ -191,7 +209,8 @@ def main():
                                f"{cfg['coarsest']}^2->{prob.mu.grid.dims[0]}^2, "
                                f"eps {eps_start / prob.mu.grid.dx ** 2:g}h^2->{prob.eps / prob.mu.grid.dx ** 2:g}h^2, "
                                f"lambda={cfg['lam']}, cells {cfg['cell']}x{cfg['cell']} (2x2 composites), "
-                               "staggered, delta=2e-5",
+                               "staggered, delta=2e-5, SPEC multiscale (global Sinkhorn at delta/4 below "
+                               "layer 8 / the finest layer, domdec above)",
                    "grid": list(prob.mu.grid.dims), "cell": cfg["cell"], "lambda": cfg["lam"],
                    "strategy": "staggered", "l2": "flushed (256 MiB write) before every step",
                    "parallelism": (f"cell-sharded x{world} (batch cell solves partitioned, "
@@ -201,26 +220,28 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        # CPU reference arm: the oracle port, bounded sample, extrapolated by FLOP ratio
+        # CPU reference arm: the oracle (reference algorithm restated) on the
+        # recorded cell sample, process-parallel over the host cores
+        from oracle.cell_sample import run_sample
+        run_sample(2, None)          # warm-up: process pool and numpy paths
         ts = []
-        rep = None
-        for _ in range(max(1, args.warmup // 3)):
-            pass
         for _ in range(args.steps):
-            t, rep, sample = cpu_sample(prob, cfg, eps_start)
+            t, fl, cores, sample, d = cpu_sample()
             ts.append(t)
         t = float(np.median(ts))
-        frac = _sample_fraction(args.config)
-        value = t / frac if frac else None
-        line = {"metric": "converged UOT domdec solve time (s)", "value": value, "unit": "s",
-                "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": value * 1e3 if value else None, "higher_is_better": False,
+        full = float(d["full_solve_cell_flops"])
+        line = {"metric": "converged UOT domdec solve time (s)", "value": t, "unit": "s",
+                "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": 1,
+                "ms_per_step": t * 1e3, "higher_is_better": False,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_desc,
-                "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "port",
-                                 "sample": f"{sample}: {t:.2f}s measured, extrapolated x{1 / frac:.1f} "
-                                           "by the GPU run's cell-sweep FLOP ratio" if frac else sample},
-                "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0,
+                "cpu_baseline": {"value": t, "unit": "s", "cores": cores, "kind": "port",
+                                 "sample": sample},
+                "scaled_full_solve_s": {"value": t * full / fl, "how":
+                                        "measured sample seconds x (algorithmic cell-sweep FLOPs "
+                                        "of one whole converged GPU solve / the sample's); an "
+                                        "estimate, not a measurement"},
+                "e2e": {"value": t, "unit": "s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -291,24 +312,29 @@ def main():
     n_launch = len(solve_ms) // max(1, args.steps)
     mean_ms = float(np.mean(solve_ms)) if solve_ms else float("nan")
     achieved = (flops / max(n_launch, 1)) / (mean_ms * 1e-3) / 1e12 if solve_ms else None
+    peak, peak_src = _peak()
+    prof = _ncu_profile()
+    traffic = None
+    if prof is not None:
+        traffic = {"dram_bytes_per_launch": prof.get("dram_bytes"),
+                   "achieved_gbs": prof.get("dram_gbs"),
+                   "fp64_pipe_pct": prof.get("fp64_pipe_pct"),
+                   "source": prof.get("source")}
     roofline = {"bound": "fp64", "kernel": "dd_cell_solve (cell_solve_kernel + cluster variant)",
-                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                "peak_source": "B200 nominal FP64 (no FP64 entry in MEASURED_PEAKS.json)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if achieved else None, "peak_source": peak_src,
                 "flops_per_launch": flops / max(n_launch, 1), "launches_per_step": n_launch,
                 "mean_launch_ms": mean_ms,
                 "share_of_step": (sum(solve_ms) / 1e3 / args.steps) / t_dev if solve_ms else None,
                 "grid_lse_share_of_step": (sum(lse_ms) / 1e3 / args.steps) / t_dev if lse_ms else None,
-                "traffic": None}
+                "traffic": traffic}
     cpu = None
-    if rank == 0 and args.cpu_sample:
-        t_cpu, crep, sample = cpu_sample(prob, cfg, eps_start)
-        stage0 = rep.stages[0][2].diagnostics.get("cell_flops", 0.0)
-        frac = stage0 / flops if flops else None
-        cpu = {"value": t_cpu / frac if frac else None, "unit": "s", "cores": 1, "kind": "port",
-               "sample": f"{sample}: {t_cpu:.2f}s measured on 1 core, extrapolated x{1 / frac:.1f} "
-                         "by the GPU run's cell-sweep FLOP ratio (same iteration sequence)"}
-        _save_fraction(args.config, frac)
+    if rank == 0 and args.cpu_sample and world == 1 and args.config == "ms_1024":
+        t_cpu, fl_cpu, cores, sample, _ = cpu_sample()
+        cpu = {"value": t_cpu, "unit": "s", "cores": cores, "kind": "port", "sample": sample,
+               "scaled_full_solve_s": t_cpu * flops / fl_cpu,
+               "scaling": "measured sample seconds x (this run's algorithmic cell-sweep FLOPs per "
+                          "solve / the sample's): an estimate of one whole solve on these cores"}
     if rank == 0:
         line = {"metric": "converged UOT domdec solve time (s)", "value": t_dev, "unit": "s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -318,8 +344,11 @@ def main():
                 "max_step_s": t_max_step,
                 "converged": bool(rep.converged), "rel_pd_gap": rep.rel_pd_gap,
                 "final_total": rep.final_score.get("total"),
-                "stages": [[n, e / prob.mu.grid.dx ** 2, r.iterations,
-                            round(r.timings["total"], 3)] for n, e, r in rep.stages],
+                "stages": [[n, e / prob.mu.grid.dx ** 2, r.diagnostics.get("solver", "domdec"),
+                            r.iterations, round(r.timings["total"], 3),
+                            r.diagnostics.get("nonconverged_cells", 0)] for n, e, r in rep.stages],
+                "stage_fields": ["grid n", "eps/h^2", "solver", "iterations", "seconds",
+                                 "capped cell solves"],
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": int(d2h)},
@@ -328,27 +357,6 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-_FRAC_FILE = os.path.join(ROOT, "profiles", "cpu_sample_fraction.json")
-
-
-def _save_fraction(cfg, frac):
-    try:
-        d = json.load(open(_FRAC_FILE)) if os.path.exists(_FRAC_FILE) else {}
-        d[cfg] = frac
-        os.makedirs(os.path.dirname(_FRAC_FILE), exist_ok=True)
-        json.dump(d, open(_FRAC_FILE, "w"), indent=1)
-    except Exception:
-        pass
-
-
-def _sample_fraction(cfg):
-    """FLOP fraction of the coarsest stage in the GPU run (recorded by a GPU bench run)."""
-    try:
-        return json.load(open(_FRAC_FILE)).get(cfg)
-    except Exception:
-        return None
 
 
 if __name__ == "__main__":

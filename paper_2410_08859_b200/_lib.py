@@ -120,8 +120,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
 # kernels each entry point launches (used for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "dd_grid_lse": 2, "dd_axpb": 1, "dd_newton_global": 1, "dd_newton_nodes": 1,
-    "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_solve2": 3, "dd_cell_delta": 1, "dd_blend_energy": 5,
-    "dd_cell_commit": 1, "dd_assemble": 1, "dd_energy_terms": 4, "dd_product_init": 1,
+    "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_solve2": 3, "dd_cell_delta": 1, "dd_blend_energy": 6,
+    "dd_cell_commit": 1, "dd_assemble": 2, "dd_energy_terms": 4, "dd_product_init": 1,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1, "dd_refine_dual": 1,
 }

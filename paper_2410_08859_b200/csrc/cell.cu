@@ -1704,21 +1704,6 @@ __global__ void __launch_bounds__(DD_NT) cell_delta_kernel(dd_geom g, dd_state s
     }
 }
 
-__global__ void __launch_bounds__(DD_NT) blend_scatter_kernel(dd_batch b, const double* dy,
-                                                              const double* theta, double* ywork,
-                                                              int ny1g) {
-    const int c = blockIdx.x;
-    const double th = theta[c];
-    if (th == 0.0) return;
-    const int32_t* d = b.desc + (int64_t)c * 12;
-    const int64_t yoff = b.offs[(int64_t)c * 4];
-    const int ye0 = d[6], ye1 = d[8];
-    for (int y = threadIdx.x; y < ye0 * ye1; y += DD_NT) {
-        const int y0 = y / ye1, y1 = y - y0 * ye1;
-        atomicAdd(ywork + (int64_t)(d[5] + y0) * ny1g + (d[7] + y1), th * dy[yoff + y]);
-    }
-}
-
 // per-cell blend pieces: out[c*4] = theta*t_delta, theta*k_delta, d1_blend - d1_old
 __global__ void __launch_bounds__(DD_NT) blend_cell_kernel(dd_geom g, dd_state s, dd_batch b,
                                                            const double* cd, const double* theta,
@@ -2139,14 +2124,11 @@ extern "C" int dd_blend_energy(const dd_geom* g, const dd_state* s, const dd_bat
                                double* ywork, double* partial, double* out, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = (int64_t)g->ny0 * g->ny1;
-    cudaError_t e = cudaMemcpyAsync(ywork, b->snapshot, n * sizeof(double),
-                                    cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) return dd_set_error(e);
-    if (b->n_cells > 0) {
-        dd::blend_scatter_kernel<<<b->n_cells, DD_NT, 0, st>>>(*b, dy, theta, ywork, g->ny1);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return dd_set_error(e);
-    }
+    cudaError_t e;
+    // ywork = snapshot + sum_c theta_c dy_c over the cells' Y windows, in cell order
+    int rc0 = dd_box_gather(b->n_cells, b->desc + 5, 12, dy, 0, b->offs, 4, theta, g->ny0, g->ny1,
+                            b->snapshot, ywork, st);
+    if (rc0) return rc0;
     int rc = dd_grid_kl(n, ywork, s->nu, 1, partial, out, stream);
     if (rc) return rc;
     if (b->n_cells > 0) {

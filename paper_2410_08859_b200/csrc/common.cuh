@@ -5,6 +5,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <limits.h>
+
 #define DD_NT 512
 #define DD_NW (DD_NT / 32)
 
@@ -315,3 +317,9 @@ __device__ __forceinline__ void newton_step(NewtonState& s, double inv_eps, doub
 }
 
 }  // namespace dd
+
+// Deterministic boxed gather-sum (grid.cu): out = base + sum_i scale_i * v_i over
+// the items' boxes, accumulated in item order; library-internal.
+int dd_box_gather(int n, const int32_t* box, int bstride, const double* vals, int64_t vstride,
+                  const int64_t* voff, int voff_stride, const double* scale, int ny0, int ny1,
+                  const double* base, double* out, cudaStream_t st);

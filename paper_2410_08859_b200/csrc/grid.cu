@@ -167,17 +167,149 @@ __global__ void __launch_bounds__(DD_NT) reduce_rows_kernel(int64_t n_rows, int 
     if (threadIdx.x == 0) out[q] = s;
 }
 
-__global__ void __launch_bounds__(DD_NT) assemble_kernel(dd_geom g, dd_state s, double* out) {
-    const int i = blockIdx.x;
-    const int32_t* bx = s.ybox + (int64_t)i * 4;
-    const int o0 = bx[0], e0 = bx[1], o1 = bx[2], e1 = bx[3];
-    if (e0 <= 0 || e1 <= 0) return;
-    const double* v = s.yval + (int64_t)i * s.cap;
-    for (int t = threadIdx.x; t < e0 * e1; t += DD_NT) {
-        const int a0 = t / e1, a1 = t - a0 * e1;
-        atomicAdd(out + (int64_t)(o0 + a0) * g.ny1 + (o1 + a1), v[t]);
+// ---- deterministic boxed gather-sum ------------------------------------------------
+// out[y] = base[y] (or 0) + sum over items i in index order with y in box_i of
+// scale_i * v_i[y - box_i], each product rounded before its add (no FMA), i.e.
+// exactly the reference's sequential accumulation (measures.py:410-425
+// assemble_y_marginal; engine.py:441-456 BlendScorer.energy_at y[ids] += th*dy).
+// One CTA per Y tile: items are scanned in chunks of DD_NT; a chunk whose
+// bounding box (precomputed) misses the tile is skipped; the hits of a chunk
+// are compacted in index order (warp ballots) and every node of the tile
+// accumulates them in that order.  No atomics: bitwise reproducible.
+struct gather_items {
+    int n;
+    const int32_t* box;      // (o0, e0, o1, e1) at box + i*bstride
+    int bstride;
+    const double* vals;      // values of item i at vals + (voff ? voff[i*voff_stride] : i*vstride)
+    int64_t vstride;
+    const int64_t* voff;
+    int voff_stride;
+    const double* scale;     // nullable: plain sum
+};
+
+__device__ __forceinline__ bool item_live(const gather_items& it, int i, int4& b) {
+    const int32_t* p = it.box + (int64_t)i * it.bstride;
+    b = make_int4(p[0], p[1], p[2], p[3]);
+    if (b.y <= 0 || b.w <= 0) return false;
+    if (it.scale && it.scale[i] == 0.0) return false;
+    return true;
+}
+
+__global__ void __launch_bounds__(DD_NT) chunk_bbox_kernel(gather_items it, int4* cb) {
+    __shared__ int red[4][DD_NW];
+    const int i = blockIdx.x * DD_NT + threadIdx.x;
+    int lo0 = INT_MAX, hi0 = INT_MIN, lo1 = INT_MAX, hi1 = INT_MIN;
+    int4 b;
+    if (i < it.n && item_live(it, i, b)) {
+        lo0 = b.x; hi0 = b.x + b.y; lo1 = b.z; hi1 = b.z + b.w;
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo0 = min(lo0, __shfl_xor_sync(0xffffffffu, lo0, o));
+        hi0 = max(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+        lo1 = min(lo1, __shfl_xor_sync(0xffffffffu, lo1, o));
+        hi1 = max(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { red[0][w] = lo0; red[1][w] = hi0; red[2][w] = lo1; red[3][w] = hi1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < DD_NW; ++k) {
+            lo0 = min(lo0, red[0][k]); hi0 = max(hi0, red[1][k]);
+            lo1 = min(lo1, red[2][k]); hi1 = max(hi1, red[3][k]);
+        }
+        cb[blockIdx.x] = make_int4(lo0, hi0, lo1, hi1);
     }
 }
+
+template <int TC>
+__global__ void __launch_bounds__(DD_NT) box_gather_kernel(gather_items it, const int4* cb,
+                                                           int nchunks, int ny0, int ny1,
+                                                           const double* base, double* out) {
+    constexpr int TR = DD_NT / TC;
+    __shared__ int4 sbox[DD_NT];
+    __shared__ int64_t soff[DD_NT];
+    __shared__ double ssc[DD_NT];
+    __shared__ int wcnt[DD_NW + 1];
+    const int tiles1 = (ny1 + TC - 1) / TC;
+    const int r0 = (blockIdx.x / tiles1) * TR, c0 = (blockIdx.x % tiles1) * TC;
+    const int y0 = r0 + threadIdx.x / TC, y1 = c0 + threadIdx.x % TC;
+    const bool valid = y0 < ny0 && y1 < ny1;
+    const int64_t node = (int64_t)y0 * ny1 + y1;
+    double acc = (valid && base) ? base[node] : 0.0;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int4 c = cb[ch];
+        if (c.x >= r0 + TR || c.y <= r0 || c.z >= c0 + TC || c.w <= c0) continue;
+        const int i = ch * DD_NT + threadIdx.x;
+        int4 b = make_int4(0, 0, 0, 0);
+        bool hit = false;
+        if (i < it.n && item_live(it, i, b))
+            hit = b.x < r0 + TR && b.x + b.y > r0 && b.z < c0 + TC && b.z + b.w > c0;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (l == 0) wcnt[w] = __popc(m);
+        __syncthreads();
+        int pre = 0, tot = 0;
+        for (int k = 0; k < DD_NW; ++k) {
+            pre += (k < w) ? wcnt[k] : 0;
+            tot += wcnt[k];
+        }
+        if (hit) {
+            const int pos = pre + __popc(m & ((1u << l) - 1u));
+            sbox[pos] = b;
+            soff[pos] = it.voff ? it.voff[(int64_t)i * it.voff_stride] : (int64_t)i * it.vstride;
+            ssc[pos] = it.scale ? it.scale[i] : 1.0;
+        }
+        __syncthreads();
+        if (valid) {
+            for (int k = 0; k < tot; ++k) {
+                const int4 bb = sbox[k];
+                const int a0 = y0 - bb.x, a1 = y1 - bb.z;
+                if (a0 >= 0 && a0 < bb.y && a1 >= 0 && a1 < bb.w) {
+                    const double v = it.vals[soff[k] + (int64_t)a0 * bb.w + a1];
+                    acc = it.scale ? __dadd_rn(acc, __dmul_rn(ssc[k], v)) : __dadd_rn(acc, v);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (valid) out[node] = acc;
+}
+
+}  // namespace dd
+
+// host launcher shared by dd_assemble and dd_blend_energy (cell.cu)
+int dd_box_gather(int n, const int32_t* box, int bstride, const double* vals, int64_t vstride,
+                  const int64_t* voff, int voff_stride, const double* scale, int ny0, int ny1,
+                  const double* base, double* out, cudaStream_t st) {
+    const int nchunks = (n + DD_NT - 1) / DD_NT;
+    int4* cb = nullptr;
+    cudaError_t e;
+    if (nchunks > 0) {
+        e = cudaMallocAsync((void**)&cb, sizeof(int4) * nchunks, st);
+        if (e != cudaSuccess) return dd_set_error(e);
+        dd::gather_items it{n, box, bstride, vals, vstride, voff, voff_stride, scale};
+        dd::chunk_bbox_kernel<<<nchunks, DD_NT, 0, st>>>(it, cb);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
+    dd::gather_items it{n, box, bstride, vals, vstride, voff, voff_stride, scale};
+    if (ny0 == 1) {
+        const int tiles = (ny1 + DD_NT - 1) / DD_NT;
+        dd::box_gather_kernel<DD_NT><<<tiles, DD_NT, 0, st>>>(it, cb, nchunks, ny0, ny1, base, out);
+    } else {
+        const int tiles = ((ny0 + DD_NT / 32 - 1) / (DD_NT / 32)) * ((ny1 + 31) / 32);
+        dd::box_gather_kernel<32><<<tiles, DD_NT, 0, st>>>(it, cb, nchunks, ny0, ny1, base, out);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return dd_set_error(e);
+    if (cb) {
+        e = cudaFreeAsync(cb, st);
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
+    return 0;
+}
+
+namespace dd {
 
 // per basic cell: [transport, kl, d1_i, 0]
 __global__ void __launch_bounds__(DD_NT) cell_terms_kernel(dd_geom g, dd_state s, double* pc) {
@@ -825,11 +957,8 @@ extern "C" int dd_grid_kl(int64_t n, const double* y, const double* nu, int clip
 }
 
 extern "C" int dd_assemble(const dd_geom* g, const dd_state* s, double* out, void* stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(out, 0, (size_t)g->ny0 * g->ny1 * sizeof(double), st);
-    if (e != cudaSuccess) return dd_set_error(e);
-    if (s->n_basic > 0) dd::assemble_kernel<<<s->n_basic, DD_NT, 0, st>>>(*g, *s, out);
-    return dd_set_error(cudaGetLastError());
+    return dd_box_gather(s->n_basic, s->ybox, 4, s->yval, s->cap, nullptr, 0, nullptr, g->ny0,
+                         g->ny1, nullptr, out, (cudaStream_t)stream);
 }
 
 extern "C" int dd_energy_terms(const dd_geom* g, const dd_state* s, const double* y,

@@ -47,31 +47,66 @@ __all__ = [
     "initial_plan_state", "warm_start_plan", "BlendScorer", "get_weights_safe",
     "get_weights_swift", "get_weights_opt", "StitchedGapEvaluator", "IterationStats",
     "iteration_sequential", "iteration_parallel", "domdec_solve", "ShardSpec", "set_shard",
-    "clear_shard",
+    "clear_shard", "ExecMode", "set_exec_mode", "get_exec_mode",
 ]
 
 STRATEGY_KINDS = ("sequential", "safe", "fast", "swift", "opt", "staggered")
 import os as _os
 
-# dynamic shared memory budget per CTA (227 KB opt-in on sm_100a minus the solve
-# kernel's ~3 KB of static shared memory); DD_FORCE_GLOBAL_WS=1 forces the
-# global-memory workspace path (used by the tests to cover it)
-def _occupancy() -> int:
-    try:
-        h = _lib.load()
-        return int(h.dd_cell_min_blocks())
-    except Exception:
-        return 1
-
-
-_OCC = _occupancy()
-SMEM_LIMIT = 0 if _os.environ.get("DD_FORCE_GLOBAL_WS") == "1" else (220 * 1024) // _OCC - 1024 * (_OCC - 1)
-CLUSTER_SMEM = (220 * 1024) // _OCC - 1024 * (_OCC - 1)
+# dynamic shared memory budget per CTA: 227 KB opt-in on sm_100a minus the solve
+# kernel's ~3 KB of static shared memory, split over the CTAs the build keeps
+# resident per SM (dd_cell_min_blocks; queried lazily, so importing the package
+# maps no library).
 CLUSTER_SIZES = (2, 4, 8, 16)
-# test switches: DD_FORCE_CLUSTER=C runs every cell through the cluster kernel
-# with C CTAs; DD_NO_CLUSTER=1 keeps large cells on the single-CTA global path
-_FORCE_CLUSTER = int(_os.environ.get("DD_FORCE_CLUSTER", "0") or 0)
-_NO_CLUSTER = _os.environ.get("DD_NO_CLUSTER") == "1"
+_OCC_CACHE: list = []
+
+
+def _occupancy() -> int:
+    if not _OCC_CACHE:
+        _OCC_CACHE.append(int(_lib.lib().dd_cell_min_blocks()))
+    return _OCC_CACHE[0]
+
+
+def _smem_budget() -> int:
+    occ = _occupancy()
+    return (220 * 1024) // occ - 1024 * (occ - 1)
+
+
+@dataclass
+class ExecMode:
+    """Which execution path the cell solves take (runtime-settable; tests cover each).
+
+    ``force_cluster=C`` runs every cell's Sinkhorn loop on a C-CTA thread-block
+    cluster; ``force_global_ws`` puts every cell's workspace in the global arena
+    (single-CTA kernel); ``no_cluster`` keeps large cells on the single-CTA
+    global-workspace path.  Defaults come from DD_FORCE_CLUSTER /
+    DD_FORCE_GLOBAL_WS / DD_NO_CLUSTER."""
+
+    force_cluster: int = 0
+    force_global_ws: bool = False
+    no_cluster: bool = False
+    skip_stagnant: bool = True
+
+
+def _env_mode() -> ExecMode:
+    return ExecMode(force_cluster=int(_os.environ.get("DD_FORCE_CLUSTER", "0") or 0),
+                    force_global_ws=_os.environ.get("DD_FORCE_GLOBAL_WS") == "1",
+                    no_cluster=_os.environ.get("DD_NO_CLUSTER") == "1",
+                    skip_stagnant=_os.environ.get("DD_NO_SKIP") != "1")
+
+
+_MODE = [_env_mode()]
+
+
+def set_exec_mode(mode: ExecMode | None = None, **kw) -> ExecMode:
+    """Set the cell-solve execution path; returns the previous mode."""
+    prev = _MODE[0]
+    _MODE[0] = mode if mode is not None else ExecMode(**kw)
+    return prev
+
+
+def get_exec_mode() -> ExecMode:
+    return _MODE[0]
 
 
 def _cluster_ws(nw0: int, nw1: int, ny0: np.ndarray, ny1: np.ndarray, C: int) -> np.ndarray:
@@ -317,8 +352,6 @@ class PlanState:
         out = out if out is not None else self.dp.empty_y()
         _lib.check(_lib.lib().dd_assemble(self.dp.geom, self.state_struct(), out.data_ptr(),
                                           _lib.stream_handle()))
-        if _SHARD is not None and _SHARD.world > 1:
-            _SHARD.broadcast(out[:self.dp.ny])
         return out
 
     def energy_terms(self, y) -> np.ndarray:
@@ -452,12 +485,16 @@ def _member_boxes(st: PlanState, pt: _PartTables, ids) -> np.ndarray:
 
 def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta: float = 1e-3,
                     max_iters: int = 20_000, trunc_threshold: float = 1e-15,
-                    dp: DeviceProblem | None = None) -> PlanState:
-    """Loose global presolve, plan cut along basic cells, duals seeded (engine.py:260-345)."""
+                    dp: DeviceProblem | None = None, alpha0=None, beta0=None) -> PlanState:
+    """Loose global presolve, plan cut along basic cells, duals seeded (engine.py:260-345).
+
+    ``alpha0``/``beta0`` warm-start the presolve (the multiscale driver passes
+    duals prolonged from the previous layer; ``max_iters=0`` cuts the plan of
+    those duals directly)."""
     import torch
 
     dp = dp if dp is not None else DeviceProblem(problem)
-    res = sinkhorn_solve(dp, config=SolverConfig(delta=delta, max_iters=max_iters))
+    res = sinkhorn_solve(dp, alpha0, beta0, config=SolverConfig(delta=delta, max_iters=max_iters))
     st = PlanState(problem, partitions.basic, dp, cap=1)
     L = _lib.lib()
     trunc_out = torch.zeros(st.n_basic, dtype=torch.float64, device=dp.device)
@@ -496,12 +533,10 @@ class ShardSpec:
     only the cell solves of each batch are partitioned (cost-balanced by window
     size).  Each rank solves its own cells, the solve's output arenas (zero for
     cells owned elsewhere) are summed across ranks (adding zeros is exact), and
-    everything downstream proceeds identically everywhere.  The two kernels
-    that accumulate with float atomics (the Y-marginal assembly and the blend
-    scatter) are not bitwise reproducible, so the assembled Y-marginal and the
-    weight decision are taken from rank 0 and broadcast; every other step is
-    deterministic, which keeps the ranks' states, window layouts and control
-    flow identical.
+    everything downstream proceeds identically everywhere: every kernel is
+    deterministic (the Y-marginal assembly and the blend are fixed-order
+    gathers, no float atomics), so the ranks' states, window layouts and
+    control flow stay bitwise identical without any broadcast.
     """
 
     def __init__(self, group=None):
@@ -631,8 +666,10 @@ class _Batch:
         moff = np.concatenate([[0], np.cumsum(6 * nmem * ny)[:-1]]).astype(np.int64)
         xoff = np.concatenate([[0], np.cumsum(nmem * st.bs)[:-1]]).astype(np.int64)
         ws = _ws_total(pt.nw0, pt.nw1, ny0, ny1).astype(np.int64)
-        fits = ws * 8 <= SMEM_LIMIT
-        if _FORCE_CLUSTER:
+        mode = _MODE[0]
+        budget = _smem_budget()
+        fits = ws * 8 <= (0 if mode.force_global_ws else budget)
+        if mode.force_cluster:
             fits = np.zeros_like(fits)
         # cells whose workspace fits run in shared memory (sized for the largest
         # of them); the rest get global-arena slots
@@ -647,11 +684,11 @@ class _Batch:
         clu = np.zeros(n, dtype=bool)
         csize = np.zeros(n, dtype=np.int64)
         csmem = np.zeros(n, dtype=np.int64)
-        if big.any() and not _NO_CLUSTER:
-            sizes = (_FORCE_CLUSTER,) if _FORCE_CLUSTER else CLUSTER_SIZES
+        if big.any() and not mode.no_cluster and not mode.force_global_ws:
+            sizes = (mode.force_cluster,) if mode.force_cluster else CLUSTER_SIZES
             for C in sizes:
                 cws = _cluster_ws(pt.nw0, pt.nw1, ny0, ny1, C) * 8
-                ok = big & ~clu & (cws <= CLUSTER_SMEM) & (ny0 >= C)
+                ok = big & ~clu & (cws <= budget) & (ny0 >= C)
                 csize[ok] = C
                 csmem[ok] = cws[ok]
                 clu |= ok
@@ -731,7 +768,7 @@ class _Batch:
             smem_mode=1 if smem_mode else 0, smem_bytes=smem_bytes if smem_mode else 0,
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
-            lout=self.lout.data_ptr(), skip_stagnant=0 if _os.environ.get("DD_NO_SKIP") == "1" else 1)
+            lout=self.lout.data_ptr(), skip_stagnant=1 if mode.skip_stagnant else 0)
         self.cfg = cfg
 
     def solve(self):
@@ -1143,19 +1180,6 @@ def iteration_parallel(plan: PlanState, part: CompositePartition, strategy: Stra
                 theta = np.full(kb, 1.0 / kb)
                 actions.append("safe-fallback")
                 stats.safe_fallbacks += 1
-        if bt.shard is not None:
-            # one decision for all ranks (the blend energies use float atomics)
-            import torch
-            th = torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64)).to(plan.dp.device)
-            bt.shard.broadcast(th)
-            theta = th.cpu().numpy()
-            if strategy.kind == "staggered":
-                greedy = bool(np.all(theta == 1.0))
-                if actions[-1] == "safe-fallback" and greedy:
-                    stats.safe_fallbacks -= 1
-                if actions[-1] == "greedy" and not greedy:
-                    stats.safe_fallbacks += 1
-                actions[-1] = "greedy" if greedy else "safe-fallback"
         stats.score_time += time.perf_counter() - t0
         t0 = time.perf_counter()
         e = bt.commit(theta, ag, None)

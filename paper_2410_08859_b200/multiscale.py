@@ -20,12 +20,23 @@ grids refined x2 per level from ``n_coarsest`` up to the problem grid):
 * each eps stage is one ``domdec_solve`` warm-started from the previous
   stage's plan, cell duals and certificate duals.
 
+``protocol="spec"`` (the default) is SPEC ``multiscale_solve`` / paper §4.3.1
+(PAPER.md:1291-1294): per-layer eps ladder 2dx^2 -> dx^2/2 (seams coincide),
+global unbalanced Sinkhorn at tolerance delta/4 on every layer below the
+switch layer (l_switch = 8 for N >= 512, else log2 N - 1; layer l holds
+2^(l+1) nodes per axis, so for N < 512 only the finest layer runs domdec),
+a global Sinkhorn presolve at the switch layer (warm-started from the
+prolonged duals, same delta/4) whose plan is cut along the basic cells
+(``warm_start_plan``), and domdec (staggered) from there on.  ``protocol="ladder"`` keeps the round-1 schedule
+(one loose warm start at the coarsest level, domdec at every level).
+
 All numerical work runs in libdomdec_b200; host code here only builds the
 pyramid (input preparation) and sequences the stages.
 """
 
 from __future__ import annotations
 
+import math
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -37,10 +48,12 @@ from .decomposition import make_decomposition
 from .engine import (EngineConfig, PlanState, StitchedGapEvaluator, StrategyConfig, _member_boxes,
                      _tables, domdec_solve, warm_start_plan)
 from .grids import Grid, GridMeasure, TransportProblem
-from .sinkhorn import DeviceProblem
+from .report import SolveReport
+from .sinkhorn import DeviceProblem, SolverConfig, sinkhorn_solve
 
-__all__ = ["Level", "build_pyramid", "stage_pyramid", "eps_schedule", "refine_plan",
-           "MultiscaleReport", "multiscale_solve"]
+__all__ = ["Level", "build_pyramid", "stage_pyramid", "eps_schedule", "spec_eps_schedule",
+           "switch_layer", "layer_index", "refine_plan", "prolong_duals", "MultiscaleReport",
+           "multiscale_solve"]
 
 
 @dataclass
@@ -108,6 +121,53 @@ def eps_schedule(levels: list, eps_start: float, eps_final: float, final_stages:
         if per[li - 1] and per[li]:
             per[li] = [e for e in per[li] if e <= per[li - 1][-1]]
     return per
+
+
+def layer_index(n: int) -> int:
+    """Paper layer number of an n-node axis: layer l holds 2^(l+1) nodes (finest = log2 N - 1)."""
+    return int(round(math.log2(n))) - 1
+
+
+def switch_layer(n_finest: int) -> int:
+    """First domdec layer: 8 for N >= 512, else floor(log2 N) - 1."""
+    return 8 if n_finest >= 512 else int(math.floor(math.log2(n_finest))) - 1
+
+
+def spec_eps_schedule(levels: list, eps_start: float, eps_final: float) -> list:
+    """Per level, its eps ladder (SPEC eps_schedule): 2dx^2, dx^2, dx^2/2 on every
+    layer, so a layer's last value is the next layer's first; clipped to
+    [eps_final, eps_start].  A layer whose whole ladder lies above eps_start
+    runs eps_start; the finest layer ends on eps_final."""
+    per = []
+    top = float(eps_start)
+    for li, lv in enumerate(levels):
+        d2 = lv.grid.dx ** 2
+        lad = [2.0 * d2, d2, 0.5 * d2]
+        if li == len(levels) - 1:
+            lad.append(0.25 * d2)
+        row = [e for e in lad if eps_final * (1 - 1e-12) <= e <= top * (1 + 1e-12)]
+        if not row:
+            row = [min(top, max(lad[0], eps_final))]
+        if li == len(levels) - 1 and abs(row[-1] - eps_final) > 1e-12 * eps_final:
+            row = [e for e in row if e > eps_final] + [float(eps_final)]
+        per.append(row)
+        top = row[-1]
+    return per
+
+
+def prolong_duals(duals, coarse_geom, fine_geom):
+    """Bilinear prolongation of an (alpha, beta) pair to the next finer layer (dd_prolong)."""
+    import torch
+
+    ca, cb = duals
+    fa = torch.empty(fine_geom.nx0 * fine_geom.nx1, dtype=torch.float64, device=ca.device)
+    fb = torch.empty(fine_geom.ny0 * fine_geom.ny1, dtype=torch.float64, device=ca.device)
+    L = _lib.lib()
+    _lib.check(L.dd_prolong(fine_geom.nx0, fine_geom.nx1, coarse_geom.nx0, coarse_geom.nx1,
+                            ca.data_ptr(), fa.data_ptr(), _lib.stream_handle()))
+    _lib.check(L.dd_prolong(fine_geom.ny0, fine_geom.ny1, coarse_geom.ny0, coarse_geom.ny1,
+                            cb.data_ptr(), fb.data_ptr(), _lib.stream_handle()))
+    return fa, fb
 
 
 def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
@@ -204,40 +264,98 @@ def _with_eps(lv: Level, lam_div, eps: float) -> TransportProblem:
     return TransportProblem(GridMeasure(lv.grid, lv.mu), GridMeasure(lv.grid, lv.nu), lam_div, eps)
 
 
+def _global_report(res, eps: float, t: float, delta: float) -> SolveReport:
+    return SolveReport(converged=bool(res.converged), iterations=int(res.iterations),
+                       final_score={}, rel_pd_gap=float("nan"), x_err=0.0, y_err=0.0,
+                       timings={"total": t, "solve": t, "score": 0.0, "commit": 0.0},
+                       diagnostics={"solver": "sinkhorn", "gap": float(res.gap), "delta": delta,
+                                    "cell_iterations": 0, "cell_flops": 0.0,
+                                    "nonconverged_cells": 0, "safe_fallbacks": 0})
+
+
 def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int, eps_start: float,
                      eps_final: float | None = None, strategy: StrategyConfig = StrategyConfig(),
                      config: EngineConfig = EngineConfig(), warm_delta: float = 1e-3,
                      warm_max_iters: int = 20_000, progress=None, levels: list | None = None,
-                     final_stages: int = 1):
+                     final_stages: int = 1, protocol: str = "spec", switch: int | None = None,
+                     global_delta: float | None = None, global_max_iters: int = 100_000,
+                     switch_delta: float | None = None, switch_iters: int = 20_000):
     """Solve ``problem`` coarse-to-fine; returns (fine PlanState, MultiscaleReport).
 
     ``levels`` may carry a pre-built (and device-staged) pyramid from
-    :func:`build_pyramid` / :func:`stage_pyramid`.
+    :func:`build_pyramid` / :func:`stage_pyramid`.  ``protocol="spec"``:
+    global Sinkhorn at ``global_delta`` (default delta/4) below layer
+    ``switch`` (default :func:`switch_layer`), then domdec; at the switch layer
+    the plan comes from ``warm_start_plan`` warm-started with the prolonged
+    duals: global Sinkhorn to ``switch_delta`` (default: the coarse-layer
+    tolerance delta/4, so the first marginal handed to domdec is as close to
+    optimal as on the layers below), at most ``switch_iters``
+    iterations, then the plan cut along the basic cells.  ``protocol="ladder"``: the round-1 schedule
+    (``warm_delta`` warm start at the coarsest level, domdec at every level).
     """
+    if protocol not in ("spec", "ladder"):
+        raise ValueError(f"unknown multiscale protocol {protocol!r}")
     t_all = time.perf_counter()
     eps_final = problem.eps if eps_final is None else eps_final
     if levels is None:
         levels = build_pyramid(problem.mu, problem.nu, n_coarsest)
-    sched = eps_schedule(levels, eps_start, eps_final, final_stages)
+    n_fine = max(levels[-1].grid.dims)
+    lsw = (switch_layer(n_fine) if switch is None else int(switch)) if protocol == "spec" else -1
+    sched = (spec_eps_schedule(levels, eps_start, eps_final) if protocol == "spec"
+             else eps_schedule(levels, eps_start, eps_final, final_stages))
+    gdelta = config.delta / 4.0 if global_delta is None else float(global_delta)
     rep = MultiscaleReport(converged=True)
     state = None
     duals = None
-    timings = {"warm": 0.0, "refine": 0.0, "domdec": 0.0}
+    duals_geom = None
+    timings = {"global": 0.0, "warm": 0.0, "refine": 0.0, "domdec": 0.0}
     for li, lv in enumerate(levels):
         eps_list = sched[li] or [None]
         first_eps = eps_list[0] if eps_list[0] is not None else (
             next((e for row in sched[li:] for e in row), eps_final))
         prob = _with_eps(lv, problem.div, first_eps)
+        if lv.dp is not None:
+            lv.dp.problem = prob
+            lv.dp.geom.eps = float(prob.eps)
+        if protocol == "spec" and layer_index(max(lv.grid.dims)) < lsw and li < len(levels) - 1:
+            # coarse layer: global unbalanced Sinkhorn at delta/4 (PAPER.md:1291-1294)
+            dp = lv.dp if lv.dp is not None else DeviceProblem(prob)
+            a0 = b0 = None
+            if duals is not None:
+                a0, b0 = prolong_duals(duals, duals_geom, dp.geom)
+            for eps in eps_list:
+                dp.problem = _with_eps(lv, problem.div, eps)
+                dp.geom.eps = float(eps)
+                t0 = time.perf_counter()
+                res = sinkhorn_solve(dp, a0, b0, SolverConfig(delta=gdelta,
+                                                              max_iters=global_max_iters))
+                t = time.perf_counter() - t0
+                timings["global"] += t
+                a0, b0 = res.alpha, res.beta
+                r = _global_report(res, eps, t, gdelta)
+                rep.stages.append((lv.grid.dims[0], eps, r))
+                rep.converged = rep.converged and r.converged
+                if progress is not None:
+                    progress(lv.grid.dims[0], eps, r)
+            duals, duals_geom = (a0, b0), dp.geom
+            continue
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             dec = make_decomposition(prob.mu, cell_size)
         t0 = time.perf_counter()
-        if lv.dp is not None:
-            lv.dp.problem = prob
-            lv.dp.geom.eps = float(prob.eps)
         if state is None:
-            state = warm_start_plan(prob, dec, delta=warm_delta, max_iters=warm_max_iters,
-                                    dp=lv.dp)
+            if protocol == "spec":
+                a0 = b0 = None
+                if duals is not None:
+                    dp = lv.dp if lv.dp is not None else DeviceProblem(prob)
+                    a0, b0 = prolong_duals(duals, duals_geom, dp.geom)
+                state = warm_start_plan(prob, dec,
+                                        delta=gdelta if switch_delta is None else switch_delta,
+                                        max_iters=switch_iters,
+                                        dp=lv.dp, alpha0=a0, beta0=b0)
+            else:
+                state = warm_start_plan(prob, dec, delta=warm_delta, max_iters=warm_max_iters,
+                                        dp=lv.dp)
             timings["warm"] += time.perf_counter() - t0
         else:
             state = refine_plan(state, prob, dec, duals, config.cell.trunc_threshold, dp=lv.dp)
@@ -265,6 +383,7 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
             if progress is not None:
                 progress(lv.grid.dims[0], eps, r)
         duals = state.global_duals
+        duals_geom = state.dp.geom
     timings["total"] = time.perf_counter() - t_all
     rep.timings = timings
     return state, rep

@@ -88,14 +88,33 @@ CASES = [
          max_iters=4, warm=True, seed=11, uniform=False, zero_mu=True, nu_scale=1.1),
 ]
 
+# BASELINE.json configs[0] (the PR1 correctness model) on its own generator
+# (paper_2410_08859_b200.problems.config_problem_arrays(0, seed=0): 64^2, 3
+# Gaussians + 1e-4 floor, masses 1.0 / 1.3), lam = 1, eps = 2h^2, 4x4 basic
+# cells, staggered, warm start (reference warm_start_plan, delta 1e-3), exactly
+# 30 domdec sweeps (global delta 1e-12 never stops early) with the cell
+# Sinkhorn tolerance 1e-7 (cell_delta_factor 1e5).  Slow: ~1 h of reference CPU.
+BASELINE_CASES = [
+    dict(name="pr1_64", baseline=0, s=4, lam=1.0, strategy="staggered", delta=1e-12,
+         cell_delta_factor=1e5, max_iters=30, warm=True, seed=0),
+]
+
 
 def run_case(eng, meas, c):
-    dims = c["dims"]
-    n = dims[0] if len(dims) == 1 else dims[0]
-    dx = 1.0 / n
-    origin = tuple(0.5 * dx for _ in dims)
-    rng = np.random.default_rng(c["seed"])
-    if c.get("uniform"):
+    if "baseline" in c:
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        from paper_2410_08859_b200.problems import config_problem_arrays
+        mu, nu, dx, origin, _ = config_problem_arrays(c["baseline"], seed=c["seed"])
+        dims = mu.shape
+    else:
+        dims = c["dims"]
+        n = dims[0] if len(dims) == 1 else dims[0]
+        dx = 1.0 / n
+        origin = tuple(0.5 * dx for _ in dims)
+        rng = np.random.default_rng(c["seed"])
+    if "baseline" in c:
+        pass
+    elif c.get("uniform"):
         origin = tuple(0.0 for _ in dims)
         mu = np.full(dims, 1.0 / np.prod(dims))
         nu = np.full(dims, 1.0 / np.prod(dims))
@@ -115,13 +134,14 @@ def run_case(eng, meas, c):
         warnings.simplefilter("ignore")
         dec = eng.make_decomposition(prob.mu, c["s"])
     cell = eng.CellSolverConfig(max_iters=c.get("cell_max_iters", 10_000))
-    cfg = eng.EngineConfig(delta=c["delta"], max_iters=c["max_iters"], cell=cell)
+    cfg = eng.EngineConfig(delta=c["delta"], max_iters=c["max_iters"], cell=cell,
+                           cell_delta_factor=c.get("cell_delta_factor", 0.25))
     state = eng.warm_start_plan(prob, dec, delta=1e-3) if c["warm"] else None
     st, rep = eng.domdec_solve(prob, dec, eng.StrategyConfig(kind=c["strategy"]), cfg, state=state)
     out = dict(mu=mu, nu=nu, dx=dx, origin=np.array(origin), lam=c["lam"], eps=eps, s=c["s"],
                cell_max_iters=c.get("cell_max_iters", 10_000),
                strategy=c["strategy"], delta=c["delta"], max_iters=c["max_iters"],
-               warm=c["warm"])
+               warm=c["warm"], cell_delta_factor=c.get("cell_delta_factor", 0.25))
     boxes, vals, offs = [], [], [0]
     for m in st.nu_i:
         b = [x for ax in m.box for x in ax]
@@ -217,11 +237,17 @@ def main():
     eng, meas, sk = _import_ref()
     OUT.mkdir(parents=True, exist_ok=True)
     only = set(sys.argv[1:])
-    kernel_fixtures(sk, meas)
-    for c in CASES:
+    if not only or only & {"kernels"}:
+        kernel_fixtures(sk, meas)
+    for c in CASES + BASELINE_CASES:
+        if not only and c in BASELINE_CASES:
+            continue   # slow: generate explicitly by name
         if only and c["name"] not in only:
             continue
+        import time as _t
+        t0 = _t.perf_counter()
         out = run_case(eng, meas, c)
+        out["ref_seconds"] = _t.perf_counter() - t0
         np.savez_compressed(OUT / f"{c['name']}.npz", **out)
         print(c["name"], "iters", out["iterations"], "total", out["score"][-1],
               "size", os.path.getsize(OUT / f"{c['name']}.npz"))

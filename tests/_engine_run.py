@@ -28,7 +28,9 @@ def run_device(g):
         warnings.simplefilter("ignore")
         dec = make_decomposition(prob.mu, int(g["s"]))
     cfg = EngineConfig(delta=float(g["delta"]), max_iters=int(g["max_iters"]),
-                       cell=CellSolverConfig(max_iters=cell_cap(g)))
+                       cell=CellSolverConfig(max_iters=cell_cap(g)),
+                       cell_delta_factor=float(g["cell_delta_factor"]) if "cell_delta_factor" in g
+                       else 0.25)
     state = warm_start_plan(prob, dec, delta=1e-3) if bool(g["warm"]) else None
     st, rep = domdec_solve(prob, dec, StrategyConfig(kind=str(g["strategy"])), cfg, state=state)
     return prob, dec, st, rep

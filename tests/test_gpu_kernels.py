@@ -29,8 +29,31 @@ def test_newton_nodes_match_reference_grid():
     np.testing.assert_allclose(got, g["beta"], rtol=1e-12, atol=1e-300)
 
 
+def _bisect_root(m, z, eps, lam):
+    """Bisection oracle for g(b) = log(m + exp(b/eps + z)) + b/lam = 0 (increasing in b),
+    run until the bracket is two adjacent doubles."""
+    ratio = eps * lam / (eps + lam)
+    with np.errstate(divide="ignore"):
+        lm = np.log(m)
+    hi = np.minimum(-lam * lm, -ratio * z)
+    hi = hi + 1e-6 * (1.0 + np.abs(hi))      # rounding margin: g(hi) >= 0 strictly
+    lo = hi - lam * np.log(2.0) * 1.01 - 1.0
+    g = lambda b: np.logaddexp(lm, b / eps + z) + b / lam  # noqa: E731
+    assert np.all(g(lo) <= 0) and np.all(g(hi) >= 0)
+    for _ in range(2200):
+        mid = 0.5 * (lo + hi)
+        up = g(mid) > 0
+        hi = np.where(up, mid, hi)
+        lo = np.where(up, lo, mid)
+        if np.all(np.nextafter(lo, np.inf) >= hi):
+            break
+    return 0.5 * (lo + hi)
+
+
 def test_newton_residual_and_bisection_agreement_random():
-    """g(beta) ~ 0 and agreement with a bisection oracle on a 10^4-point grid (SPEC crit. 2)."""
+    """SPEC acceptance criterion 2: on a 10^4-point randomized (m, z, eps, lam)
+    grid, residual |g(beta)| <= 1e-12 (scaled), agreement with an independent
+    bisection oracle <= 1e-10, and the closed form at m = 0 exact."""
     import torch
     from paper_2410_08859_b200 import _lib
 
@@ -52,6 +75,32 @@ def test_newton_residual_and_bisection_agreement_random():
     assert np.max(np.abs(res)) <= 1e-12 * 10  # residual scale O(1) after the log
     ratio = eps * lam / (eps + lam)
     np.testing.assert_allclose(b[~gen], -ratio[~gen] * z[~gen], rtol=1e-15)
+    bis = _bisect_root(m[gen], z[gen], eps[gen], lam[gen])
+    err = np.abs(b[gen] - bis) / np.maximum(1.0, np.abs(bis))
+    assert err.max() <= 1e-10, err.max()
+
+
+def test_assemble_is_the_sequential_cell_order_sum_bitwise():
+    """dd_assemble (fixed-order gather) equals the reference's assemble_y_marginal
+    (measures.py:410-425: zeros, then += each cell's box in index order) bit for bit."""
+    import warnings
+    from _engine_run import problem_from_golden
+    from paper_2410_08859_b200.decomposition import make_decomposition
+    from paper_2410_08859_b200.engine import warm_start_plan
+
+    g = load("mix32_staggered")
+    prob = problem_from_golden(g)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        dec = make_decomposition(prob.mu, int(g["s"]))
+    st = warm_start_plan(prob, dec, delta=1e-3)
+    got = st.assemble_device().cpu().numpy().reshape(prob.nu.mass.shape)
+    want = np.zeros(prob.nu.mass.shape)
+    for m in st.nu_i:
+        if m.is_empty:
+            continue
+        want[tuple(slice(o, o + e) for o, e in m.box)] += m.values
+    assert np.array_equal(got, want)
 
 
 def test_grid_sweeps_match_reference():

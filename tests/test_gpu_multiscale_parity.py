@@ -66,7 +66,7 @@ def test_finest_stage_matches_oracle_from_refined_state():
     try:
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            M.multiscale_solve(prob, 4, 16, 8 * h2)
+            M.multiscale_solve(prob, 4, 16, 8 * h2, protocol="ladder")
     except StopIteration:
         pass
     finally:

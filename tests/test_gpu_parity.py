@@ -18,9 +18,23 @@ OBJ_TOL = 1e-10
 
 DEVICE_CASES = ENGINE_CASES
 
+# every execution path of the cell solve: shared-memory CTA per cell (default),
+# the global-memory workspace (single CTA), thread-block clusters of 2 and 4 CTAs
+EXEC_MODES = {"default": {}, "global_ws": {"force_global_ws": True},
+              "cluster2": {"force_cluster": 2}, "cluster4": {"force_cluster": 4}}
+
+
+@pytest.fixture(params=sorted(EXEC_MODES))
+def exec_mode(request):
+    from paper_2410_08859_b200.engine import set_exec_mode
+
+    prev = set_exec_mode(**EXEC_MODES[request.param])
+    yield request.param
+    set_exec_mode(prev)
+
 
 @pytest.mark.parametrize("name", DEVICE_CASES)
-def test_engine_matches_reference_golden(name):
+def test_engine_matches_reference_golden(name, exec_mode):
     from _engine_run import box4, run_device
 
     g = load(name)
@@ -48,3 +62,21 @@ def test_engine_matches_reference_golden(name):
     np.testing.assert_allclose(st.transport, g["transport"], rtol=1e-9, atol=1e-18)
     np.testing.assert_allclose(st.kl, g["kl"], rtol=1e-9, atol=1e-15)
     assert rep.rel_pd_gap == pytest.approx(float(g["rel_pd_gap"]), rel=1e-6, abs=1e-12)
+
+
+@pytest.mark.parametrize("name", ["mix32_staggered", "mix16_zeros_warm_opt", "toy1d_swift"])
+def test_engine_runs_are_bitwise_reproducible(name):
+    """Two runs of the same solve produce identical bits (no float atomics anywhere)."""
+    from _engine_run import run_device
+
+    g = load(name)
+    _, _, st1, rep1 = run_device(g)
+    _, _, st2, rep2 = run_device(g)
+    assert [r.total for r in rep1.trace] == [r.total for r in rep2.trace]
+    assert [r.gap for r in rep1.trace] == [r.gap for r in rep2.trace]
+    assert np.array_equal(st1.ybox.cpu().numpy(), st2.ybox.cpu().numpy())
+    assert np.array_equal(st1.yval.cpu().numpy(), st2.yval.cpu().numpy())
+    assert np.array_equal(st1.x_marg_d.cpu().numpy(), st2.x_marg_d.cpu().numpy())
+    for k in st1.stores:
+        assert np.array_equal(st1.stores[k].alpha.cpu().numpy(), st2.stores[k].alpha.cpu().numpy())
+        assert np.array_equal(st1.stores[k].beta.cpu().numpy(), st2.stores[k].beta.cpu().numpy())
