@@ -95,8 +95,10 @@ typedef struct dd_batch {
     double* mstat;             /* [n_members_total*4] transport, kl, truncated, extra */
     double* cstat;             /* [n_cells*8] gap, first_gap, iters, conv, nclamped,
                                   newton_clamped, balance_fallbacks, target_miss */
-    double* cstat2;            /* [n_cells*4] drift_nodes, trunc_total, loop cycles,
-                                  Newton evaluations */
+    double* cstat2;            /* [n_cells*8] drift_nodes, trunc_total, loop cycles,
+                                  Newton evaluations, executed Sinkhorn iterations
+                                  (iters above is the reference-equivalent count),
+                                  3 unused */
     int32_t smem_mode;         /* 1: workspace in shared memory */
     int32_t smem_bytes;
     /* solver configuration */
@@ -235,17 +237,6 @@ int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy, int c, dou
 int dd_refine(const dd_geom* g, const dd_state* s, const int32_t* parent, const int32_t* cbox,
               const double* cval, int64_t ccap, const double* cmass, const double* nu_c,
               int cny1, double trunc, double* trunc_out, void* stream);
-
-/* Dual-shaped refinement: as dd_refine, but each child's Y-marginal takes the
- * shape of the diagonal-scaling plan of the (prolonged) fine duals alpha, beta
- * restricted to the child block, over the parent's doubled box, scaled to the
- * child's share of the parent mass.  tmp holds n_basic * tcap doubles (tcap >=
- * 4 * coarse box size); max_fe1 = largest doubled box extent (either axis).  Requires
- * block0 <= 8, block0*block1 <= 64. */
-int dd_refine_dual(const dd_geom* g, const dd_state* s, const int32_t* parent, const int32_t* cbox,
-                   const double* cval, int64_t ccap, const double* cmass, const double* alpha,
-                   const double* beta, double trunc, double* trunc_out, double* tmp, int64_t tcap,
-                   int max_fe1, void* stream);
 
 /* Bilinear prolongation of a cell-centred coarse field (nc0 x nc1) to the
  * x2 finer grid (nf0 x nf1); constant beyond the outer coarse centres. */

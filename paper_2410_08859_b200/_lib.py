@@ -20,7 +20,7 @@ EXPORTS = [
     "dd_newton_global", "dd_global_terms", "dd_cell_solve", "dd_cell_delta", "dd_blend_energy",
     "dd_cell_commit", "dd_assemble", "dd_energy_terms", "dd_product_init", "dd_cut_plan",
     "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
-    "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong", "dd_refine_dual",
+    "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong",
     "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks",
 ]
 
@@ -85,8 +85,6 @@ _SIGS = {
                    vp, vp], C.c_int),
     "dd_refine": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, i64, vp, vp, C.c_int, dbl, vp,
                    vp], C.c_int),
-    "dd_refine_dual": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, i64, vp, vp, vp, dbl, vp, vp,
-                        i64, C.c_int, vp], C.c_int),
     "dd_prolong": ([C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
     "dd_newton_nodes": ([i64, vp, vp, vp, vp, vp, dbl, C.c_int, vp, vp, vp], C.c_int),
     "dd_opt_set": ([C.POINTER(Geom), C.POINTER(Batch), vp, C.c_int, dbl, vp, vp], C.c_int),
@@ -123,7 +121,7 @@ KERNELS_PER_CALL = {
     "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_solve2": 3, "dd_cell_delta": 1, "dd_blend_energy": 6,
     "dd_cell_commit": 1, "dd_assemble": 2, "dd_energy_terms": 4, "dd_product_init": 1,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
-    "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1, "dd_refine_dual": 1,
+    "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
 }
 
 

@@ -139,10 +139,6 @@ __device__ __forceinline__ double negsq(double a, double b, double eps) {
 // min(-c/eps) <= -700; both of its modes agree with this one to rounding).
 
 constexpr double kTiny = 1e-290;
-#ifdef DD_COUNT_FALLBACK
-__device__ unsigned long long g_fallbacks = 0;
-__device__ unsigned long long g_outputs = 0;
-#endif
 
 // Exact 1D log-sum-exp  log sum_k exp(v[k*stride] - (p - q[k])^2 / eps)  (two passes).
 __device__ __forceinline__ double lse1d(const double* v, int64_t stride, int n, double p,
@@ -275,38 +271,11 @@ struct SweepScratch {
     double* redm;   // [2*DD_NW] block-max buffers
     int* flag;      // shared underflow flag
     int* par;       // block-max buffer parity
-#ifdef DD_PHASE_TIMING
-    long long* fb_cycles;   // [2] cycles spent in the staged fallback (X, Y)
-    int* fb_count;          // [4] shared: fallback sweeps (X, Y), underflowed outputs (X, Y)
-#endif
-#ifdef DD_SWEEP_TIMING
-    long long* sub;         // [4] X-sweep sub-phases: prologue+max, exp, stage 1, stage 2
-#endif
 };
-#ifdef DD_SWEEP_TIMING
-#define DD_SUB_(i) do { __syncthreads(); const long long tn_ = clock64(); sc.sub[i] += tn_ - ts_; ts_ = tn_; } while (0)
-#else
-#define DD_SUB_(i) do {} while (0)
-#endif
-#if defined(DD_SWEEP_TIMING) && DD_SWEEP_TIMING == 1
-#define DD_SUBX(i) DD_SUB_(i)
-#else
-#define DD_SUBX(i) do {} while (0)
-#endif
-#if defined(DD_SWEEP_TIMING) && DD_SWEEP_TIMING == 2
-#define DD_SUBY(i) DD_SUB_(i)
-#elif defined(DD_SWEEP_BARRIERS)
-#define DD_SUBY(i) __syncthreads()
-#else
-#define DD_SUBY(i) do {} while (0)
-#endif
 
 __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
-#ifdef DD_SWEEP_TIMING
-    long long ts_ = clock64();
-#endif
     double lmax = kNegInf;
     int y = threadIdx.x;
     // four nodes per pass: all loads issue before the first store (the arrays are
@@ -340,10 +309,8 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
 #pragma unroll
         for (int j = 0; j < 4; ++j) w.wy[y + j * DD_NT] = exp(tv[j] - B);
     }
-    DD_SUBX(0);
     for (; y < ny; y += DD_NT) w.wy[y] = exp(w.ty[y] - B);
     __syncthreads();
-    DD_SUBX(1);
     *sc.par ^= 1;
     double* T = w.mid;   // [ny0][nw1]
     // A warp reads the same k of up to min(nw1, 16) K1 rows, ny1 doubles apart.  They
@@ -378,7 +345,6 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         T[o] = s0 + s1;
     }
     __syncthreads();
-    DD_SUBX(2);
     int bad = 0;
     for (int o = threadIdx.x; o < nx; o += DD_NT) {
         const int x0 = o / nw1, x1 = o - x0 * nw1;
@@ -395,29 +361,15 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         else ++bad;
     }
     if (bad) *sc.flag = 1;
-#ifdef DD_PHASE_TIMING
-    if (bad) atomicAdd(&sc.fb_count[2 + 0], bad);   // outputs that underflowed
-#endif
     __syncthreads();
-    DD_SUBX(3);
     if (*sc.flag) {
-#ifdef DD_PHASE_TIMING
-        const long long t0 = clock64();
-#endif
         cell_lse_x_staged(w, c, nw0, nw1, eps, out);
-#ifdef DD_PHASE_TIMING
-        sc.fb_cycles[0] += clock64() - t0;
-        if (threadIdx.x == 0) sc.fb_count[0] += 1;
-#endif
     }
 }
 
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double ratio, double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
-#ifdef DD_SWEEP_TIMING
-    long long ts_ = clock64();
-#endif
     double lmax = kNegInf;
     for (int x = threadIdx.x; x < nx; x += DD_NT) {
         if (ratio != 0.0) w.alpha[x] = -ratio * w.L[x];
@@ -428,10 +380,8 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     if (threadIdx.x == 0) *sc.flag = 0;
     double A = block_max1(lmax, sc.redm, *sc.par);
     if (!isfinite(A)) A = 0.0;
-    DD_SUBY(0);
     for (int x = threadIdx.x; x < nx; x += DD_NT) w.wx[x] = exp(w.tx[x] - A);
     __syncthreads();
-    DD_SUBY(1);
     *sc.par ^= 1;
     double* T = w.mid;   // [nw0][ny1]
     for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
@@ -447,7 +397,6 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         T[o] = s0 + s1;
     }
     __syncthreads();
-    DD_SUBY(2);
     int bad = 0;
     for (int o = threadIdx.x; o < ny; o += DD_NT) {
         const int y0 = o / ny1, y1 = o - y0 * ny1;
@@ -463,21 +412,10 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         else ++bad;
     }
     if (bad) *sc.flag = 1;
-#ifdef DD_PHASE_TIMING
-    if (bad) atomicAdd(&sc.fb_count[2 + 1], bad);   // outputs that underflowed
-#endif
     __syncthreads();
-    DD_SUBY(3);
     // alpha is already updated; the staged redo must not apply the update twice
     if (*sc.flag) {
-#ifdef DD_PHASE_TIMING
-        const long long t0 = clock64();
-#endif
         cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
-#ifdef DD_PHASE_TIMING
-        sc.fb_cycles[1] += clock64() - t0;
-        if (threadIdx.x == 0) sc.fb_count[1] += 1;
-#endif
     }
 }
 
@@ -560,6 +498,7 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
     __shared__ double red[DD_NW + 1];
     __shared__ int redi[DD_NW + 1];
     __shared__ double xslot[4];          // scalar exchange slots (double-buffered pairs)
+    __shared__ double xslot2[4];
     __shared__ int flag_sh;
 
     const int C = (int)cluster.num_blocks();
@@ -616,6 +555,21 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
         for (int r = 0; r < C; ++r) t += *cluster.map_shared_rank(&xslot[spar], r);
         spar ^= 1;
         return t;
+    };
+    // two sums in one cluster exchange (own slot pair, same parity discipline)
+    auto csum2 = [&](double v0, double v1, double& o1) -> double {
+        v0 = block_sum(v0, red);
+        v1 = block_sum(v1, red);
+        if (tid == 0) { xslot2[2 * spar] = v0; xslot2[2 * spar + 1] = v1; }
+        cluster.sync();
+        double t0 = 0.0, t1 = 0.0;
+        for (int r = 0; r < C; ++r) {
+            t0 += *cluster.map_shared_rank(&xslot2[2 * spar], r);
+            t1 += *cluster.map_shared_rank(&xslot2[2 * spar + 1], r);
+        }
+        spar ^= 1;
+        o1 = t1;
+        return t0;
     };
     auto cmax = [&](double v) -> double {
         v = block_max(v, red);
@@ -755,7 +709,7 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
 
     bool converged = false, have_first = false;
     double gap = __builtin_huge_val(), first_gap = 0.0;
-    int iters = 0, newton_clamped = 0;
+    int iters = 0, newton_clamped = 0, stag_k = 0;
     long long newton_steps = 0;
     const long long t0c = clock64();
     for (int k = 1; k <= b.max_iters; ++k) {
@@ -834,14 +788,16 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
             beta[yl] = nb;
             ndeg += dg;
         }
-        newton_clamped = max(newton_clamped, (int)block_sum((double)ndeg, red));
+        // cluster-wide clamped-node count of this iteration (max over iterations, as
+        // the single-CTA kernel and the reference) and whether any beta moved
+        double n_moved = 0.0;
+        const double nd = csum2((double)ndeg, (double)moved, n_moved);
+        newton_clamped = max(newton_clamped, (int)nd);
         iters = k;
-        if (b.skip_stagnant && k >= 2) {
-            // cluster-wide: did any node's beta change?  (see the single-CTA kernel)
-            if (cmax((double)moved) == 0.0) {
-                iters = b.max_iters;
-                break;
-            }
+        if (b.skip_stagnant && k >= 2 && n_moved == 0.0) {
+            stag_k = k;   // see the single-CTA kernel
+            iters = b.max_iters;
+            break;
         }
     }
     __syncthreads();
@@ -861,10 +817,11 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
         gap = lam * block_sum(part, red);
         if (!have_first) { first_gap = gap; have_first = true; }
         converged = gap / lam <= thr;
+        if (converged && stag_k) iters = stag_k;
     }
     const double cyc = (double)(clock64() - t0c);
     const double nst = csum((double)newton_steps);
-    const double ncl = csum((double)newton_clamped);
+    const double ncl = (double)newton_clamped;
     for (int yl = tid; yl < nyl; yl += DD_NT) b.beta[ybase + yl] = beta[yl];
     if (rank == 0) {
         for (int x = tid; x < nx; x += DD_NT) {
@@ -879,9 +836,10 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
             cs[3] = converged ? 1.0 : 0.0;
             cs[4] = n_clamped;
             cs[5] = ncl;
-            double* c2 = b.cstat2 + (int64_t)c * 4;
+            double* c2 = b.cstat2 + (int64_t)c * 8;
             c2[2] = cyc;
             c2[3] = nst;
+            c2[4] = (double)(stag_k ? stag_k : iters);
         }
     }
     cluster.sync();   // keep every CTA's shared memory alive until remote reads are done
@@ -1023,7 +981,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     bool converged = false;
     bool have_first = false;
     double gap = __builtin_huge_val(), first_gap = 0.0;
-    int iters = 0, newton_clamped = 0;
+    int iters = 0, newton_clamped = 0, stag_k = 0, exec_iters = 0;
     double t_loop_d = 0.0, nsteps = 0.0;
     if (epi) {
         const double* cs = b.cstat + (int64_t)c * 8;
@@ -1033,46 +991,23 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         converged = cs[3] != 0.0;
         n_clamped = (int)cs[4];
         newton_clamped = (int)cs[5];
-        t_loop_d = b.cstat2[(int64_t)c * 4 + 2];
-        nsteps = b.cstat2[(int64_t)c * 4 + 3];
+        t_loop_d = b.cstat2[(int64_t)c * 8 + 2];
+        nsteps = b.cstat2[(int64_t)c * 8 + 3];
     } else {
         const long long t_loop0 = clock64();
-    #ifdef DD_NEWTON_STATS
-        int nst[4] = {0, 0, 0, 0};   // clips, bisections, max evals, nodes with >= 6 evals
-    #endif
         long long newton_steps = 0;
         __shared__ double red2[2 * DD_NW];
         __shared__ double redm[2 * DD_NW];
         __shared__ int sweep_flag;
         int mpar = 0;
-#if defined(DD_SWEEP_TIMING)
-        long long fbc[2] = {0, 0};
-        __shared__ int fbn[4];
-        if (tid < 4) fbn[tid] = 0;
-        long long subc[4] = {0, 0, 0, 0};
-        const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn, subc};
-#elif defined(DD_PHASE_TIMING)
-        long long fbc[2] = {0, 0};
-        __shared__ int fbn[4];
-        if (tid < 4) fbn[tid] = 0;
-        const SweepScratch sc{redm, &sweep_flag, &mpar, fbc, fbn};
-#else
         const SweepScratch sc{redm, &sweep_flag, &mpar};
-#endif
         __shared__ int ndeg_sh[2];
         __shared__ int moved_sh[2];
         if (tid < 2) { ndeg_sh[tid] = 0; moved_sh[tid] = 0; }
         int par = 0;
-    #ifdef DD_PHASE_TIMING
-        long long ph[4] = {0, 0, 0, 0};
-        long long tp = clock64();
-    #define DD_PH(i) do { __syncthreads(); long long tn = clock64(); ph[i] += tn - tp; tp = tn; } while (0)
-    #else
-    #define DD_PH(i) do {} while (0)
-    #endif
+        stag_k = 0;
         for (int k = 1; k <= b.max_iters; ++k) {
             cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
-            DD_PH(0);
             if (k >= 2) {
                 double part = 0.0;
                 for (int x = tid; x < nx; x += DD_NT) {
@@ -1090,41 +1025,12 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
                 if (!have_first) { first_gap = gap; have_first = true; }
                 if (gap / lam <= thr) { converged = true; break; }
             }
-            DD_PH(1);
             // alpha = -ratio L is fused into the Y sweep's row preparation
             cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
-            DD_PH(2);
             int ndeg = 0;
             bool moved = false;
             for (int y = tid; y < ny; y += DD_NT) {
                 int dg = 0;
-#if defined(DD_NEWTON_STATS)
-                moved = true;   // diagnostic build: no stagnation shortcut
-                w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, b.newton_tol,
-                                        b.newton_max_iters, &dg, &newton_steps, nst);
-#elif defined(DD_NEWTON_PAIR)
-                moved = true;   // variant build: no stagnation shortcut
-                const int y2 = y + DD_NT;
-                if (y2 < ny) {
-                    NewtonState sa, sb;
-                    double oa = 0.0, ob = 0.0;
-                    newton_init(sa, w.ty[y], w.m[y], has_m, w.beta[y], eps, lam, &oa, &dg);
-                    newton_init(sb, w.ty[y2], w.m[y2], has_m, w.beta[y2], eps, lam, &ob, &dg);
-                    const double ie = 1.0 / eps, il = 1.0 / lam;
-                    while (!(sa.done && sb.done)) {
-                        newton_step(sa, ie, il, b.newton_tol, b.newton_max_iters, &oa,
-                                    &newton_steps);
-                        newton_step(sb, ie, il, b.newton_tol, b.newton_max_iters, &ob,
-                                    &newton_steps);
-                    }
-                    w.beta[y] = oa;
-                    w.beta[y2] = ob;
-                    y += DD_NT;   // the loop's own increment then skips past y2
-                } else {
-                    w.beta[y] = newton_node(w.ty[y], w.m[y], has_m, w.beta[y], eps, lam,
-                                            b.newton_tol, b.newton_max_iters, &dg, &newton_steps);
-                }
-#else
                 {
                     const double ob = w.beta[y];
                     const double lmv = y == tid ? lmc0 : (y == tid + DD_NT ? lmc1 : __builtin_nan(""));
@@ -1134,7 +1040,6 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
                     moved |= (nb != ob);
                     w.beta[y] = nb;
                 }
-#endif
                 ndeg += dg;
             }
             const int cur = k & 1;
@@ -1146,44 +1051,16 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
             const bool any_moved = moved_sh[cur] != 0;
             if (tid == 0) { ndeg_sh[cur ^ 1] = 0; moved_sh[cur ^ 1] = 0; }
             iters = k;
-            DD_PH(3);
             if (!any_moved && k >= 2 && b.skip_stagnant) {
-                // beta reproduced itself bitwise: every later iteration recomputes the
-                // same L, alpha, z and beta and fails the same gap test, so the loop
-                // would end at the cap in exactly this state (cells.py:320-348)
+                // beta reproduced itself bitwise: iteration k+1 recomputes the same L
+                // and tests it against the new alpha_k (the post-loop gap below); if
+                // that fails, every later iteration repeats exactly the same state and
+                // test, so the reference loop ends at the cap (cells.py:320-348)
+                stag_k = k;
                 iters = b.max_iters;
                 break;
             }
         }
-    #ifdef DD_NEWTON_STATS
-        {
-            const double a0 = block_sum((double)nst[0], red);
-            const double a1 = block_sum((double)nst[1], red);
-            const double a3 = block_sum((double)nst[3], red);
-            const double a2 = block_max((double)nst[2], red);
-            if (tid == 0) {
-                b.cstat[(int64_t)c * 8 + 4] = a0;
-                b.cstat[(int64_t)c * 8 + 5] = a1;
-                b.cstat[(int64_t)c * 8 + 6] = a2;
-                b.cstat[(int64_t)c * 8 + 7] = a3;
-            }
-        }
-    #endif
-    #ifdef DD_PHASE_TIMING
-        if (tid == 0) {
-            b.cstat2[(int64_t)c * 4 + 0] = (double)fbn[3];   // underflowed Y-sweep outputs
-            b.cstat2[(int64_t)c * 4 + 1] = (double)fbn[0] * 1e6 + (double)fbn[1];
-#ifdef DD_SWEEP_TIMING
-            // sweep sub-phases in place of the loop phases
-            for (int q = 0; q < 4; ++q) b.cstat[(int64_t)c * 8 + 4 + q] = (double)subc[q];
-#else
-            b.cstat[(int64_t)c * 8 + 4] = (double)ph[0];
-            b.cstat[(int64_t)c * 8 + 5] = (double)ph[1];
-            b.cstat[(int64_t)c * 8 + 6] = (double)ph[2];
-            b.cstat[(int64_t)c * 8 + 7] = (double)ph[3];
-#endif
-        }
-    #endif
         __syncthreads();
         if (!converged) {
             // cap reached: final X sweep and gap for the last (post-Y-step) pair
@@ -1203,7 +1080,10 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
             gap = lam * block_sum(part, red);
             if (!have_first) { first_gap = gap; have_first = true; }
             converged = gap / lam <= thr;
+            // stagnant loop: the reference freezes the cell at iteration stag_k + 1
+            if (converged && stag_k) iters = stag_k;
         }
+        exec_iters = stag_k ? stag_k : iters;
 
         t_loop_d = (double)(clock64() - t_loop0);
         nsteps = block_sum((double)newton_steps, red);
@@ -1632,19 +1512,16 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         cs[1] = first_gap;
         cs[2] = (double)iters;
         cs[3] = converged ? 1.0 : 0.0;
-#if !defined(DD_PHASE_TIMING) && !defined(DD_NEWTON_STATS)
         cs[4] = (double)n_clamped;
         cs[5] = (double)newton_clamped;
         cs[6] = (double)fallbacks;
         cs[7] = target_miss;
-#endif
-        double* c2 = b.cstat2 + (int64_t)c * 4;
-#if !defined(DD_PHASE_TIMING)
+        double* c2 = b.cstat2 + (int64_t)c * 8;
         c2[0] = (double)drift;    // (phase-timing builds keep the sweep-fallback stats here)
         c2[1] = trunc_total;
-#endif
         c2[2] = t_loop_d;         // SM cycles spent in the Sinkhorn loop
         c2[3] = nsteps;           // Newton evaluations over all nodes and iterations
+        if (!epi) c2[4] = (double)exec_iters;   // Sinkhorn iterations actually executed
     }
 }
 
@@ -1780,7 +1657,7 @@ __global__ void __launch_bounds__(DD_NT) cell_commit_kernel(dd_geom g, dd_state 
     __syncthreads();
     double added = 0.0;
     if (th >= 1.0) {
-        added = b.cstat2[(int64_t)c * 4 + 1];
+        added = b.cstat2[(int64_t)c * 8 + 1];
         for (int k = 0; k < nmem; ++k) {
             const int i = mem[k];
             const int mslot = d[10] + k;
@@ -1847,7 +1724,7 @@ __global__ void __launch_bounds__(DD_NT) cell_commit_kernel(dd_geom g, dd_state 
                 s.x_marg[(int64_t)i * bs + t] = (1.0 - th) * s.x_marg[(int64_t)i * bs + t] + th * xn[t];
             __syncthreads();
         }
-        added = th * b.cstat2[(int64_t)c * 4 + 1] + removed_all;
+        added = th * b.cstat2[(int64_t)c * 8 + 1] + removed_all;
     }
     __syncthreads();
     // dual store
@@ -2169,12 +2046,5 @@ extern "C" int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy,
     return dd_set_error(cudaGetLastError());
 }
 
-#ifdef DD_COUNT_FALLBACK
-extern "C" int dd_debug_fallbacks(unsigned long long* out) {
-    cudaMemcpyFromSymbol(out, dd::g_fallbacks, sizeof(unsigned long long));
-    cudaMemcpyFromSymbol(out + 1, dd::g_outputs, sizeof(unsigned long long));
-    return 0;
-}
-#endif
 
 extern "C" int dd_cell_min_blocks(void) { return DD_CELL_MIN_BLOCKS; }

@@ -228,7 +228,6 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         // further pass of the reference loop recomputes the same g and step and
         // leaves b unchanged until max_iters, so stopping here returns the same b
         if (nb == b) break;
-#if !defined(DD_NEWTON_CONFIRM)
         // Converged step.  Newton's next correction is at most
         //   |g''| step^2 / (2 g') <= (1 - sig) step^2 / (2 eps)   (g'' = sig(1-sig)/eps^2),
         // so once step^2/eps <= 2^-52 |nb| it is below one ulp of nb and the confirming
@@ -239,7 +238,6 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
             b = nb;
             break;
         }
-#endif
         b = nb;
     }
     if (nstat) {

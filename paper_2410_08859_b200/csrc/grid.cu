@@ -661,170 +661,6 @@ __global__ void __launch_bounds__(DD_NT) refine_kernel(dd_geom g, dd_state s, Re
     }
 }
 
-// Dual-shaped refinement of fine basic cell j (multiscale refine_plan, B200
-// variant): the child's Y-marginal takes the shape of the diagonal-scaling
-// plan of the prolonged duals restricted to the child block,
-//   w_j(y) = nu(y) e^{beta(y)/eps} sum_{x in X_j} mu(x) e^{alpha(x)/eps} K(x,y),
-// evaluated factorised over the parent's doubled box, and the mass the
-// product refinement would give it (f_j |nu_i|); then truncation at `trunc`
-// and product-plan fragments.  tmp holds one candidate box per cell.
-__global__ void __launch_bounds__(DD_NT) refine_dual_kernel(dd_geom g, dd_state s, RefineArgs a,
-                                                           const double* alpha,
-                                                           const double* beta, double* tmp,
-                                                           int64_t tcap) {
-    __shared__ double red[DD_NW + 1];
-    __shared__ int redi[DD_NW + 1];
-    __shared__ double wx[64];
-    __shared__ double xc0s[8], xc1s[64];
-    extern __shared__ double m1[];   // [block0][fe1]
-    const int j = blockIdx.x;
-    const int i = a.parent[j];
-    const int32_t* cb = a.cbox + (int64_t)i * 4;
-    const double* cv = a.cval + (int64_t)i * a.ccap;
-    const int fo0 = 2 * cb[0], fe0 = 2 * cb[1], fo1 = 2 * cb[2], fe1 = 2 * cb[3];
-    const int n = fe0 * fe1;
-    const double eps = g.eps;
-    const int32_t* bx = s.basic_xbox + (int64_t)j * 4;
-    const int e0 = bx[1], e1 = bx[3];
-    const int bs = e0 * e1;
-    // parent mass -> child target mass
-    double pm = 0.0;
-    for (int t = threadIdx.x; t < cb[1] * cb[3]; t += DD_NT) pm += cv[t];
-    pm = block_sum(pm, red);
-    const double target = pm * (s.basic_mass[j] / a.cmass[i]);
-    // child X weights
-    double am = kNegInf;
-    for (int t = threadIdx.x; t < bs; t += DD_NT) {
-        const int a0 = t / e1, a1 = t - a0 * e1;
-        const int64_t id = (int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1);
-        const double v = s.mu[id] > 0 ? alpha[id] / eps + s.log_mu[id] : kNegInf;
-        wx[t] = v;
-        am = fmax(am, v);
-    }
-    const double A = block_max(am, red);
-    for (int t = threadIdx.x; t < bs; t += DD_NT) wx[t] = isfinite(wx[t]) ? exp(wx[t] - A) : 0.0;
-    for (int t = threadIdx.x; t < e0; t += DD_NT) xc0s[t] = g.x_org0 + g.x_dx * (double)(bx[0] + t);
-    for (int t = threadIdx.x; t < e1; t += DD_NT) xc1s[t] = g.x_org1 + g.x_dx * (double)(bx[2] + t);
-    __syncthreads();
-    // stage 1: m1[a0][q] = sum_a1 wx[a0,a1] exp(-(x1 - y1)^2/eps)
-    for (int t = threadIdx.x; t < e0 * fe1; t += DD_NT) {
-        const int a0 = t / fe1, q = t - a0 * fe1;
-        const double yc = g.y_org1 + g.y_dx * (double)(fo1 + q);
-        double sacc = 0.0;
-        for (int a1 = 0; a1 < e1; ++a1) {
-            const double d = xc1s[a1] - yc;
-            sacc += wx[a0 * e1 + a1] * exp(-(d * d) / eps);
-        }
-        m1[t] = sacc;
-    }
-    __syncthreads();
-    // K0 table [a0][r] after m1 in shared memory
-    double* k0 = m1 + e0 * fe1;
-    for (int t = threadIdx.x; t < e0 * fe0; t += DD_NT) {
-        const int a0 = t / fe0, r = t - a0 * fe0;
-        const double d = xc0s[a0] - (g.y_org0 + g.y_dx * (double)(fo0 + r));
-        k0[t] = exp(-(d * d) / eps);
-    }
-    __syncthreads();
-    double* w = tmp + (int64_t)j * tcap;
-    double tot = 0.0;
-    for (int t = threadIdx.x; t < n; t += DD_NT) {
-        const int r = t / fe1, q = t - r * fe1;
-        const int yf0 = fo0 + r, yf1 = fo1 + q;
-        double sacc = 0.0;
-        for (int a0 = 0; a0 < e0; ++a0) sacc += k0[a0 * fe0 + r] * m1[a0 * fe1 + q];
-        const int64_t id = (int64_t)yf0 * g.ny1 + yf1;
-        const double v = sacc > 0 ? exp(A + beta[id] / eps + s.log_nu[id] + log(sacc)) : 0.0;
-        w[t] = v;
-        tot += v;
-    }
-    tot = block_sum(tot, red);
-    const double scale = tot > 0 ? target / tot : 0.0;
-    int rmin = 0x7fffffff, rmax = -1, cmin = 0x7fffffff, cmax = -1;
-    double rem = 0.0;
-    for (int t = threadIdx.x; t < n; t += DD_NT) {
-        const double v = w[t] * scale;
-        w[t] = v;
-        if (v >= a.trunc) {
-            const int r = t / fe1, q = t - r * fe1;
-            rmin = min(rmin, r); rmax = max(rmax, r); cmin = min(cmin, q); cmax = max(cmax, q);
-        } else {
-            rem += v;
-        }
-    }
-    rmin = block_min_i(rmin, redi);
-    rmax = block_max_i(rmax, redi);
-    cmin = block_min_i(cmin, redi);
-    cmax = block_max_i(cmax, redi);
-    rem = block_sum(rem, red);
-    int ne0 = 0, ne1 = 0;
-    if (rmax >= 0) { ne0 = rmax - rmin + 1; ne1 = cmax - cmin + 1; }
-    double* out = s.yval + (int64_t)j * s.cap;
-    double mnu = 0.0, sy1a = 0.0, sy2a = 0.0, sy1b = 0.0, sy2b = 0.0, ent = 0.0;
-    for (int t = threadIdx.x; t < ne0 * ne1; t += DD_NT) {
-        const int a0 = t / ne1, a1 = t - a0 * ne1;
-        const int r = rmin + a0, q = cmin + a1;
-        double v = w[(int64_t)r * fe1 + q];
-        v = v >= a.trunc ? v : 0.0;
-        out[t] = v;
-        const int yf0 = fo0 + r, yf1 = fo1 + q;
-        const double nu = s.nu[(int64_t)yf0 * g.ny1 + yf1];
-        mnu += v;
-        const double ya = g.y_org0 + g.y_dx * (double)yf0;
-        const double yb = g.y_org1 + g.y_dx * (double)yf1;
-        sy1a += v * ya;
-        sy2a += v * (ya * ya);
-        sy1b += v * yb;
-        sy2b += v * (yb * yb);
-        ent += xlogy(v, v / nu);
-    }
-    mnu = block_sum(mnu, red);
-    sy1a = block_sum(sy1a, red);
-    sy2a = block_sum(sy2a, red);
-    sy1b = block_sum(sy1b, red);
-    sy2b = block_sum(sy2b, red);
-    ent = block_sum(ent, red);
-    double mmu = 0.0, sx1a = 0.0, sx2a = 0.0, sx1b = 0.0, sx2b = 0.0;
-    for (int t = threadIdx.x; t < bs; t += DD_NT) {
-        const int a0 = t / e1, a1 = t - a0 * e1;
-        const int r = bx[0] + a0, q = bx[2] + a1;
-        const double mu = s.mu[(int64_t)r * g.nx1 + q];
-        if (mu > 0) {
-            const double xa = g.x_org0 + g.x_dx * (double)r;
-            const double xb = g.x_org1 + g.x_dx * (double)q;
-            mmu += mu;
-            sx1a += mu * xa;
-            sx2a += mu * (xa * xa);
-            sx1b += mu * xb;
-            sx2b += mu * (xb * xb);
-        }
-    }
-    mmu = block_sum(mmu, red);
-    sx1a = block_sum(sx1a, red);
-    sx2a = block_sum(sx2a, red);
-    sx1b = block_sum(sx1b, red);
-    sx2b = block_sum(sx2b, red);
-    for (int t = threadIdx.x; t < bs; t += DD_NT) {
-        const int a0 = t / e1, a1 = t - a0 * e1;
-        const double mu = s.mu[(int64_t)(bx[0] + a0) * g.nx1 + (bx[2] + a1)];
-        s.x_marg[(int64_t)j * bs + t] = mu > 0 ? mu * (mnu / mmu) : 0.0;
-    }
-    if (threadIdx.x == 0) {
-        int32_t* ob = s.ybox + (int64_t)j * 4;
-        if (rmax >= 0) { ob[0] = fo0 + rmin; ob[1] = ne0; ob[2] = fo1 + cmin; ob[3] = ne1; }
-        else { ob[0] = 0; ob[1] = 0; ob[2] = 0; ob[3] = 0; }
-        a.trunc_out[j] = rem;
-        if (mnu == 0.0) {
-            s.transport[j] = 0.0;
-            s.kl[j] = mmu * g.nu_total;
-        } else {
-            double tr = sx2a * mnu - 2.0 * sx1a * sy1a + mmu * sy2a;
-            tr += sx2b * mnu - 2.0 * sx1b * sy1b + mmu * sy2b;
-            s.transport[j] = tr / mmu;
-            s.kl[j] = ent - mnu * log(mmu) - mnu + mmu * g.nu_total;
-        }
-    }
-}
 
 // Prolongation of a coarse cell-centred grid field to the fine grid (x2 per
 // axis): bilinear in the coarse node positions, constant beyond the outer
@@ -1014,21 +850,3 @@ extern "C" int dd_prolong(int nf0, int nf1, int nc0, int nc1, const double* coar
     return dd_set_error(cudaGetLastError());
 }
 
-extern "C" int dd_refine_dual(const dd_geom* g, const dd_state* s, const int32_t* parent,
-                              const int32_t* cbox, const double* cval, int64_t ccap,
-                              const double* cmass, const double* alpha, const double* beta,
-                              double trunc, double* trunc_out, double* tmp, int64_t tcap,
-                              int max_fe1, void* stream) {
-    if (s->n_basic <= 0) return 0;
-    if (s->block0 > 8 || s->block1 > 64 || s->block0 * s->block1 > 64) return -1000;
-    dd::RefineArgs a{parent, cbox, cval, ccap, cmass, nullptr, 0, trunc, trunc_out};
-    const size_t smem = (size_t)s->block0 * 2 * max_fe1 * sizeof(double);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(dd::refine_dual_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return dd_set_error(e);
-    }
-    dd::refine_dual_kernel<<<s->n_basic, DD_NT, smem, (cudaStream_t)stream>>>(*g, *s, a, alpha,
-                                                                             beta, tmp, tcap);
-    return dd_set_error(cudaGetLastError());
-}

@@ -15,8 +15,8 @@ Semantics (paper Def. 2.4 and §4.3.1):
   cell holding every basic cell (with a warning);
 * each partition splits into 2^d batches by composite-lattice parity.
 
-``device_tables`` exports the integer tables the CUDA library consumes, with
-1D problems embedded as 2D grids of shape (1, n).
+The engine builds the integer tables the CUDA library consumes from these
+objects (1D problems embedded as 2D grids of shape (1, n)).
 """
 
 from __future__ import annotations
@@ -184,32 +184,3 @@ def as2d_box(box) -> tuple:
     return tuple(box) if len(box) == 2 else ((0, 1), tuple(box[0]))
 
 
-def device_tables(dec: Decomposition) -> dict:
-    """Flat int32/float64 tables for the CUDA library (2D embedding).
-
-    basic_box[i]      = (off0, ext0, off1, ext1) of basic cell i
-    basic_mass[i]     = mu mass of cell i (reference float(block.sum()))
-    for each composite partition p:
-      comp_xbox[p][j] = (off0, ext0, off1, ext1) of the X window
-      comp_mem[p][j]  = real member ids padded with -1 (MAX_MEMBERS wide)
-      comp_nmem[p][j]
-      batches[p]      = list of int32 arrays of composite ids
-    """
-    basic = dec.basic
-    bb = np.array([[c for ax in as2d_box(b) for c in ax] for b in basic.cell_boxes], dtype=np.int32)
-    out = {"basic_box": bb, "basic_mass": basic.masses.astype(np.float64), "parts": []}
-    for part in dec.composites:
-        xb = np.array([[c for ax in as2d_box(b) for c in ax] for b in part.boxes], dtype=np.int32)
-        nm = np.array([len(part.real_members(j)) for j in range(part.n_cells)], dtype=np.int32)
-        if nm.max() > MAX_MEMBERS:
-            raise ValueError(f"composite cell with {nm.max()} members exceeds {MAX_MEMBERS}")
-        width = int(max(4, nm.max()))
-        mem = np.full((part.n_cells, width), -1, dtype=np.int32)
-        for j in range(part.n_cells):
-            r = part.real_members(j)
-            mem[j, :len(r)] = r
-        out["parts"].append({
-            "label": part.label, "xbox": xb, "members": mem, "nmem": nm,
-            "batches": [np.asarray(b, dtype=np.int32) for b in part.batches],
-        })
-    return out

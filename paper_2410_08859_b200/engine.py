@@ -753,7 +753,7 @@ class _Batch:
         self.mbox = B.get("mbox", tot_mem * 4, i32)
         self.mstat = B.get("mstat", tot_mem * 4, f64)
         self.cstat = B.get("cstat", n * 8, f64)
-        self.cstat2 = B.get("cstat2", n * 4, f64)
+        self.cstat2 = B.get("cstat2", n * 8, f64)
         self.dy = None
         self.tot = dict(y=tot_y, m=tot_m, mem=tot_mem)
         self.yoff = yoff
@@ -783,7 +783,7 @@ class _Batch:
             outs = [self.alpha[:n * nx], self.beta[:t["y"]], self.mdens[:t["y"]],
                     self.lnuw[:t["y"]], self.marena[:t["m"]], self.xarena[:t["mem"] * st.bs],
                     self.mbox[:t["mem"] * 4], self.mstat[:t["mem"] * 4], self.cstat[:n * 8],
-                    self.cstat2[:n * 4], self.lout[:n * nx]]
+                    self.cstat2[:n * 8], self.lout[:n * nx]]
             for o in outs:
                 o.zero_()
         _lib.check(_lib.lib().dd_cell_solve2(st.dp.geom, st.state_struct(self.store), self.batch,
@@ -797,7 +797,7 @@ class _Batch:
 
     def stats(self):
         c1 = self.cstat[:self.n * 8].view(self.n, 8).cpu().numpy()
-        c2 = self.cstat2[:self.n * 4].view(self.n, 4).cpu().numpy()
+        c2 = self.cstat2[:self.n * 8].view(self.n, 8).cpu().numpy()
         return c1, c2
 
     def commit(self, theta: np.ndarray, alpha_grid=None, yrun=None) -> np.ndarray:
@@ -1075,7 +1075,9 @@ def _absorb(stats: IterationStats, batch: _Batch) -> None:
     c1, c2 = batch.stats()
     fl = cell_lse_flops(batch.pt.nw0, batch.pt.nw1, batch.ybox[:, 1].astype(np.float64),
                         batch.ybox[:, 3].astype(np.float64))
-    stats.cell_flops += float((c1[:, 2] * fl).sum())
+    # roofline work counts executed iterations only (a stagnant cell's loop ends
+    # early with the reference-equivalent count reported in c1)
+    stats.cell_flops += float((c2[:, 4] * fl).sum())
     stats.entry_gap += float(c1[:, 1].sum())
     stats.balance_fallbacks += int(c1[:, 6].sum())
     stats.newton_clamped = max(stats.newton_clamped, int(c1[:, 5].max(initial=0)))

@@ -171,19 +171,14 @@ def prolong_duals(duals, coarse_geom, fine_geom):
 
 
 def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
-                coarse_duals=None, trunc_threshold: float = 1e-15, dp=None,
-                shape: str = "split") -> PlanState:
+                coarse_duals=None, trunc_threshold: float = 1e-15, dp=None) -> PlanState:
     """Fine-level state from a solved coarse state (SPEC multiscale.refine_plan).
 
     Each child basic cell keeps its share f_j = mu(X_j)/mu(X_i) of the parent's
-    Y-marginal mass.  ``shape="split"`` (default) splits the parent marginal
-    over fine Y nodes by fine nu mass (``dd_refine``), which keeps the summed
-    children consistent with the coarse plan's Y-marginal.  ``shape="dual"``
-    shapes each child by the plan of the prolonged duals restricted to its
-    block (``dd_refine_dual``): tighter boxes, but the children no longer sum
-    to the coarse marginal and the first fine sweeps pay for it (measured: many
-    more cell iterations), so it is opt-in.  Both truncate at the threshold and
-    install product-plan fragments; duals are prolonged bilinearly.
+    Y-marginal mass, split over fine Y nodes by fine nu mass (``dd_refine``), so
+    the summed children stay consistent with the coarse plan's Y-marginal;
+    children are truncated at the threshold and carry product-plan fragments;
+    duals are prolonged bilinearly.
     """
     import torch
 
@@ -216,23 +211,11 @@ def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
                                 _lib.stream_handle()))
         _lib.check(L.dd_prolong(g.ny0, g.ny1, cg.ny0, cg.ny1, cbeta.data_ptr(), fbeta.data_ptr(),
                                 _lib.stream_handle()))
-    if shape == "dual" and fa is not None and st.block[0] <= 8 and st.bs <= 64:
-        tcap = 4 * cmax
-        tmp = torch.empty(fb.n_cells * tcap, dtype=torch.float64, device=dp.device)
-        max_fe = 2 * int(max(boxes[:, 1].max(initial=1), boxes[:, 3].max(initial=1)))
-        _lib.check(L.dd_refine_dual(dp.geom, st.state_struct(), parent_d.data_ptr(),
-                                    coarse.ybox.data_ptr(), coarse.yval.data_ptr(), coarse.cap,
-                                    coarse.basic_mass.data_ptr(), fa.data_ptr(), fbeta.data_ptr(),
-                                    float(trunc_threshold), trunc_out.data_ptr(), tmp.data_ptr(),
-                                    tcap, max_fe, _lib.stream_handle()))
-        torch.cuda.synchronize()
-        del tmp
-    else:
-        _lib.check(L.dd_refine(dp.geom, st.state_struct(), parent_d.data_ptr(),
-                               coarse.ybox.data_ptr(), coarse.yval.data_ptr(), coarse.cap,
-                               coarse.basic_mass.data_ptr(), coarse.dp.nu.data_ptr(),
-                               coarse.dp.geom.ny1, float(trunc_threshold), trunc_out.data_ptr(),
-                               _lib.stream_handle()))
+    _lib.check(L.dd_refine(dp.geom, st.state_struct(), parent_d.data_ptr(),
+                           coarse.ybox.data_ptr(), coarse.yval.data_ptr(), coarse.cap,
+                           coarse.basic_mass.data_ptr(), coarse.dp.nu.data_ptr(),
+                           coarse.dp.geom.ny1, float(trunc_threshold), trunc_out.data_ptr(),
+                           _lib.stream_handle()))
     st.sync_boxes()
     st.truncated_mass = coarse.truncated_mass + float(trunc_out.sum().item())
     if fa is not None:

@@ -3,9 +3,11 @@
 The reference benchmarks on Gaussian-mixture images (paper §4.3.1, "Gaussian
 mixtures supported on X = [0,1]^2 with random variances, means, and
 magnitudes"); no image files travel, so every config is regenerated from a
-seed.  The generator is host-side setup, shared verbatim by the CUDA path,
-the CPU oracle and the golden-fixture script, so both arms of every
-comparison see bit-identical inputs.
+seed.  The generator is host-side setup used by bench.py (both arms), the
+BASELINE-config parity tests and the configs[0] golden fixture
+(scripts/make_golden.py ``pr1_64``), so those comparisons see bit-identical
+inputs.  The small hand-made golden cases (toy1d_*, mix16_*, mix32_*) use
+make_golden.py's own mixture helper instead.
 
 Density recipe (documented in DESIGN.md §Data):
     dens = sum_k w_k exp(-|x - c_k|^2 / (2 sigma_k^2))      (isotropic)
