@@ -109,8 +109,11 @@ typedef struct dd_batch {
     double trunc;
     double* lnuw;              /* y arena: log nu on each cell window (kernel scratch) */
     double* lout;              /* [n_cells*nxw0*nxw1] final X sweep of cluster-solved cells */
-    int32_t skip_stagnant;     /* 1: end a cell's loop at the cap as soon as an iteration
-                                  reproduces beta bitwise (exactly equivalent) */
+    int32_t skip_stagnant;     /* 1: end a cell's loop early once an iteration reproduces
+                                  beta bitwise (same results and reference iteration
+                                  count; executed iterations in cstat2) */
+    const int32_t* order;      /* nullable [n_cells]: CTA b of the solve kernel takes cell
+                                  order[b] (longest-expected-first scheduling) */
 } dd_batch;
 
 const char* dd_last_error(void);

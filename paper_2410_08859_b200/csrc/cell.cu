@@ -857,7 +857,9 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     __shared__ int redi[DD_NW + 1];
     __shared__ int sh_flag[4];
 
-    const int c = blockIdx.x;
+    // CTAs are dispatched in blockIdx order: the host orders cells by expected
+    // cost (longest first) so the capped tail does not start last
+    const int c = b.order ? b.order[blockIdx.x] : blockIdx.x;
     const int32_t* d = b.desc + (int64_t)c * 12;
     const int64_t* off = b.offs + (int64_t)c * 4;
     const int nw0 = b.nxw0, nw1 = b.nxw1;

@@ -306,6 +306,7 @@ class PlanState:
         self.stores: dict = {}
         self.truncated_mass = 0.0
         self.global_duals = None
+        self.iter_hist: dict = {}   # partition label -> executed iterations of the last solve
         self.buf = _Buffers(dev)
         self.partial = torch.empty(8192 + 4 * nb, dtype=torch.float64, device=dev)
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -445,6 +446,7 @@ class PlanState:
         c.x_marg_d, c.transport_d, c.kl_d = (self.x_marg_d.clone(), self.transport_d.clone(),
                                              self.kl_d.clone())
         c.stores = {k: v.clone() for k, v in self.stores.items()}
+        c.iter_hist = {k: v.copy() for k, v in self.iter_hist.items()}
         c.buf = _Buffers(self.dp.device)
         c.partial = self.partial.clone()
         c.sums = self.sums.clone()
@@ -700,9 +702,17 @@ class _Batch:
             owned = self.shard.owners(cost) == self.shard.rank
             clu &= owned
         self.owned = owned
+        # expected cost of each cell: window size x the executed iterations of its
+        # previous solve (the iteration count is strongly persistent across sweeps);
+        # CTAs and cluster launches take cells longest-first
+        hist = st.iter_hist.get(pt.label)
+        prev = hist[ids] if hist is not None else np.zeros(n)
+        cost = ny.astype(np.float64) * (prev + 1.0)
+        self.order_h = np.argsort(-cost, kind="stable").astype(np.int32)
         groups = []
         for C in sorted(set(csize[clu].tolist())):
             sel = np.flatnonzero(clu & (csize == C))
+            sel = sel[np.argsort(-cost[sel], kind="stable")]
             groups.append((int(C), sel, int(csmem[sel].max())))
         self.clu_groups = groups
         self.n_clu = int(clu.sum())
@@ -729,6 +739,7 @@ class _Batch:
         B = st.buf
         f64, i32, i64 = torch.float64, torch.int32, torch.int64
         self.desc_d = torch.from_numpy(desc.ravel()).to(dev)
+        self.order_d = torch.from_numpy(self.order_h).to(dev) if n else B.get("order", 1, i32)
         self.offs_d = torch.from_numpy(offs.ravel()).to(dev)
         self.mem_d = torch.from_numpy(mflat).to(dev) if tot_mem else B.get("mem", 1, i32)
         self.alpha = B.get("alpha", n * pt.nw0 * pt.nw1, f64)
@@ -768,7 +779,8 @@ class _Batch:
             smem_mode=1 if smem_mode else 0, smem_bytes=smem_bytes if smem_mode else 0,
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
-            lout=self.lout.data_ptr(), skip_stagnant=1 if mode.skip_stagnant else 0)
+            lout=self.lout.data_ptr(), skip_stagnant=1 if mode.skip_stagnant else 0,
+            order=self.order_d.data_ptr() if n else None)
         self.cfg = cfg
 
     def solve(self):
@@ -1073,6 +1085,8 @@ def cell_lse_flops(nw0: int, nw1: int, ny0, ny1):
 
 def _absorb(stats: IterationStats, batch: _Batch) -> None:
     c1, c2 = batch.stats()
+    hist = batch.st.iter_hist.setdefault(batch.pt.label, np.zeros(batch.pt.ncomp))
+    hist[batch.ids] = c2[:, 4]
     fl = cell_lse_flops(batch.pt.nw0, batch.pt.nw1, batch.ybox[:, 1].astype(np.float64),
                         batch.ybox[:, 3].astype(np.float64))
     # roofline work counts executed iterations only (a stagnant cell's loop ends
