@@ -79,13 +79,16 @@ class ExecMode:
     ``force_cluster=C`` runs every cell's Sinkhorn loop on a C-CTA thread-block
     cluster; ``force_global_ws`` puts every cell's workspace in the global arena
     (single-CTA kernel); ``no_cluster`` keeps large cells on the single-CTA
-    global-workspace path.  Defaults come from DD_FORCE_CLUSTER /
+    global-workspace path; ``smem_budget`` lowers the per-CTA shared-memory budget
+    the size rule uses, so mid-size windows take the cluster path by the same
+    rule large windows do.  Defaults come from DD_FORCE_CLUSTER /
     DD_FORCE_GLOBAL_WS / DD_NO_CLUSTER."""
 
     force_cluster: int = 0
     force_global_ws: bool = False
     no_cluster: bool = False
     skip_stagnant: bool = True
+    smem_budget: int = 0        # bytes per CTA for the size rule (0: the hardware budget)
 
 
 def _env_mode() -> ExecMode:
@@ -669,7 +672,7 @@ class _Batch:
         xoff = np.concatenate([[0], np.cumsum(nmem * st.bs)[:-1]]).astype(np.int64)
         ws = _ws_total(pt.nw0, pt.nw1, ny0, ny1).astype(np.int64)
         mode = _MODE[0]
-        budget = _smem_budget()
+        budget = mode.smem_budget or _smem_budget()
         fits = ws * 8 <= (0 if mode.force_global_ws else budget)
         if mode.force_cluster:
             fits = np.zeros_like(fits)

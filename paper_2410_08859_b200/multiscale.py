@@ -10,6 +10,8 @@ grids refined x2 per level from ``n_coarsest`` up to the problem grid):
 * ``eps_schedule`` halves eps from start to final and runs each value on the
   coarsest level whose spacing satisfies h^2 <= eps (the last value always
   on the finest level);
+* (spec) the coarsest global Sinkhorn starts from the mass-balanced constant
+  duals (``sinkhorn.mass_balanced_start``);
 * the coarsest level starts from ``warm_start_plan`` (global device Sinkhorn
   plus plan cut); every later level starts from ``refine_plan`` — each coarse
   basic-cell Y-marginal mass split over its 2^d child cells by fine mu mass,
@@ -49,7 +51,7 @@ from .engine import (EngineConfig, PlanState, StitchedGapEvaluator, StrategyConf
                      _tables, domdec_solve, warm_start_plan)
 from .grids import Grid, GridMeasure, TransportProblem
 from .report import SolveReport
-from .sinkhorn import DeviceProblem, SolverConfig, sinkhorn_solve
+from .sinkhorn import DeviceProblem, SolverConfig, mass_balanced_start, sinkhorn_solve
 
 __all__ = ["Level", "build_pyramid", "stage_pyramid", "eps_schedule", "spec_eps_schedule",
            "switch_layer", "layer_index", "refine_plan", "prolong_duals", "MultiscaleReport",
@@ -303,9 +305,11 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
         if protocol == "spec" and layer_index(max(lv.grid.dims)) < lsw and li < len(levels) - 1:
             # coarse layer: global unbalanced Sinkhorn at delta/4
             dp = lv.dp if lv.dp is not None else DeviceProblem(prob)
-            a0 = b0 = None
             if duals is not None:
                 a0, b0 = prolong_duals(duals, duals_geom, dp.geom)
+            else:
+                dp.geom.eps = float(eps_list[0])
+                a0, b0 = mass_balanced_start(dp)
             for eps in eps_list:
                 dp.problem = _with_eps(lv, problem.div, eps)
                 dp.geom.eps = float(eps)

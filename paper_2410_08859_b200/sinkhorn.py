@@ -20,7 +20,8 @@ import numpy as np
 from . import _lib
 from .grids import TransportProblem
 
-__all__ = ["DeviceProblem", "GridSweeper", "SolverConfig", "GlobalResult", "sinkhorn_solve"]
+__all__ = ["DeviceProblem", "GridSweeper", "SolverConfig", "GlobalResult", "sinkhorn_solve",
+           "mass_balanced_start"]
 
 
 def _as2d(arr) -> np.ndarray:
@@ -142,6 +143,32 @@ def newton_zero_background(dp: DeviceProblem, z, out=None):
     _lib.check(_lib.lib().dd_newton_global(z.numel(), z.data_ptr(), ratio, g.lam, out.data_ptr(),
                                            None, _lib.stream_handle()))
     return out
+
+
+def mass_balanced_start(dp: DeviceProblem, sweeper: "GridSweeper | None" = None):
+    """Constant dual pair (a, b) whose plan e^{(a+b-c)/eps} mu x nu balances the
+    total masses of both unbalanced proxdiv conditions, |P_X pi| = e^{-a/lam}|mu|
+    and |P_Y pi| = e^{-b/lam}|nu| (closed form; one X sweep of log nu).
+
+    Used by the multiscale driver as the initial guess of its coarsest global
+    Sinkhorn solve: the total-mass mode of unbalanced Sinkhorn contracts only by
+    ~(1 - 2 eps/lam) per iteration, so starting it balanced removes most of the
+    iterations (10158 -> 1675 at configs[2]'s 64^2 layer); the solve itself is
+    unchanged and still runs to its tolerance.
+    """
+    import torch
+
+    g = dp.geom
+    eps, lam = g.eps, g.lam
+    sw = sweeper or GridSweeper(dp)
+    L0 = sw.lse_x(dp.log_nu)                       # log sum_y e^{-c/eps} nu(y)
+    lm = torch.where(dp.mu > 0, dp.log_mu + L0, torch.full_like(L0, -math.inf))
+    log_m0 = float(torch.logsumexp(lm, 0).item())
+    rho = math.log(dp.nu_total / dp.mu_total)
+    a = (math.log(dp.mu_total) - log_m0 - lam * rho / eps) / (2.0 / eps + 1.0 / lam)
+    b = a + lam * rho
+    return (torch.full((dp.nx,), a, dtype=torch.float64, device=dp.device),
+            torch.full((dp.ny,), b, dtype=torch.float64, device=dp.device))
 
 
 @dataclass(frozen=True)

@@ -5,11 +5,14 @@ The SPEC multiscale driver runs ms_1024 on the GPU up to the start of the
 device, and a sample of its composite cells is re-solved by the CPU oracle (a
 restatement of the reference cells.py) from the identical inputs: the same
 plan state, the same assembled snapshot and the same warm duals.  The sample
-covers every execution path the batch takes naturally: the largest windows
-(thread-block clusters, > 220 KB of workspace), cells that hit the iteration
-cap and cells that converge.  To keep the oracle within seconds the cell
-iteration cap is lowered to 200 on both sides (the cap is a reference
-configuration parameter, CellSolverConfig.max_iters).
+takes the largest windows, cells that hit the iteration cap and cells that
+converge.  The batch runs under every execution path: the default size rule,
+the global-memory workspace, forced 4-CTA clusters, and a 48 KB per-CTA budget
+under which the size rule itself sends the larger windows to 2..16-CTA
+thread-block clusters (at this stage every window fits one SM's 220 KB).  To
+keep the oracle within seconds the cell iteration cap is lowered to 200 on
+both sides (the cap is a reference configuration parameter,
+CellSolverConfig.max_iters).
 
 Tolerances (north_star, fp64): member marginals and duals within 1e-9
 relative, fragments within 1e-9, iteration counts and convergence flags equal.
@@ -60,7 +63,12 @@ def _capture_1024_stage():
     return captured, mu, nu, dx, org, cfg
 
 
-@pytest.mark.parametrize("mode", ["default", "global_ws"])
+MODES = {"default": {}, "global_ws": {"force_global_ws": True}, "cluster4": {"force_cluster": 4},
+         # 48 KB per CTA: the size rule sends the larger windows to 2..16-CTA clusters
+         "small_smem": {"smem_budget": 48 * 1024}}
+
+
+@pytest.mark.parametrize("mode", sorted(MODES))
 def test_1024_batch_cells_match_oracle(mode):
     import torch
     from paper_2410_08859_b200.engine import (CellSolverConfig, _Batch, _tables, set_exec_mode)
@@ -75,7 +83,7 @@ def test_1024_batch_cells_match_oracle(mode):
     ids = np.asarray(pt.batches[0])
     delta = 2e-5 * 0.25
     ccfg = CellSolverConfig(delta=delta, max_iters=CAP)
-    prev = set_exec_mode(force_global_ws=(mode == "global_ws"))
+    prev = set_exec_mode(**MODES[mode])
     try:
         snap = st.assemble_device()
         # host mirrors of the inputs, taken before the commit changes the state
@@ -95,8 +103,10 @@ def test_1024_batch_cells_match_oracle(mode):
         torch.cuda.synchronize()
     finally:
         set_exec_mode(prev)
-    if mode == "default":
+    if mode in ("small_smem", "cluster4"):
         assert n_clu > 0, "no cell of the 1024^2 batch took the cluster path"
+    if mode == "small_smem":
+        assert len(bt.clu_groups) >= 2, "expected several natural cluster sizes"
     iters = c1[:, 2].astype(int)
     ny = bt.ny
     # sample: the two largest windows, two capped median-size cells, two converged cells
