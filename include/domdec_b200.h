@@ -121,7 +121,8 @@ int dd_device_count(void);
 int dd_abi_version(void);
 
 /* out = separable log-sum-exp sweep (to_x = 1: Y grid -> X grid). work holds
- * max(ny0*nx1, nx0*ny1) doubles. */
+ * max(ny0*nx1, nx0*ny1) + max(nx0*ny0, nx1*ny1) doubles (intermediate + the
+ * per-stage axis table). */
 int dd_grid_lse(const dd_geom* g, const double* v, double* out, int to_x, double* work,
                 void* stream);
 

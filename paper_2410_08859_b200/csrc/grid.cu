@@ -1,6 +1,7 @@
 // Full-grid kernels: separable log-sum-exp sweeps, reductions, state setup.
 
 #include <stdio.h>
+#include <algorithm>
 #include <string.h>
 
 #include "common.cuh"
@@ -26,44 +27,66 @@ extern "C" int dd_abi_version(void) { return 1; }
 
 namespace dd {
 
-// out[r][n] (or out[n][r] when transposed) =
-//   LSE_m( in[r][m] - (p0 + pd*n - (q0 + qd*m))^2 / eps )
-// Two passes (max, then sum) with exact skipping of terms whose exponent is
-// below -760 (exp underflows to exactly zero there).
-__global__ void __launch_bounds__(DD_NT) row_lse_kernel(int R, int M, int N, const double* in,
-                                                        double p0, double pd, double q0, double qd,
-                                                        double eps, double* out, int transpose) {
-    extern __shared__ double sh[];
-    double* row = sh;
-    double* qc = sh + M;
-    const int r = blockIdx.x;
-    for (int m = threadIdx.x; m < M; m += DD_NT) {
-        row[m] = in[(int64_t)r * M + m];
-        qc[m] = q0 + qd * (double)m;
+// Axis table in the reference's rounding, transposed: tab[m*N + n] = -(d*d)/eps with
+// d = (p0 + pd*n) - (q0 + qd*m)  (sinkhorn.py:149-151 _neg_sq, computed once per sweep).
+__global__ void neg_sq_table_kernel(int M, int N, double p0, double pd, double q0, double qd,
+                                    double eps, double* tab) {
+    const int64_t tot = (int64_t)M * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int m = (int)(i / N), n = (int)(i - (int64_t)m * N);
+        const double d = (p0 + pd * (double)n) - (q0 + qd * (double)m);
+        tab[i] = -(d * d) / eps;
+    }
+}
+
+// One separable stage for kRows input rows at once (they share every table load):
+//   out[r][n] = LSE_m(in[r][m] + tab[m][n])
+// two passes (max, then sum of exp(t - max) over the terms with t - max > -760; the
+// skipped ones are exactly 0 in double), the reference's _lse order per output.
+// Table reads are coalesced over n and L2-resident; input rows live in shared memory.
+template <int kRows>
+__global__ void __launch_bounds__(256) row_lse_tab_kernel(int R, int M, int N,
+                                                          const double* __restrict__ in,
+                                                          const double* __restrict__ tab,
+                                                          double* __restrict__ out, int transpose) {
+    extern __shared__ double rows[];   // [kRows][M]
+    const int r0 = blockIdx.x * kRows;
+    const int nr = min(kRows, R - r0);
+    for (int i = threadIdx.x; i < kRows * M; i += blockDim.x) {
+        const int q = i / M, m = i - q * M;
+        rows[i] = q < nr ? in[(int64_t)(r0 + q) * M + m] : kNegInf;
     }
     __syncthreads();
-    const int n = blockIdx.y * DD_NT + threadIdx.x;
+    const int n = blockIdx.y * blockDim.x + threadIdx.x;
     if (n >= N) return;
-    const double pc = p0 + pd * (double)n;
-    double mx = kNegInf;
+    double mx[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) mx[q] = kNegInf;
     for (int m = 0; m < M; ++m) {
-        const double d = pc - qc[m];
-        mx = fmax(mx, row[m] + (-(d * d) / eps));
+        const double t = __ldg(tab + (int64_t)m * N + n);
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) mx[q] = fmax(mx[q], rows[q * M + m] + t);
     }
-    double res;
-    if (!isfinite(mx)) {
-        res = kNegInf;
-    } else {
-        double s = 0.0;
-        for (int m = 0; m < M; ++m) {
-            const double d = pc - qc[m];
-            const double t = row[m] + (-(d * d) / eps) - mx;
-            if (t > -760.0) s += exp(t);
+    double sm[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) sm[q] = 0.0;
+    for (int m = 0; m < M; ++m) {
+        const double t = __ldg(tab + (int64_t)m * N + n);
+#pragma unroll
+        for (int q = 0; q < kRows; ++q) {
+            const double u = rows[q * M + m] + t - mx[q];
+            if (u > -760.0) sm[q] += exp(u);
         }
-        res = log(s) + mx;
     }
-    if (transpose) out[(int64_t)n * R + r] = res;
-    else out[(int64_t)r * N + n] = res;
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+        if (q >= nr) break;
+        const int r = r0 + q;
+        const double res = isfinite(mx[q]) ? log(sm[q]) + mx[q] : kNegInf;
+        if (transpose) out[(int64_t)n * R + r] = res;
+        else out[(int64_t)r * N + n] = res;
+    }
 }
 
 // divide == 0: out = a*s + b;  divide == 1: out = a/s + b  (b may be NULL)
@@ -704,36 +727,49 @@ static int grid_blocks(int64_t n) {
 }
 
 static int row_lse(int R, int M, int N, const double* in, double p0, double pd, double q0,
-                   double qd, double eps, double* out, int transpose, cudaStream_t st) {
-    const size_t smem = (size_t)2 * M * sizeof(double);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(dd::row_lse_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return dd_set_error(e);
-    }
-    dim3 grid(R, (N + DD_NT - 1) / DD_NT);
-    dd::row_lse_kernel<<<grid, DD_NT, smem, st>>>(R, M, N, in, p0, pd, q0, qd, eps, out, transpose);
-    return dd_set_error(cudaGetLastError());
+                   double qd, double eps, double* out, int transpose, double* tab,
+                   cudaStream_t st) {
+    const int64_t nt = (int64_t)M * N;
+    dd::neg_sq_table_kernel<<<grid_blocks(nt), DD_NT, 0, st>>>(M, N, p0, pd, q0, qd, eps, tab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return dd_set_error(e);
+    auto launch = [&](auto kern, int rows) -> int {
+        const size_t smem = (size_t)rows * M * sizeof(double);
+        if (smem > 48 * 1024) {
+            cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)smem);
+            if (e2 != cudaSuccess) return dd_set_error(e2);
+        }
+        dim3 grid((R + rows - 1) / rows, (N + 255) / 256);
+        kern<<<grid, 256, smem, st>>>(R, M, N, in, tab, out, transpose);
+        return dd_set_error(cudaGetLastError());
+    };
+    // rows per block: 8 while the rows fit 200 KB of shared memory
+    if ((size_t)8 * M * sizeof(double) <= 200 * 1024) return launch(dd::row_lse_tab_kernel<8>, 8);
+    if ((size_t)2 * M * sizeof(double) <= 200 * 1024) return launch(dd::row_lse_tab_kernel<2>, 2);
+    return launch(dd::row_lse_tab_kernel<1>, 1);
 }
 
 extern "C" int dd_grid_lse(const dd_geom* g, const double* v, double* out, int to_x, double* work,
                            void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    const int64_t mid = std::max((int64_t)g->ny0 * g->nx1, (int64_t)g->nx0 * g->ny1);
+    double* tab = work + mid;   // axis table of the current stage (reused by both)
     int rc;
     if (to_x) {
         // stage A: rows y0 of v (over y1) -> x1, stored transposed [nx1][ny0]
         rc = row_lse(g->ny0, g->ny1, g->nx1, v, g->x_org1, g->x_dx, g->y_org1, g->y_dx, g->eps,
-                     work, 1, st);
+                     work, 1, tab, st);
         if (rc) return rc;
         // stage B: rows x1 (over y0) -> x0, stored transposed [nx0][nx1]
         return row_lse(g->nx1, g->ny0, g->nx0, work, g->x_org0, g->x_dx, g->y_org0, g->y_dx,
-                       g->eps, out, 1, st);
+                       g->eps, out, 1, tab, st);
     }
     rc = row_lse(g->nx0, g->nx1, g->ny1, v, g->y_org1, g->y_dx, g->x_org1, g->x_dx, g->eps, work,
-                 1, st);
+                 1, tab, st);
     if (rc) return rc;
     return row_lse(g->ny1, g->nx0, g->ny0, work, g->y_org0, g->y_dx, g->x_org0, g->x_dx, g->eps,
-                   out, 1, st);
+                   out, 1, tab, st);
 }
 
 extern "C" int dd_axpb(int64_t n, const double* a, double s, const double* b, double* out,

@@ -86,7 +86,7 @@ class GridSweeper:
 
         self.dp = dp
         g = dp.geom
-        n = max(g.ny0 * g.nx1, g.nx0 * g.ny1)
+        n = max(g.ny0 * g.nx1, g.nx0 * g.ny1) + max(g.nx0 * g.ny0, g.nx1 * g.ny1)
         self.work = torch.empty(n, dtype=torch.float64, device=dp.device)
         self.sweeps = 0
 
