@@ -16,6 +16,7 @@
  * Reference interfaces replaced (paths under the reference package
  * pkg/src/domdec/):
  *   dd_grid_lse          sinkhorn.py:133-175   SeparableKernel.lse_x / lse_y
+ *   dd_sinkhorn_run      sinkhorn.py:361-432   sinkhorn_solve (device-side iteration loop)
  *   dd_newton_global     sinkhorn.py:256-260   y_halfstep_newton, m = None branch
  *   dd_global_terms      sinkhorn.py:336-358   gap_kl_terms / _gap_kl
  *                        engine.py:654-662     StitchedGapEvaluator._dual_at sums
@@ -241,6 +242,19 @@ int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy, int c, dou
 int dd_refine(const dd_geom* g, const dd_state* s, const int32_t* parent, const int32_t* cbox,
               const double* cval, int64_t ccap, const double* cmass, const double* nu_c,
               int cny1, double trunc, double* trunc_out, void* stream);
+
+/* Global unbalanced Sinkhorn iterations on the device (zero background):
+ * iterations k0 .. k0+n_iters-1 of sinkhorn.py:361-432 are enqueued without host
+ * synchronisation; the stopping test (gap/lam <= thr, checked at the top of every
+ * iteration k >= 2) runs on the device and sets ctl_i[0]; ctl_i[1] = completed
+ * iterations, ctl_d[0] = gap at the stop.  work holds dd_sinkhorn_ws(g) doubles
+ * (axis tables built when tables_ready == 0, reused after).  L, px (X grid) and
+ * z, bv, av (bv: Y grid, av: X grid) are scratch/outputs as in the host loop. */
+int64_t dd_sinkhorn_ws(const dd_geom* g);
+int dd_sinkhorn_run(const dd_geom* g, double* alpha, double* beta, const double* mu,
+                    const double* log_mu, const double* log_nu, double* L, double* z, double* bv,
+                    double* av, double* px, double* work, int* ctl_i, double* ctl_d, double thr,
+                    int k0, int n_iters, int tables_ready, void* stream);
 
 /* Bilinear prolongation of a cell-centred coarse field (nc0 x nc1) to the
  * x2 finer grid (nf0 x nf1); constant beyond the outer coarse centres. */

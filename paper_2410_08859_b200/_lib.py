@@ -21,7 +21,8 @@ EXPORTS = [
     "dd_cell_commit", "dd_assemble", "dd_energy_terms", "dd_product_init", "dd_cut_plan",
     "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
     "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong",
-    "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks",
+    "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks", "dd_sinkhorn_ws",
+    "dd_sinkhorn_run",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -86,6 +87,9 @@ _SIGS = {
     "dd_refine": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, i64, vp, vp, C.c_int, dbl, vp,
                    vp], C.c_int),
     "dd_prolong": ([C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
+    "dd_sinkhorn_ws": ([C.POINTER(Geom)], i64),
+    "dd_sinkhorn_run": ([C.POINTER(Geom), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, dbl,
+                         C.c_int, C.c_int, C.c_int, vp], C.c_int),
     "dd_newton_nodes": ([i64, vp, vp, vp, vp, vp, dbl, C.c_int, vp, vp, vp], C.c_int),
     "dd_opt_set": ([C.POINTER(Geom), C.POINTER(Batch), vp, C.c_int, dbl, vp, vp], C.c_int),
 }
@@ -117,12 +121,21 @@ def load(path: str = LIB_PATH) -> C.CDLL:
 
 # kernels each entry point launches (used for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
-    "dd_grid_lse": 2, "dd_axpb": 1, "dd_newton_global": 1, "dd_newton_nodes": 1,
+    "dd_grid_lse": 4, "dd_axpb": 1, "dd_newton_global": 1, "dd_newton_nodes": 1,
     "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_solve2": 3, "dd_cell_delta": 1, "dd_blend_energy": 6,
     "dd_cell_commit": 1, "dd_assemble": 2, "dd_energy_terms": 4, "dd_product_init": 1,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
 }
+
+
+# entry points whose kernel count depends on the arguments
+VARIABLE_LAUNCHES = {"dd_sinkhorn_run", "dd_sinkhorn_ws"}
+
+
+def _sinkhorn_run_launches(args) -> int:
+    k0, n, tables_ready = int(args[15]), int(args[16]), int(args[17])
+    return 10 * n + 2 * (n - (1 if k0 == 1 else 0)) + (0 if tables_ready else 4)
 
 
 class Tracer:
@@ -133,9 +146,11 @@ class Tracer:
         self.timed = set(timed)
         self.calls: dict = {}
         self.events: dict = {}
+        self.extra = 0          # launches of variable-length entry points
 
     def launches(self) -> int:
-        return sum(KERNELS_PER_CALL.get(k, 1) * n for k, n in self.calls.items())
+        return self.extra + sum(KERNELS_PER_CALL.get(k, 1) * n for k, n in self.calls.items()
+                                if k not in VARIABLE_LAUNCHES)
 
     def times_ms(self) -> dict:
         import torch
@@ -164,11 +179,14 @@ class _Traced:
         if t is None or not name.startswith("dd_") or name in ("dd_last_error", "dd_device_count",
                                                                "dd_abi_version", "dd_cell_ws_size",
                                                                "dd_cell_cluster_ws",
-                                                               "dd_cell_min_blocks"):
+                                                               "dd_cell_min_blocks",
+                                                               "dd_sinkhorn_ws"):
             return fn
 
         def call(*args):
             t.calls[name] = t.calls.get(name, 0) + 1
+            if name == "dd_sinkhorn_run":
+                t.extra += _sinkhorn_run_launches(args)
             if name in t.timed:
                 import torch
                 a = torch.cuda.Event(enable_timing=True)

@@ -7,7 +7,9 @@
 
 #include <limits.h>
 
+#ifndef DD_NT
 #define DD_NT 512
+#endif
 #define DD_NW (DD_NT / 32)
 
 namespace dd {

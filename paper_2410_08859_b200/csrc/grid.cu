@@ -49,8 +49,10 @@ template <int kRows>
 __global__ void __launch_bounds__(256) row_lse_tab_kernel(int R, int M, int N,
                                                           const double* __restrict__ in,
                                                           const double* __restrict__ tab,
-                                                          double* __restrict__ out, int transpose) {
+                                                          double* __restrict__ out, int transpose,
+                                                          const int* stop) {
     extern __shared__ double rows[];   // [kRows][M]
+    if (stop && *stop) return;
     const int r0 = blockIdx.x * kRows;
     const int nr = min(kRows, R - r0);
     for (int i = threadIdx.x; i < kRows * M; i += blockDim.x) {
@@ -91,7 +93,8 @@ __global__ void __launch_bounds__(256) row_lse_tab_kernel(int R, int M, int N,
 
 // divide == 0: out = a*s + b;  divide == 1: out = a/s + b  (b may be NULL)
 __global__ void axpb_kernel(int64_t n, const double* a, double s, const double* b, double* out,
-                            int divide) {
+                            int divide, const int* stop = nullptr) {
+    if (stop && *stop) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double t = divide ? a[i] / s : a[i] * s;
@@ -100,7 +103,10 @@ __global__ void axpb_kernel(int64_t n, const double* a, double s, const double* 
 }
 
 __global__ void newton_global_kernel(int64_t n, const double* z, double ratio, double lam,
-                                     double* beta, int32_t* n_deg) {
+                                     double* beta, int32_t* n_deg, const int* stop = nullptr,
+                                     int* iters = nullptr, int k = 0) {
+    if (stop && *stop) return;
+    if (iters && blockIdx.x == 0 && threadIdx.x == 0) *iters = k;
     int cnt = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -137,7 +143,9 @@ __global__ void __launch_bounds__(DD_NT) terms_kernel(int mode, int64_t n_x, int
                                                       const double* a, const double* l,
                                                       const double* w, const double* b,
                                                       const double* z, const double* w2, double eps,
-                                                      double lam, double* px, double* partial) {
+                                                      double lam, double* px, double* partial,
+                                                      const int* stop = nullptr) {
+    if (stop && *stop) return;
     __shared__ double red[DD_NW + 1];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     const int64_t stride = (int64_t)gridDim.x * DD_NT;
@@ -180,6 +188,24 @@ __global__ void __launch_bounds__(DD_NT) terms_kernel(int mode, int64_t n_x, int
 }
 
 // out[q] = sum_r in[r*width + q] in a fixed order (one block per q)
+// Global Sinkhorn stopping test on the device (sinkhorn.py:361-432): the gap sum
+// reduced exactly as reduce_rows_kernel does for dd_global_terms, gap = lam * sum,
+// done when gap / lam <= thr (the host loop's arithmetic).  ctl_i = {done, iters},
+// ctl_d = {gap}.
+__global__ void __launch_bounds__(DD_NT) sk_check_kernel(const double* partial, double lam,
+                                                         double thr, int* ctl_i, double* ctl_d) {
+    __shared__ double red[DD_NW + 1];
+    if (ctl_i[0]) return;
+    double s = 0.0;
+    for (int64_t r = threadIdx.x; r < kRedBlocks; r += DD_NT) s += partial[r];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        const double gap = lam * s;
+        ctl_d[0] = gap;
+        if (gap / lam <= thr) ctl_i[0] = 1;
+    }
+}
+
 __global__ void __launch_bounds__(DD_NT) reduce_rows_kernel(int64_t n_rows, int width,
                                                             const double* in, double* out) {
     __shared__ double red[DD_NW + 1];
@@ -726,13 +752,8 @@ static int grid_blocks(int64_t n) {
     return (int)b;
 }
 
-static int row_lse(int R, int M, int N, const double* in, double p0, double pd, double q0,
-                   double qd, double eps, double* out, int transpose, double* tab,
-                   cudaStream_t st) {
-    const int64_t nt = (int64_t)M * N;
-    dd::neg_sq_table_kernel<<<grid_blocks(nt), DD_NT, 0, st>>>(M, N, p0, pd, q0, qd, eps, tab);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return dd_set_error(e);
+static int row_lse_apply(int R, int M, int N, const double* in, const double* tab, double* out,
+                         int transpose, const int* stop, cudaStream_t st) {
     auto launch = [&](auto kern, int rows) -> int {
         const size_t smem = (size_t)rows * M * sizeof(double);
         if (smem > 48 * 1024) {
@@ -741,13 +762,28 @@ static int row_lse(int R, int M, int N, const double* in, double p0, double pd, 
             if (e2 != cudaSuccess) return dd_set_error(e2);
         }
         dim3 grid((R + rows - 1) / rows, (N + 255) / 256);
-        kern<<<grid, 256, smem, st>>>(R, M, N, in, tab, out, transpose);
+        kern<<<grid, 256, smem, st>>>(R, M, N, in, tab, out, transpose, stop);
         return dd_set_error(cudaGetLastError());
     };
     // rows per block: 8 while the rows fit 200 KB of shared memory
     if ((size_t)8 * M * sizeof(double) <= 200 * 1024) return launch(dd::row_lse_tab_kernel<8>, 8);
     if ((size_t)2 * M * sizeof(double) <= 200 * 1024) return launch(dd::row_lse_tab_kernel<2>, 2);
     return launch(dd::row_lse_tab_kernel<1>, 1);
+}
+
+static int neg_sq_table(int M, int N, double p0, double pd, double q0, double qd, double eps,
+                        double* tab, cudaStream_t st) {
+    const int64_t nt = (int64_t)M * N;
+    dd::neg_sq_table_kernel<<<grid_blocks(nt), DD_NT, 0, st>>>(M, N, p0, pd, q0, qd, eps, tab);
+    return dd_set_error(cudaGetLastError());
+}
+
+static int row_lse(int R, int M, int N, const double* in, double p0, double pd, double q0,
+                   double qd, double eps, double* out, int transpose, double* tab,
+                   cudaStream_t st) {
+    const int rc = neg_sq_table(M, N, p0, pd, q0, qd, eps, tab, st);
+    if (rc) return rc;
+    return row_lse_apply(R, M, N, in, tab, out, transpose, nullptr, st);
 }
 
 extern "C" int dd_grid_lse(const dd_geom* g, const double* v, double* out, int to_x, double* work,
@@ -770,6 +806,63 @@ extern "C" int dd_grid_lse(const dd_geom* g, const double* v, double* out, int t
     if (rc) return rc;
     return row_lse(g->ny1, g->nx0, g->ny0, work, g->y_org0, g->y_dx, g->x_org0, g->x_dx, g->eps,
                    out, 1, tab, st);
+}
+
+extern "C" int64_t dd_sinkhorn_ws(const dd_geom* g) {
+    const int64_t mid = std::max((int64_t)g->ny0 * g->nx1, (int64_t)g->nx0 * g->ny1);
+    return mid + 2 * ((int64_t)g->nx1 * g->ny1 + (int64_t)g->nx0 * g->ny0) + 5 * 1024;
+}
+
+// n_iters iterations k = k0 .. k0+n_iters-1 of the global unbalanced Sinkhorn with
+// zero background (sinkhorn.py:361-432), enqueued without host synchronisation:
+// the stopping test runs on the device and every later kernel of the chunk exits at
+// once after it fires.  Same operations, in the same order, as the host loop in
+// sinkhorn.sinkhorn_solve (gap at the top of iteration k >= 2 from the X sweep the
+// next alpha reuses; the loop always ends after a Y half-step).
+extern "C" int dd_sinkhorn_run(const dd_geom* g, double* alpha, double* beta, const double* mu,
+                               const double* log_mu, const double* log_nu, double* L, double* z,
+                               double* bv, double* av, double* px, double* work, int* ctl_i,
+                               double* ctl_d, double thr, int k0, int n_iters, int tables_ready,
+                               void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nx = (int64_t)g->nx0 * g->nx1, ny = (int64_t)g->ny0 * g->ny1;
+    const int64_t mid = std::max((int64_t)g->ny0 * g->nx1, (int64_t)g->nx0 * g->ny1);
+    double* tmid = work;
+    double* tXa = work + mid;                               // [ny1][nx1]
+    double* tXb = tXa + (int64_t)g->nx1 * g->ny1;           // [ny0][nx0]
+    double* tYa = tXb + (int64_t)g->nx0 * g->ny0;           // [nx1][ny1]
+    double* tYb = tYa + (int64_t)g->nx1 * g->ny1;           // [nx0][ny0]
+    double* partial = tYb + (int64_t)g->nx0 * g->ny0;       // 3 * kRedBlocks
+    const double eps = g->eps, lam = g->lam;
+    const double ratio = eps * lam / (eps + lam);
+    int rc;
+    if (!tables_ready) {
+        if ((rc = neg_sq_table(g->ny1, g->nx1, g->x_org1, g->x_dx, g->y_org1, g->y_dx, eps, tXa, st))) return rc;
+        if ((rc = neg_sq_table(g->ny0, g->nx0, g->x_org0, g->x_dx, g->y_org0, g->y_dx, eps, tXb, st))) return rc;
+        if ((rc = neg_sq_table(g->nx1, g->ny1, g->y_org1, g->y_dx, g->x_org1, g->x_dx, eps, tYa, st))) return rc;
+        if ((rc = neg_sq_table(g->nx0, g->ny0, g->y_org0, g->y_dx, g->x_org0, g->x_dx, eps, tYb, st))) return rc;
+    }
+    const int* stop = ctl_i;
+    for (int k = k0; k < k0 + n_iters; ++k) {
+        dd::axpb_kernel<<<grid_blocks(ny), DD_NT, 0, st>>>(ny, beta, eps, log_nu, bv, 1, stop);
+        if ((rc = row_lse_apply(g->ny0, g->ny1, g->nx1, bv, tXa, tmid, 1, stop, st))) return rc;
+        if ((rc = row_lse_apply(g->nx1, g->ny0, g->nx0, tmid, tXb, L, 1, stop, st))) return rc;
+        if (k >= 2) {
+            dd::terms_kernel<<<dd::kRedBlocks, DD_NT, 0, st>>>(0, nx, 0, alpha, L, mu, nullptr,
+                                                              nullptr, nullptr, eps, lam, px,
+                                                              partial, stop);
+            dd::sk_check_kernel<<<1, DD_NT, 0, st>>>(partial, lam, thr, ctl_i, ctl_d);
+        }
+        dd::axpb_kernel<<<grid_blocks(nx), DD_NT, 0, st>>>(nx, L, -ratio, nullptr, alpha, 0, stop);
+        dd::axpb_kernel<<<grid_blocks(nx), DD_NT, 0, st>>>(nx, alpha, eps, log_mu, av, 1, stop);
+        if ((rc = row_lse_apply(g->nx0, g->nx1, g->ny1, av, tYa, tmid, 1, stop, st))) return rc;
+        if ((rc = row_lse_apply(g->ny1, g->nx0, g->ny0, tmid, tYb, z, 1, stop, st))) return rc;
+        dd::newton_global_kernel<<<grid_blocks(ny), DD_NT, 0, st>>>(ny, z, ratio, lam, beta,
+                                                                    nullptr, stop, ctl_i + 1, k);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return dd_set_error(e);
+    }
+    return 0;
 }
 
 extern "C" int dd_axpb(int64_t n, const double* a, double s, const double* b, double* out,

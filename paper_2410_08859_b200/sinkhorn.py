@@ -227,6 +227,40 @@ def sinkhorn_solve(dp: DeviceProblem, alpha0=None, beta0=None, config: SolverCon
     converged = False
     iterations = 0
     trace = []
+    if not collect_trace and config.max_iters > 0:
+        # device-side loop: chunks of iterations enqueued by dd_sinkhorn_run with the
+        # stopping test on the device; one host synchronisation per chunk
+        lib = _lib.lib()
+        ws = torch.empty(int(lib.dd_sinkhorn_ws(g)), dtype=torch.float64, device=dp.device)
+        ctl_i = torch.zeros(2, dtype=torch.int32, device=dp.device)
+        ctl_d = torch.zeros(1, dtype=torch.float64, device=dp.device)
+        k, chunk, tables = 1, 16, 0
+        while k <= config.max_iters:
+            n = min(chunk, config.max_iters - k + 1)
+            _lib.check(lib.dd_sinkhorn_run(g, alpha.data_ptr(), beta.data_ptr(), dp.mu.data_ptr(),
+                                           dp.log_mu.data_ptr(), dp.log_nu.data_ptr(),
+                                           L.data_ptr(), z.data_ptr(), bv.data_ptr(),
+                                           av.data_ptr(), px.data_ptr(), ws.data_ptr(),
+                                           ctl_i.data_ptr(), ctl_d.data_ptr(), float(thr), k, n,
+                                           tables, _lib.stream_handle()))
+            tables = 1
+            c = ctl_i.cpu().numpy()
+            if c[0]:
+                converged = True
+                gap = float(ctl_d.item())
+                break
+            k += n
+            chunk = min(chunk * 2, 256)
+        iterations = int(ctl_i[1].item())
+        if converged:
+            return GlobalResult(alpha=alpha, beta=beta, gap=gap, iterations=iterations,
+                                converged=True, x_marginal=px, gap_trace=trace)
+        axpb(beta, eps, dp.log_nu, out=bv, divide=True)
+        sw.lse_x(bv, out=L)
+        gap = lam * gap_sum(dp, alpha, L, px)
+        converged = gap / lam <= thr
+        return GlobalResult(alpha=alpha, beta=beta, gap=gap, iterations=iterations,
+                            converged=converged, x_marginal=px, gap_trace=trace)
     for k in range(1, config.max_iters + 1):
         axpb(beta, eps, dp.log_nu, out=bv, divide=True)
         sw.lse_x(bv, out=L)
