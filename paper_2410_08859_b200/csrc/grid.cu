@@ -754,6 +754,8 @@ static int grid_blocks(int64_t n) {
 
 static int row_lse_apply(int R, int M, int N, const double* in, const double* tab, double* out,
                          int transpose, const int* stop, cudaStream_t st) {
+    // threads per block: the outputs of one row (rounded to warps, <= 256)
+    const int nt = std::min(256, (N + 31) / 32 * 32);
     auto launch = [&](auto kern, int rows) -> int {
         const size_t smem = (size_t)rows * M * sizeof(double);
         if (smem > 48 * 1024) {
@@ -761,13 +763,19 @@ static int row_lse_apply(int R, int M, int N, const double* in, const double* ta
                                                   (int)smem);
             if (e2 != cudaSuccess) return dd_set_error(e2);
         }
-        dim3 grid((R + rows - 1) / rows, (N + 255) / 256);
-        kern<<<grid, 256, smem, st>>>(R, M, N, in, tab, out, transpose, stop);
+        dim3 grid((R + rows - 1) / rows, (N + nt - 1) / nt);
+        kern<<<grid, nt, smem, st>>>(R, M, N, in, tab, out, transpose, stop);
         return dd_set_error(cudaGetLastError());
     };
-    // rows per block: 8 while the rows fit 200 KB of shared memory
-    if ((size_t)8 * M * sizeof(double) <= 200 * 1024) return launch(dd::row_lse_tab_kernel<8>, 8);
-    if ((size_t)2 * M * sizeof(double) <= 200 * 1024) return launch(dd::row_lse_tab_kernel<2>, 2);
+    // rows per block: as many as keep >= 2 blocks per SM (148 SMs) and fit 200 KB of
+    // shared memory; small grids get one row per block (parallelism over reuse)
+    const int64_t col_blocks = (N + nt - 1) / nt;
+    auto fits = [&](int rows) {
+        return (size_t)rows * M * sizeof(double) <= 200 * 1024 &&
+               ((R + rows - 1) / rows) * col_blocks >= 2 * 148;
+    };
+    if (fits(8)) return launch(dd::row_lse_tab_kernel<8>, 8);
+    if (fits(2)) return launch(dd::row_lse_tab_kernel<2>, 2);
     return launch(dd::row_lse_tab_kernel<1>, 1);
 }
 
