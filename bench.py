@@ -30,9 +30,11 @@ seconds (lower is better).
   cores; ``value`` is the measured seconds of one sample (what ran), the scaled
   whole-solve estimate is a separate labelled field.
 
-Multi-GPU (``--gpus N`` under torchrun): every batch's cell solves are
-partitioned across the ranks (cost-balanced) and the solve outputs summed
-with NCCL (strong scaling); value is the max over ranks.
+Multi-GPU (``--gpus N`` under torchrun): row-slab sharding (slab.py) — each
+rank owns a contiguous slab of block rows and solves its composites; the Y
+snapshot and blend sums are all-reduced per batch and the boundary block row
+moves between neighbours at every A/B switch (strong scaling: the whole job
+solves one problem); value is the max over ranks.
 """
 
 from __future__ import annotations
@@ -213,8 +215,10 @@ def main():
                                "layer 8 / the finest layer, domdec above)",
                    "grid": list(prob.mu.grid.dims), "cell": cfg["cell"], "lambda": cfg["lam"],
                    "strategy": "staggered", "l2": "flushed (256 MiB write) before every step",
-                   "parallelism": (f"cell-sharded x{world} (batch cell solves partitioned, "
-                                   "NCCL all-reduce of the solve outputs)") if world > 1 else "1 GPU",
+                   "parallelism": (f"row-slab x{world} (each rank solves the composites of its "
+                                   "block-row slab; NCCL all-reduce of the Y snapshot and blend "
+                                   "sums per batch, halo exchange of the boundary block row "
+                                   "at each A/B switch)") if world > 1 else "1 GPU",
                    "seed": args.seed}
 
     if args.impl == "reference":
@@ -250,8 +254,7 @@ def main():
     from paper_2410_08859_b200 import _lib
     from paper_2410_08859_b200.multiscale import build_pyramid, stage_pyramid
     if world > 1:
-        # shard every batch's cell solves across the ranks (NCCL sum of the
-        # solve's output arenas; bitwise identical to one GPU)
+        # row-slab sharding of every domdec solve (slab.py)
         from paper_2410_08859_b200.engine import set_shard
         set_shard()
 

@@ -25,7 +25,7 @@
  *   dd_cell_delta        engine.py:388-433     BlendScorer.__init__ (per-cell deltas)
  *   dd_blend_energy      engine.py:441-456     BlendScorer.energy_at
  *   dd_cell_commit       engine.py:726-785     _commit_cell + _stitch_alpha
- *   dd_assemble          measures.py:410-425   assemble_y_marginal
+ *   dd_assemble          measures.py:410-425   assemble_y_marginal (+ _masked: slab mode)
  *   dd_energy_terms      engine.py:185-196     PlanState.energy
  *   dd_product_init      engine.py:234-257     initial_plan_state (+ cells.py:566 product_plan_fragments)
  *   dd_cut_plan          engine.py:294-322     warm_start_plan (plan cut along basic cells)
@@ -190,19 +190,35 @@ int dd_blend_energy(const dd_geom* g, const dd_state* s, const dd_batch* b, cons
                     const double* cd, const double* theta, double* ywork, double* partial,
                     double* out, void* stream);
 
+/* Slab mode, rank-local parts of dd_blend_energy: dsum (Y grid) = sum_c theta_c dy_c
+ * over the cells with theta_c != 0 (no snapshot base), out[1..3] = their summed
+ * per-cell pieces, out[0] = 0.  The caller sums dsum and out over the ranks. */
+int dd_blend_parts(const dd_geom* g, const dd_state* s, const dd_batch* b, const double* dy,
+                   const double* cd, const double* theta, double* dsum, double* partial,
+                   double* out, void* stream);
+
 /* Commit theta-blends; stores duals, stitches alpha into alpha_grid, writes
  * per-cell errs[c*4] = x_err, y_err, truncated added, unused.  If yrun is
  * non-NULL it is updated in place (sequential mode). */
 int dd_cell_commit(const dd_geom* g, const dd_state* s, const dd_batch* b, const double* theta,
                    double* alpha_grid, double* yrun, double* errs, void* stream);
 
-/* out (Y grid) = sum of the basic-cell marginals. */
+/* out (Y grid) = sum of the basic-cell marginals, accumulated in cell index order
+ * (fixed-order gather, bitwise reproducible). */
 int dd_assemble(const dd_geom* g, const dd_state* s, double* out, void* stream);
+
+/* Slab mode: the same sum over the basic cells whose mask entry is 1.0 (0.0 skips;
+ * one double per basic cell). */
+int dd_assemble_masked(const dd_geom* g, const dd_state* s, const double* mask, double* out,
+                       void* stream);
 
 /* sums[0] = sum transport, [1] = sum kl, [2] = sum_i KL(x_marg_i | mu_i),
  * [3] = KL(y | nu) for the given Y grid y. */
 int dd_energy_terms(const dd_geom* g, const dd_state* s, const double* y, double* partial,
                     double* sums, void* stream);
+/* Slab mode: sums[0..2] over the basic cells with mask 1.0 only; sums[3] as above. */
+int dd_energy_terms_masked(const dd_geom* g, const dd_state* s, const double* y,
+                           const double* mask, double* partial, double* sums, void* stream);
 
 /* Product start nu_i = (m_i/|mu|) nu on the full box (cap >= ny0*ny1). */
 int dd_product_init(const dd_geom* g, const dd_state* s, double mu_total, void* stream);

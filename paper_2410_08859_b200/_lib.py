@@ -22,7 +22,7 @@ EXPORTS = [
     "dd_seed_duals", "dd_cell_ws_size", "dd_reduce_rows", "dd_grid_kl", "dd_opt_gh",
     "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong",
     "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks", "dd_sinkhorn_ws",
-    "dd_sinkhorn_run",
+    "dd_sinkhorn_run", "dd_assemble_masked", "dd_energy_terms_masked", "dd_blend_parts",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -74,7 +74,11 @@ _SIGS = {
     "dd_cell_commit": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp],
                        C.c_int),
     "dd_assemble": ([C.POINTER(Geom), C.POINTER(State), vp, vp], C.c_int),
+    "dd_assemble_masked": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp], C.c_int),
     "dd_energy_terms": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, vp], C.c_int),
+    "dd_energy_terms_masked": ([C.POINTER(Geom), C.POINTER(State), vp, vp, vp, vp, vp], C.c_int),
+    "dd_blend_parts": ([C.POINTER(Geom), C.POINTER(State), C.POINTER(Batch), vp, vp, vp, vp, vp,
+                        vp, vp], C.c_int),
     "dd_product_init": ([C.POINTER(Geom), C.POINTER(State), dbl, vp], C.c_int),
     "dd_cut_plan": ([C.POINTER(Geom), C.POINTER(State), vp, vp, dbl, vp, vp, vp], C.c_int),
     "dd_seed_duals": ([C.POINTER(Geom), C.POINTER(State), C.c_int, C.c_int, C.c_int, vp, vp, vp,
@@ -124,6 +128,7 @@ KERNELS_PER_CALL = {
     "dd_grid_lse": 4, "dd_axpb": 1, "dd_newton_global": 1, "dd_newton_nodes": 1,
     "dd_global_terms": 4, "dd_cell_solve": 1, "dd_cell_solve2": 3, "dd_cell_delta": 1, "dd_blend_energy": 6,
     "dd_cell_commit": 1, "dd_assemble": 2, "dd_energy_terms": 4, "dd_product_init": 1,
+    "dd_assemble_masked": 2, "dd_energy_terms_masked": 4, "dd_blend_parts": 4,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
 }

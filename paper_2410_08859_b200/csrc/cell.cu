@@ -1541,6 +1541,11 @@ __global__ void __launch_bounds__(DD_NT) cell_delta_kernel(dd_geom g, dd_state s
     const int32_t* mem = b.members + d[10];
     const int ny = cw.ny, ny1 = cw.ye1;
     const int64_t yoff = off[0];
+    if (d[11] & 2) {   // cell held by another rank (slab mode): no update from here
+        for (int y = threadIdx.x; y < ny; y += DD_NT) dy[yoff + y] = 0.0;
+        if (threadIdx.x < 4) cd[(int64_t)c * 4 + threadIdx.x] = 0.0;
+        return;
+    }
     const double* NEWV = b.marena + off[1] + (int64_t)5 * nmem * ny;
     for (int y = threadIdx.x; y < ny; y += DD_NT) {
         const int y0 = y / ny1, y1 = y - y0 * ny1;
@@ -1646,6 +1651,10 @@ __global__ void __launch_bounds__(DD_NT) cell_commit_kernel(dd_geom g, dd_state 
     const double th = theta[c];
     const int bs = s.block0 * s.block1;
     const int tid = threadIdx.x;
+    if (d[11] & 2) {   // cell held by another rank (slab mode): its owner commits it
+        if (tid < 4) errs[(int64_t)c * 4 + tid] = 0.0;
+        return;
+    }
 
     // old member windows on the cell's Y box
     for (int k = 0; k < nmem; ++k) {
@@ -2021,6 +2030,30 @@ extern "C" int dd_blend_energy(const dd_geom* g, const dd_state* s, const dd_bat
     } else {
         e = cudaMemsetAsync(out + 1, 0, 3 * sizeof(double), st);
         if (e != cudaSuccess) return dd_set_error(e);
+    }
+    return 0;
+}
+
+// Slab mode: the rank-local parts of dd_blend_energy.  dsum = sum_c theta_c dy_c over
+// the cells with theta_c != 0 (no snapshot base; the caller masks theta to its own
+// cells, sums dsum over the ranks and adds the snapshot), out[1..3] = the summed
+// per-cell pieces of those cells, out[0] = 0.
+extern "C" int dd_blend_parts(const dd_geom* g, const dd_state* s, const dd_batch* b,
+                              const double* dy, const double* cd, const double* theta,
+                              double* dsum, double* partial, double* out, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = dd_box_gather(b->n_cells, b->desc + 5, 12, dy, 0, b->offs, 4, theta, g->ny0, g->ny1,
+                           nullptr, dsum, st);
+    if (rc) return rc;
+    cudaError_t e = cudaMemsetAsync(out, 0, 4 * sizeof(double), st);
+    if (e != cudaSuccess) return dd_set_error(e);
+    if (b->n_cells > 0) {
+        double* pc = partial + 4096;
+        dd::blend_cell_kernel<<<b->n_cells, DD_NT, 0, st>>>(*g, *s, *b, cd, theta, pc);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return dd_set_error(e);
+        rc = dd_reduce_rows(b->n_cells, 4, pc, out + 1, stream);
+        if (rc) return rc;
     }
     return 0;
 }

@@ -361,9 +361,14 @@ int dd_box_gather(int n, const int32_t* box, int bstride, const double* vals, in
 namespace dd {
 
 // per basic cell: [transport, kl, d1_i, 0]
-__global__ void __launch_bounds__(DD_NT) cell_terms_kernel(dd_geom g, dd_state s, double* pc) {
+__global__ void __launch_bounds__(DD_NT) cell_terms_kernel(dd_geom g, dd_state s, double* pc,
+                                                           const double* mask) {
     __shared__ double red[DD_NW + 1];
     const int i = blockIdx.x;
+    if (mask && mask[i] == 0.0) {   // basic cell held by another rank (slab mode)
+        if (threadIdx.x < 4) pc[(int64_t)i * 4 + threadIdx.x] = 0.0;
+        return;
+    }
     const int32_t* bx = s.basic_xbox + (int64_t)i * 4;
     const int bs = s.block0 * s.block1;
     double p = 0.0;
@@ -934,11 +939,28 @@ extern "C" int dd_assemble(const dd_geom* g, const dd_state* s, double* out, voi
                          g->ny1, nullptr, out, (cudaStream_t)stream);
 }
 
+extern "C" int dd_assemble_masked(const dd_geom* g, const dd_state* s, const double* mask,
+                                  double* out, void* stream) {
+    // mask entries are exactly 1 or 0: 1 * v is v, 0 skips the cell
+    return dd_box_gather(s->n_basic, s->ybox, 4, s->yval, s->cap, nullptr, 0, mask, g->ny0,
+                         g->ny1, nullptr, out, (cudaStream_t)stream);
+}
+
+extern "C" int dd_energy_terms_masked(const dd_geom* g, const dd_state* s, const double* y,
+                                      const double* mask, double* partial, double* sums,
+                                      void* stream);
+
 extern "C" int dd_energy_terms(const dd_geom* g, const dd_state* s, const double* y,
                                double* partial, double* sums, void* stream) {
+    return dd_energy_terms_masked(g, s, y, nullptr, partial, sums, stream);
+}
+
+extern "C" int dd_energy_terms_masked(const dd_geom* g, const dd_state* s, const double* y,
+                                      const double* mask, double* partial, double* sums,
+                                      void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     double* pc = partial + 4096;
-    dd::cell_terms_kernel<<<s->n_basic, DD_NT, 0, st>>>(*g, *s, pc);
+    dd::cell_terms_kernel<<<s->n_basic, DD_NT, 0, st>>>(*g, *s, pc, mask);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return dd_set_error(e);
     int rc = dd_reduce_rows(s->n_basic, 4, pc, sums, stream);

@@ -38,6 +38,7 @@ from .grids import GridMeasure, SparseCellMarginal, TransportProblem
 from .report import SolveReport, TraceRow
 from .sinkhorn import (DeviceProblem, GridSweeper, SolverConfig, axpb, dual_sums,
                        sinkhorn_solve)
+from .slab import ShardSpec
 
 log = logging.getLogger(__name__)
 
@@ -310,6 +311,10 @@ class PlanState:
         self.truncated_mass = 0.0
         self.global_duals = None
         self.iter_hist: dict = {}   # partition label -> executed iterations of the last solve
+        # slab mode: owning rank of each basic cell (None: every cell current here)
+        self.owner = None
+        self._mask_d = None
+        self.comp_owner: dict = {}  # slab mode: partition label -> owner of each composite
         self.buf = _Buffers(dev)
         self.partial = torch.empty(8192 + 4 * nb, dtype=torch.float64, device=dev)
         self.sums = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -351,14 +356,41 @@ class PlanState:
     def sync_boxes(self):
         self.ybox_h = self.ybox.view(-1, 4).cpu().numpy().copy()
 
+    def set_owner(self, owner) -> None:
+        """Slab mode: the owning rank of every basic cell (None: all current here)."""
+        import torch
+
+        self.owner = None if owner is None else np.asarray(owner, dtype=np.int64).copy()
+        if self.owner is None or _SHARD is None:
+            self._mask_d = None
+        else:
+            m = (self.owner == _SHARD.rank).astype(np.float64)
+            self._mask_d = torch.from_numpy(m).to(self.dp.device)
+
+    def _sharded(self) -> bool:
+        return _SHARD is not None and _SHARD.world > 1 and self._mask_d is not None
+
     # ---- energy
     def assemble_device(self, out=None):
         out = out if out is not None else self.dp.empty_y()
+        if self._sharded():
+            # own basic cells, then one dense all-reduce over the slabs
+            _lib.check(_lib.lib().dd_assemble_masked(self.dp.geom, self.state_struct(),
+                                                     self._mask_d.data_ptr(), out.data_ptr(),
+                                                     _lib.stream_handle()))
+            _SHARD.all_reduce(out[:self.dp.ny])
+            return out
         _lib.check(_lib.lib().dd_assemble(self.dp.geom, self.state_struct(), out.data_ptr(),
                                           _lib.stream_handle()))
         return out
 
     def energy_terms(self, y) -> np.ndarray:
+        if self._sharded():
+            _lib.check(_lib.lib().dd_energy_terms_masked(
+                self.dp.geom, self.state_struct(), y.data_ptr(), self._mask_d.data_ptr(),
+                self.partial.data_ptr(), self.sums.data_ptr(), _lib.stream_handle()))
+            _SHARD.all_reduce(self.sums[:3])    # per-cell sums; sums[3] is KL of the global y
+            return self.sums[:4].cpu().numpy().copy()
         _lib.check(_lib.lib().dd_energy_terms(self.dp.geom, self.state_struct(), y.data_ptr(),
                                               self.partial.data_ptr(), self.sums.data_ptr(),
                                               _lib.stream_handle()))
@@ -450,6 +482,8 @@ class PlanState:
                                              self.kl_d.clone())
         c.stores = {k: v.clone() for k, v in self.stores.items()}
         c.iter_hist = {k: v.copy() for k, v in self.iter_hist.items()}
+        c.owner = None if self.owner is None else self.owner.copy()
+        c.comp_owner = dict(self.comp_owner)
         c.buf = _Buffers(self.dp.device)
         c.partial = self.partial.clone()
         c.sums = self.sums.clone()
@@ -531,66 +565,12 @@ def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta:
     return st
 
 
-class ShardSpec:
-    """Cell-sharded execution over a torch.distributed process group.
-
-    Every rank holds the full plan state and runs the identical control flow;
-    only the cell solves of each batch are partitioned (cost-balanced by window
-    size).  Each rank solves its own cells, the solve's output arenas (zero for
-    cells owned elsewhere) are summed across ranks (adding zeros is exact), and
-    everything downstream proceeds identically everywhere: every kernel is
-    deterministic (the Y-marginal assembly and the blend are fixed-order
-    gathers, no float atomics), so the ranks' states, window layouts and
-    control flow stay bitwise identical without any broadcast.
-    """
-
-    def __init__(self, group=None):
-        import torch.distributed as dist
-
-        self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-        self.nccl = dist.get_backend(group) == "nccl"
-
-    def all_reduce_sum(self, t) -> None:
-        import torch.distributed as dist
-
-        if self.nccl:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
-        else:   # gloo: reduce through host memory
-            c = t.cpu()
-            dist.all_reduce(c, op=dist.ReduceOp.SUM, group=self.group)
-            t.copy_(c)
-
-    def broadcast(self, t) -> None:
-        """Rank 0's values to every rank (in place)."""
-        import torch.distributed as dist
-
-        src = dist.get_global_rank(self.group, 0) if self.group is not None else 0
-        if self.nccl:
-            dist.broadcast(t, src=src, group=self.group)
-        else:
-            c = t.cpu()
-            dist.broadcast(c, src=src, group=self.group)
-            t.copy_(c)
-
-    def owners(self, cost: np.ndarray) -> np.ndarray:
-        """Greedy longest-processing-time assignment (deterministic on every rank)."""
-        order = np.argsort(-cost, kind="stable")
-        load = np.zeros(self.world)
-        own = np.empty(len(cost), dtype=np.int64)
-        for c in order:
-            r = int(np.argmin(load))
-            own[c] = r
-            load[r] += cost[c]
-        return own
-
-
 _SHARD: ShardSpec | None = None
 
 
 def set_shard(group=None) -> ShardSpec:
-    """Shard the cell solves of every batch over ``group`` (default: WORLD)."""
+    """Row-slab sharding of every domdec solve over ``group`` (default: WORLD);
+    see :mod:`paper_2410_08859_b200.slab`."""
     global _SHARD
     _SHARD = ShardSpec(group)
     return _SHARD
@@ -629,6 +609,13 @@ def _tables(part: CompositePartition) -> _PartTables:
         hit = _PartTables(part)
         _TABLE_CACHE[key] = hit
     return hit
+
+
+def _slab_layout(st: "PlanState", pt: _PartTables):
+    """(composite owner, basic-cell owner) of a partition under the active slab sharding."""
+    lat = st.basic.lattice_to_cell.shape
+    rows, cols = (lat[0], lat[1]) if len(lat) == 2 else (1, lat[0])
+    return _SHARD.layout(pt, st.block, st.n_basic, rows, cols)
 
 
 # -- one batch on the device -----------------------------------------------------------
@@ -697,12 +684,12 @@ class _Batch:
                 csize[ok] = C
                 csmem[ok] = cws[ok]
                 clu |= ok
-        # sharded solve: cells owned by other ranks are skipped (desc flag bit 1)
+        # slab mode: composites of other ranks' slabs are skipped (desc flag bit 1)
         owned = np.ones(n, dtype=bool)
-        self.shard = _SHARD if (_SHARD is not None and _SHARD.world > 1) else None
+        self.shard = _SHARD if st._sharded() else None
         if self.shard is not None:
-            cost = (ny.astype(np.float64) + 1.0) * (pt.nw0 * pt.nw1)
-            owned = self.shard.owners(cost) == self.shard.rank
+            comp, _ = _slab_layout(st, pt)
+            owned = comp[ids] == self.shard.rank
             clu &= owned
         self.owned = owned
         # expected cost of each cell: window size x the executed iterations of its
@@ -792,23 +779,10 @@ class _Batch:
         st = self.st
         n_big = int(self.n_big)
         side = C_void(_side_stream(st.dp.device).cuda_stream) if n_big else None
-        outs = None
-        if self.shard is not None:
-            n, nx, t = self.n, self.pt.nw0 * self.pt.nw1, self.tot
-            outs = [self.alpha[:n * nx], self.beta[:t["y"]], self.mdens[:t["y"]],
-                    self.lnuw[:t["y"]], self.marena[:t["m"]], self.xarena[:t["mem"] * st.bs],
-                    self.mbox[:t["mem"] * 4], self.mstat[:t["mem"] * 4], self.cstat[:n * 8],
-                    self.cstat2[:n * 8], self.lout[:n * nx]]
-            for o in outs:
-                o.zero_()
         _lib.check(_lib.lib().dd_cell_solve2(st.dp.geom, st.state_struct(self.store), self.batch,
                                              _lib.stream_handle(), side, n_big,
                                              self.clu_ids.data_ptr(), self.clu_n_groups,
                                              self.clu_goff, self.clu_gsize, self.clu_gsmem))
-        if outs is not None:
-            # every rank contributes its own cells (zeros elsewhere): exact sum
-            for o in outs:
-                self.shard.all_reduce_sum(o)
 
     def stats(self):
         c1 = self.cstat[:self.n * 8].view(self.n, 8).cpu().numpy()
@@ -863,12 +837,30 @@ class BlendScorer:
         import torch
 
         st, b = self.plan, self.batch
-        th = torch.from_numpy(np.ascontiguousarray(theta_vec, dtype=np.float64)).to(st.dp.device)
-        _lib.check(_lib.lib().dd_blend_energy(st.dp.geom, st.state_struct(b.store), b.batch,
-                                              self.dy.data_ptr(), self.cd.data_ptr(),
-                                              th.data_ptr(), self.ywork.data_ptr(),
-                                              st.partial.data_ptr(), self.out.data_ptr(),
-                                              _lib.stream_handle()))
+        th = np.ascontiguousarray(theta_vec, dtype=np.float64)
+        if b.shard is not None:
+            # slab mode: this rank's cells only; dense sum of theta*dy and the per-cell
+            # pieces are reduced over the slabs, then y = snapshot + sum, KL(y | nu)
+            thd = torch.from_numpy(np.where(b.owned, th, 0.0)).to(st.dp.device)
+            L = _lib.lib()
+            _lib.check(L.dd_blend_parts(st.dp.geom, st.state_struct(b.store), b.batch,
+                                        self.dy.data_ptr(), self.cd.data_ptr(), thd.data_ptr(),
+                                        self.ywork.data_ptr(), st.partial.data_ptr(),
+                                        self.out.data_ptr(), _lib.stream_handle()))
+            ny = st.dp.ny
+            b.shard.all_reduce(self.ywork[:ny])
+            b.shard.all_reduce(self.out[1:4])
+            axpb(self.ywork[:ny], 1.0, self.snapshot[:ny], out=self.ywork[:ny])
+            _lib.check(L.dd_grid_kl(ny, self.ywork.data_ptr(), st.dp.nu.data_ptr(), 1,
+                                    st.partial.data_ptr(), self.out.data_ptr(),
+                                    _lib.stream_handle()))
+        else:
+            thd = torch.from_numpy(th).to(st.dp.device)
+            _lib.check(_lib.lib().dd_blend_energy(st.dp.geom, st.state_struct(b.store), b.batch,
+                                                  self.dy.data_ptr(), self.cd.data_ptr(),
+                                                  thd.data_ptr(), self.ywork.data_ptr(),
+                                                  st.partial.data_ptr(), self.out.data_ptr(),
+                                                  _lib.stream_handle()))
         o = self.out[:4].cpu().numpy()
         self.evaluations += 1
         t = self.base_t + float(o[1])
@@ -973,6 +965,9 @@ def get_weights_opt(old_cells, new_cells, part, scorer: BlendScorer, max_sweeps:
     iterate, greedy, safe} (engine.py:557-588)."""
     ids = list(new_cells)
     k = len(ids)
+    if scorer.batch.shard is not None:
+        raise ValueError("the opt strategy needs per-cell global coordination inside a batch; "
+                         "slab-sharded solves support safe, fast, swift and staggered")
     ones, safe = np.ones(k), np.full(k, 1.0 / k)
     start = ones if scorer.energy_at(ones) <= scorer.energy_at(safe) else safe
     op = _OptState(scorer)
@@ -1089,20 +1084,28 @@ def cell_lse_flops(nw0: int, nw1: int, ny0, ny1):
 def _absorb(stats: IterationStats, batch: _Batch) -> None:
     c1, c2 = batch.stats()
     hist = batch.st.iter_hist.setdefault(batch.pt.label, np.zeros(batch.pt.ncomp))
-    hist[batch.ids] = c2[:, 4]
-    fl = cell_lse_flops(batch.pt.nw0, batch.pt.nw1, batch.ybox[:, 1].astype(np.float64),
-                        batch.ybox[:, 3].astype(np.float64))
+    own = batch.owned
+    hist[batch.ids[own]] = c2[own, 4]
+    c1, c2 = c1[own], c2[own]
+    fl = cell_lse_flops(batch.pt.nw0, batch.pt.nw1, batch.ybox[own, 1].astype(np.float64),
+                        batch.ybox[own, 3].astype(np.float64))
     # roofline work counts executed iterations only (a stagnant cell's loop ends
     # early with the reference-equivalent count reported in c1)
-    stats.cell_flops += float((c2[:, 4] * fl).sum())
-    stats.entry_gap += float(c1[:, 1].sum())
-    stats.balance_fallbacks += int(c1[:, 6].sum())
-    stats.newton_clamped = max(stats.newton_clamped, int(c1[:, 5].max(initial=0)))
-    stats.nu_minus_clamped += int(c1[:, 4].sum())
-    stats.nonconverged_cells += int((c1[:, 3] == 0).sum())
-    stats.balance_target_miss = max(stats.balance_target_miss, float(c1[:, 7].max(initial=0.0)))
-    stats.nu_j_drift_nodes += int(c2[:, 0].sum())
-    stats.cell_iterations += int(c1[:, 2].sum())
+    sums = np.array([(c2[:, 4] * fl).sum(), c1[:, 1].sum(), c1[:, 6].sum(), c1[:, 4].sum(),
+                     (c1[:, 3] == 0).sum(), c2[:, 0].sum(), c1[:, 2].sum()], dtype=np.float64)
+    maxs = np.array([c1[:, 5].max(initial=0), c1[:, 7].max(initial=0.0)], dtype=np.float64)
+    if batch.shard is not None:
+        sums = batch.shard.reduce_np(sums, "sum", batch.st.dp.device)
+        maxs = batch.shard.reduce_np(maxs, "max", batch.st.dp.device)
+    stats.cell_flops += float(sums[0])
+    stats.entry_gap += float(sums[1])
+    stats.balance_fallbacks += int(sums[2])
+    stats.nu_minus_clamped += int(sums[3])
+    stats.nonconverged_cells += int(sums[4])
+    stats.nu_j_drift_nodes += int(sums[5])
+    stats.cell_iterations += int(sums[6])
+    stats.newton_clamped = max(stats.newton_clamped, int(maxs[0]))
+    stats.balance_target_miss = max(stats.balance_target_miss, float(maxs[1]))
 
 
 def _alpha_grid(plan: PlanState, stats: IterationStats):
@@ -1121,6 +1124,8 @@ def iteration_sequential(plan: PlanState, part: CompositePartition,
                          config: EngineConfig = EngineConfig(),
                          stats: IterationStats | None = None) -> PlanState:
     """Cell-by-cell pass on a running Y-marginal (engine.py:799-836)."""
+    if _SHARD is not None and _SHARD.world > 1:
+        raise ValueError("the sequential sweep is inherently serial; run it on one rank")
     stats = stats if stats is not None else IterationStats()
     cfg = config.cell_config()
     pt = _tables(part)
@@ -1156,6 +1161,13 @@ def iteration_parallel(plan: PlanState, part: CompositePartition, strategy: Stra
     pt = _tables(part)
     batches = pt.batches if strategy.kind == "staggered" else [np.arange(pt.ncomp)]
     ag = _alpha_grid(plan, stats)
+    shard = _SHARD if (_SHARD is not None and _SHARD.world > 1) else None
+    if shard is not None:
+        # this partition's slab ownership; the boundary block row's basic cells
+        # (the halo) arrive from the neighbour that updated them last
+        comp_owner, basic_owner = _slab_layout(plan, pt)
+        shard.halo_exchange(plan, basic_owner)
+        plan.comp_owner[pt.label] = comp_owner
     actions = []
     for batch in batches:
         t0 = time.perf_counter()
@@ -1202,12 +1214,17 @@ def iteration_parallel(plan: PlanState, part: CompositePartition, strategy: Stra
         stats.score_time += time.perf_counter() - t0
         t0 = time.perf_counter()
         e = bt.commit(theta, ag, None)
-        stats.x_err += float(e[:, 0].sum())
-        stats.y_err += float(e[:, 1].sum())
-        added = float(e[:, 2].sum())
+        es = e[:, :3].sum(axis=0)
+        if shard is not None:
+            es = shard.reduce_np(es, "sum", plan.dp.device)
+        stats.x_err += float(es[0])
+        stats.y_err += float(es[1])
+        added = float(es[2])
         plan.truncated_mass += added
         stats.truncated_mass += added
         stats.commit_time += time.perf_counter() - t0
+    if shard is not None:
+        shard.all_reduce(ag)   # stitched alpha: each rank wrote its own composites' blocks
     if len(actions) == 1:
         stats.action = actions[0]
     else:
@@ -1279,6 +1296,8 @@ def domdec_solve(problem: TransportProblem, partitions: Decomposition,
         if last_gap / lam <= config.delta * mu_total:
             converged = True
             break
+    if _SHARD is not None and _SHARD.world > 1:
+        _SHARD.replicate(state)     # the whole plan current on every rank again
     timings["total"] = time.perf_counter() - t_all
     diag["truncated_mass"] = state.truncated_mass
     report = SolveReport(converged=converged, iterations=len(trace), final_score=_score_dict(sb),
