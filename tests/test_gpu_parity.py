@@ -8,7 +8,7 @@ the reference array), primal-dual objective within 1e-10 relative.
 import numpy as np
 import pytest
 
-from _golden import ENGINE_CASES, dense, load, ref_duals, ref_marginals, rel_err
+from _golden import BASELINE_CASES, ENGINE_CASES, dense, load, ref_duals, ref_marginals, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -16,7 +16,7 @@ MARG_TOL = 1e-9
 DUAL_TOL = 1e-9
 OBJ_TOL = 1e-10
 
-DEVICE_CASES = ENGINE_CASES
+DEVICE_CASES = ENGINE_CASES + BASELINE_CASES
 
 # every execution path of the cell solve: shared-memory CTA per cell (default),
 # the global-memory workspace (single CTA), thread-block clusters of 2 and 4 CTAs

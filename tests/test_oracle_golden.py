@@ -76,3 +76,18 @@ def test_engine_matches_reference(name):
     np.testing.assert_allclose(st.transport, g["transport"], rtol=1e-9, atol=1e-18)
     np.testing.assert_allclose(st.kl, g["kl"], rtol=1e-9, atol=1e-15)
     assert rep["rel_pd_gap"] == pytest.approx(scalar(g, "rel_pd_gap"), rel=1e-6, abs=1e-12)
+
+
+def test_pr1_64_fixture_is_baseline_configs0():
+    """The configs[0] golden fixture was produced by the reference on exactly the
+    bench/problem generator's input (64^2, 3 Gaussians + 1e-4 floor, masses 1.0/1.3,
+    lam = 1, eps = 2h^2, 4x4 cells, 30 sweeps)."""
+    from paper_2410_08859_b200.problems import config_problem_arrays
+
+    g = load("pr1_64")
+    mu, nu, dx, org, cfg = config_problem_arrays(0, seed=0)
+    assert np.array_equal(g["mu"], mu) and np.array_equal(g["nu"], nu)
+    assert float(g["dx"]) == dx and float(g["lam"]) == cfg["lam"] == 1.0
+    assert float(g["eps"]) == 2 * dx * dx and int(g["s"]) == cfg["cell"] == 4
+    assert int(g["iterations"]) == int(g["max_iters"]) == cfg["domdec_sweeps"] == 30
+    assert abs(mu.sum() - 1.0) < 1e-12 and abs(nu.sum() - 1.3) < 1e-12
