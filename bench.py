@@ -67,6 +67,8 @@ def parse():
                     choices=sorted(CONFIGS))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=1, help="run the CPU baseline sample")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp32: north_star fp32 mode (cell sweeps in fp32, 1e-4 parity)")
     return ap.parse_args()
 
 
@@ -146,12 +148,16 @@ def flush_l2(buf):
     buf.fill_(1.0)
 
 
+PRECISION = "fp64"
+
+
 def run_solve(prob, cfg, eps_start, levels=None):
-    from paper_2410_08859_b200.engine import EngineConfig, StrategyConfig
+    from paper_2410_08859_b200.engine import CellSolverConfig, EngineConfig, StrategyConfig
     from paper_2410_08859_b200.multiscale import multiscale_solve
 
     return multiscale_solve(prob, cfg["cell"], cfg["coarsest"], eps_start,
-                            strategy=StrategyConfig("staggered"), config=EngineConfig(),
+                            strategy=StrategyConfig("staggered"),
+                            config=EngineConfig(cell=CellSolverConfig(precision=PRECISION)),
                             levels=levels)
 
 
@@ -205,6 +211,9 @@ def main():
         # DD_DIST_BACKEND=gloo: functional multi-rank runs on fewer GPUs than ranks
         backend = os.environ.get("DD_DIST_BACKEND") or ("nccl" if args.impl == "ours" else "gloo")
         dist.init_process_group(backend)
+    global PRECISION
+    PRECISION = args.precision
+    dtype = "f64" if args.precision == "fp64" else "f32 cell sweeps / f64 state"
     prob, cfg, eps_start = problem(args.config, args.seed)
     config_desc = {"workload": f"{args.config}: BASELINE configs[{CONFIGS[args.config]}] "
                                f"{prob.mu.grid.dims[0]}x{prob.mu.grid.dims[1]} multiscale "
@@ -219,7 +228,7 @@ def main():
                                    "block-row slab; NCCL all-reduce of the Y snapshot and blend "
                                    "sums per batch, halo exchange of the boundary block row "
                                    "at each A/B switch)") if world > 1 else "1 GPU",
-                   "seed": args.seed}
+                   "seed": args.seed, "precision": args.precision}
 
     if args.impl == "reference":
         if rank != 0:
@@ -237,7 +246,7 @@ def main():
         line = {"metric": "converged UOT domdec solve time (s)", "value": t, "unit": "s",
                 "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": 1,
                 "ms_per_step": t * 1e3, "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": config_desc,
                 "cpu_baseline": {"value": t, "unit": "s", "cores": cores, "kind": "port",
                                  "sample": sample},
@@ -343,7 +352,7 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": t_dev * 1e3, "higher_is_better": False,
                 "scaling": "strong" if world > 1 else "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_desc,
+                "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config_desc,
                 "max_step_s": t_max_step,
                 "converged": bool(rep.converged), "rel_pd_gap": rep.rel_pd_gap,
                 "final_total": rep.final_score.get("total"),

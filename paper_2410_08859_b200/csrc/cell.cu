@@ -419,6 +419,142 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     }
 }
 
+// ---- fp32 mode of the fast sweeps ----------------------------------------------
+// The same two factorised contractions with the kernel tables, shifted weights and
+// stage intermediates in fp32 (tables rounded from the fp64 values, weights by
+// __expf of the fp64-formed shifted argument, fmaf contractions, __logf of the
+// sum added to the fp64 shift).  Potentials, shifts, the Newton Y-step, the gap
+// test and the epilogue stay fp64.  An output whose shifted fp32 sum is below
+// kTinyF may have lost terms to fp32 underflow (< 1.2e-38, so dropped terms are
+// < 1e-5 relative of such a sum for windows up to 1e4 nodes); the whole sweep is
+// then redone by the fp64 stage-wise path.  north_star fp32 mode: 1e-4 relative.
+constexpr float kTinyF = 1e-30f;
+
+__device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                               double* out, SweepScratch sc) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    float* wyf = reinterpret_cast<float*>(w.wy);
+    const float* K1f = reinterpret_cast<const float*>(w.K1y);
+    const float* K0f = reinterpret_cast<const float*>(w.K0y);
+    float* T = reinterpret_cast<float*>(w.mid);   // [ny0][nw1]
+    double lmax = kNegInf;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const int y0 = y / ny1;
+        const double bv = w.beta[y] / eps + w.lnu[y] + (w.c0[y0] + w.c1[y - y0 * ny1]);
+        w.ty[y] = bv;
+        lmax = fmax(lmax, bv);
+    }
+    if (threadIdx.x == 0) *sc.flag = 0;
+    double B = block_max1(lmax, sc.redm, *sc.par);
+    if (!isfinite(B)) B = 0.0;
+    for (int y = threadIdx.x; y < ny; y += DD_NT) wyf[y] = __expf((float)(w.ty[y] - B));
+    __syncthreads();
+    *sc.par ^= 1;
+    // fp32: 32 words per bank cycle; rotate rows whose stride shares banks
+    const int low = ny1 & -ny1;
+    const bool rotate = ny1 > 0 && (low < 32 ? low : 32) * (nw1 < 32 ? nw1 : 32) > 32;
+    for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
+        const int y0 = o / nw1, x1 = o - y0 * nw1;
+        const float* tr = wyf + (int64_t)y0 * ny1;
+        const float* kr = K1f + (int64_t)x1 * ny1;
+        float s0 = 0.f, s1 = 0.f;
+        int k = rotate ? x1 % ny1 : 0;
+        for (int j = 0; j + 1 < ny1; j += 2) {
+            const int k1 = k + 1 == ny1 ? 0 : k + 1;
+            s0 = fmaf(tr[k], kr[k], s0);
+            s1 = fmaf(tr[k1], kr[k1], s1);
+            k = k1 + 1 == ny1 ? 0 : k1 + 1;
+        }
+        if (ny1 & 1) s0 = fmaf(tr[k], kr[k], s0);
+        T[o] = s0 + s1;
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int o = threadIdx.x; o < nx; o += DD_NT) {
+        const int x0 = o / nw1, x1 = o - x0 * nw1;
+        const float* kr = K0f + (int64_t)x0 * ny0;
+        float s0 = 0.f, s1 = 0.f;
+        int k = 0;
+        for (; k + 1 < ny0; k += 2) {
+            s0 = fmaf(kr[k], T[(int64_t)k * nw1 + x1], s0);
+            s1 = fmaf(kr[k + 1], T[(int64_t)(k + 1) * nw1 + x1], s1);
+        }
+        if (k < ny0) s0 = fmaf(kr[k], T[(int64_t)k * nw1 + x1], s0);
+        const float sm = s0 + s1;
+        if (sm >= kTinyF) out[o] = (double)__logf(sm) + B;
+        else ++bad;
+    }
+    if (bad) *sc.flag = 1;
+    __syncthreads();
+    if (*sc.flag) cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+}
+
+__device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                               double ratio, double* out, SweepScratch sc) {
+    const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    float* wxf = reinterpret_cast<float*>(w.wx);
+    const float* K1f = reinterpret_cast<const float*>(w.K1y);
+    const float* K0f = reinterpret_cast<const float*>(w.K0y);
+    float* T = reinterpret_cast<float*>(w.mid);   // [nw0][ny1]
+    double lmax = kNegInf;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) {
+        if (ratio != 0.0) w.alpha[x] = -ratio * w.L[x];
+        const double av = w.alpha[x] / eps + w.lmu[x];
+        w.tx[x] = av;
+        lmax = fmax(lmax, av);
+    }
+    if (threadIdx.x == 0) *sc.flag = 0;
+    double A = block_max1(lmax, sc.redm, *sc.par);
+    if (!isfinite(A)) A = 0.0;
+    for (int x = threadIdx.x; x < nx; x += DD_NT) wxf[x] = __expf((float)(w.tx[x] - A));
+    __syncthreads();
+    *sc.par ^= 1;
+    for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
+        const int x0 = o / ny1, y1 = o - x0 * ny1;
+        const float* tr = wxf + (int64_t)x0 * nw1;
+        float s0 = 0.f, s1 = 0.f;
+        int k = 0;
+        for (; k + 1 < nw1; k += 2) {
+            s0 = fmaf(tr[k], K1f[(int64_t)k * ny1 + y1], s0);
+            s1 = fmaf(tr[k + 1], K1f[(int64_t)(k + 1) * ny1 + y1], s1);
+        }
+        if (k < nw1) s0 = fmaf(tr[k], K1f[(int64_t)k * ny1 + y1], s0);
+        T[o] = s0 + s1;
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int o = threadIdx.x; o < ny; o += DD_NT) {
+        const int y0 = o / ny1, y1 = o - y0 * ny1;
+        float s0 = 0.f, s1 = 0.f;
+        int k = 0;
+        for (; k + 1 < nw0; k += 2) {
+            s0 = fmaf(K0f[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+            s1 = fmaf(K0f[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
+        }
+        if (k < nw0) s0 = fmaf(K0f[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+        const float sm = s0 + s1;
+        if (sm >= kTinyF) out[o] = (double)__logf(sm) + A + (w.c0[y0] + w.c1[y1]);
+        else ++bad;
+    }
+    if (bad) *sc.flag = 1;
+    __syncthreads();
+    if (*sc.flag) cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
+}
+
+template <bool F32>
+__device__ __forceinline__ void sweep_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                                        double* out, SweepScratch sc) {
+    if constexpr (F32) cell_lse_x_f32(w, c, nw0, nw1, eps, out, sc);
+    else cell_lse_x(w, c, nw0, nw1, eps, out, sc);
+}
+
+template <bool F32>
+__device__ __forceinline__ void sweep_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                                        double ratio, double* out, SweepScratch sc) {
+    if constexpr (F32) cell_lse_y_f32(w, c, nw0, nw1, eps, ratio, out, sc);
+    else cell_lse_y(w, c, nw0, nw1, eps, ratio, out, sc);
+}
+
 // Value of a boxed marginal at absolute node (r, q); zero outside.
 __device__ __forceinline__ double boxed_at(const int32_t* box, const double* vals, int r, int q) {
     const int o0 = box[0], e0 = box[1], o1 = box[2], e1 = box[3];
@@ -849,7 +985,7 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
 // kPass 1: the remaining (large-window) cells, workspace in the global arena,
 //          compiled as a separate function so it can run with a max-L1
 //          carveout on a second stream, concurrently with pass 0.
-template <int kPass>
+template <int kPass, bool kF32>
 __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
     extern __shared__ double smem[];
@@ -971,11 +1107,15 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     __syncthreads();
     for (int o = tid; o < nw0 * ny0; o += DD_NT) {
         const int x0 = o / ny0, y0 = o - x0 * ny0;
-        w.K0y[o] = exp(negsq(w.xc0[x0], w.yc0[y0], eps) - w.c0[y0]);
+        const double kv = exp(negsq(w.xc0[x0], w.yc0[y0], eps) - w.c0[y0]);
+        if constexpr (kF32) reinterpret_cast<float*>(w.K0y)[o] = (float)kv;
+        else w.K0y[o] = kv;
     }
     for (int o = tid; o < nw1 * ny1; o += DD_NT) {
         const int x1 = o / ny1, y1 = o - x1 * ny1;
-        w.K1y[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps) - w.c1[y1]);
+        const double kv = exp(negsq(w.xc1[x1], w.yc1[y1], eps) - w.c1[y1]);
+        if constexpr (kF32) reinterpret_cast<float*>(w.K1y)[o] = (float)kv;
+        else w.K1y[o] = kv;
     }
     __syncthreads();
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
@@ -1009,7 +1149,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         int par = 0;
         stag_k = 0;
         for (int k = 1; k <= b.max_iters; ++k) {
-            cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
+            sweep_x<kF32>(w, cw, nw0, nw1, eps, w.L, sc);
             if (k >= 2) {
                 double part = 0.0;
                 for (int x = tid; x < nx; x += DD_NT) {
@@ -1028,7 +1168,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
                 if (gap / lam <= thr) { converged = true; break; }
             }
             // alpha = -ratio L is fused into the Y sweep's row preparation
-            cell_lse_y(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
+            sweep_y<kF32>(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
             int ndeg = 0;
             bool moved = false;
             for (int y = tid; y < ny; y += DD_NT) {
@@ -1067,7 +1207,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         if (!converged) {
             // cap reached: final X sweep and gap for the last (post-Y-step) pair
             // (cells.py:341-348)
-            cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc);
+            sweep_x<kF32>(w, cw, nw0, nw1, eps, w.L, sc);
             double part = 0.0;
             for (int x = tid; x < nx; x += DD_NT) {
                 const double mu = w.mu[x];
@@ -1906,19 +2046,26 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel<0>);
+        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel<0, false>);
         if (e != cudaSuccess) return dd_set_error(e);
         const int avail = optin - (int)fa.sharedSizeBytes;
         if (smem > avail) return dd_set_error(cudaErrorInvalidValue);
-        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0>,
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
+        if (e != cudaSuccess) return dd_set_error(e);
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
         if (e != cudaSuccess) return dd_set_error(e);
         configured = avail;
     }
     if (!big_configured) {
-        cudaError_t e = cudaFuncSetAttribute(dd::cell_solve_kernel<1>,
+        cudaError_t e = cudaFuncSetAttribute(dd::cell_solve_kernel<1, false>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxL1);
+        if (e != cudaSuccess) return dd_set_error(e);
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<1, true>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxL1);
         if (e != cudaSuccess) return dd_set_error(e);
         big_configured = true;
     }
@@ -1926,6 +2073,11 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
         const int rc = cluster_configure(gsmem[k]);
         if (rc) return rc;
     }
+    const bool f32 = b->precision == 1;
+    auto launch_small = [&]() {
+        if (f32) dd::cell_solve_kernel<0, true><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+        else dd::cell_solve_kernel<0, false><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+    };
     auto launch_big = [&](cudaStream_t sb) -> cudaError_t {
         for (int k = 0; k < n_groups; ++k) {
             const int ncl = goff[k + 1] - goff[k];
@@ -1946,7 +2098,8 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
                                                clu_ids + goff[k]);
             if (e != cudaSuccess) return e;
         }
-        dd::cell_solve_kernel<1><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
+        if (f32) dd::cell_solve_kernel<1, true><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
+        else dd::cell_solve_kernel<1, false><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
         return cudaGetLastError();
     };
     if (n_big > 0 && st_big != nullptr && st_big != st) {
@@ -1961,14 +2114,14 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
         cudaStreamWaitEvent(st_big, ev_fork, 0);
         cudaError_t e = launch_big(st_big);
         if (e != cudaSuccess) return dd_set_error(e);
-        if (b->smem_mode) dd::cell_solve_kernel<0><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+        if (b->smem_mode) launch_small();
         e = cudaGetLastError();
         if (e != cudaSuccess) return dd_set_error(e);
         cudaEventRecord(ev_join, st_big);
         cudaStreamWaitEvent(st, ev_join, 0);
         return dd_set_error(cudaGetLastError());
     }
-    if (b->smem_mode) dd::cell_solve_kernel<0><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+    if (b->smem_mode) launch_small();
     if (n_big > 0) {
         cudaError_t e = launch_big(st);
         if (e != cudaSuccess) return dd_set_error(e);

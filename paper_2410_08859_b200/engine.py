@@ -157,6 +157,13 @@ class CellSolverConfig:
     newton_max_iters: int = 100
     trunc_threshold: float = 1e-15
     chunk_entries: int = 4_000_000  # kept for API parity; batches are not chunked on device
+    # "fp64" (reference arithmetic) or "fp32" (north_star fp32 mode: the cell sweeps'
+    # tables, weights and contractions in fp32; potentials, Newton, gap, epilogue fp64)
+    precision: str = "fp64"
+
+    def __post_init__(self):
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError(f"precision must be 'fp64' or 'fp32', not {self.precision!r}")
 
 
 @dataclass(frozen=True)
@@ -770,7 +777,8 @@ class _Batch:
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
             lout=self.lout.data_ptr(), skip_stagnant=1 if mode.skip_stagnant else 0,
-            order=self.order_d.data_ptr() if n else None)
+            order=self.order_d.data_ptr() if n else None,
+            precision=1 if cfg.precision == "fp32" else 0)
         self.cfg = cfg
 
     def solve(self):

@@ -67,8 +67,10 @@ BASELINE_CONFIGS = [
          lam=0.5, eps_final_h2=2.0, eps_start_h2=64.0, coarsest=32, cell=4),
     dict(name="ms_1024", n=1024, mu=MixtureSpec(8, 1e-5, 1.0), nu=MixtureSpec(8, 1e-5, 1.5),
          lam=1.0, eps_final_h2=2.0, eps_start_h2=256.0, coarsest=64, cell=8),
+    # configs[3] names only the final eps (2h^2) and the pyramid 128^2 -> 2048^2; the
+    # ladder starts at the coarsest layer's 2 dx^2 = 2 (16 h)^2 = 512 h^2 (SPEC eps_schedule)
     dict(name="ms_2048", n=2048, mu=MixtureSpec(16, 1e-5, 1.0), nu=MixtureSpec(16, 1e-5, 0.7),
-         lam=2.0, eps_final_h2=2.0, eps_start_h2=None, coarsest=128, cell=8),
+         lam=2.0, eps_final_h2=2.0, eps_start_h2=512.0, coarsest=128, cell=8),
 ]
 
 

@@ -65,7 +65,9 @@ def _capture_1024_stage():
 
 MODES = {"default": {}, "global_ws": {"force_global_ws": True}, "cluster4": {"force_cluster": 4},
          # 48 KB per CTA: the size rule sends the larger windows to 2..16-CTA clusters
-         "small_smem": {"smem_budget": 48 * 1024}}
+         "small_smem": {"smem_budget": 48 * 1024},
+         # north_star fp32 mode against the fp64 oracle at 1e-4
+         "fp32": {}}
 
 
 @pytest.mark.parametrize("mode", sorted(MODES))
@@ -82,7 +84,9 @@ def test_1024_batch_cells_match_oracle(mode):
     pt = _tables(part)
     ids = np.asarray(pt.batches[0])
     delta = 2e-5 * 0.25
-    ccfg = CellSolverConfig(delta=delta, max_iters=CAP)
+    ccfg = CellSolverConfig(delta=delta, max_iters=CAP,
+                            precision="fp32" if mode == "fp32" else "fp64")
+    tol = 1e-4 if mode == "fp32" else 1e-9
     prev = set_exec_mode(**MODES[mode])
     try:
         snap = st.assemble_device()
@@ -132,11 +136,13 @@ def test_1024_batch_cells_match_oracle(mode):
         j = int(ids[k])
         probs = prepare(ctx, opart, [j], ost, snap_h)
         sol = solve_batch(probs, ctx, ocfg)[0]
-        assert sol.iterations == iters[k], (j, sol.iterations, iters[k])
-        assert bool(sol.converged) == bool(c1[k, 3]), j
+        if mode != "fp32":
+            assert sol.iterations == iters[k], (j, sol.iterations, iters[k])
+            assert bool(sol.converged) == bool(c1[k, 3]), j
         d = gd[(part.label, j)]
-        assert rel_err(d.alpha, sol.alpha) < 1e-9, j
-        assert rel_err(d.beta, sol.beta) < 1e-9, j
+        assert rel_err(d.alpha, sol.alpha) < tol, j
+        if mode != "fp32" or d.beta.shape == sol.beta.shape:
+            assert rel_err(d.beta, sol.beta) < tol, j
         for q, i in enumerate(sol.members):
             ob = tuple(int(x) for x in sol.new_box[q])
             g = nu_i[i]
@@ -144,10 +150,20 @@ def test_1024_batch_cells_match_oracle(mode):
                 assert g.is_empty
                 continue
             gb = tuple(c for ax in g.box for c in ax)
+            if mode == "fp32":
+                # truncation at 1e-15 may keep or drop an edge row: compare on the union
+                shp = (1, nu.shape[1]) if nu.ndim == 1 else nu.shape
+                a = np.zeros(shp)
+                a[gb[0]:gb[0] + gb[1], gb[2]:gb[2] + gb[3]] = g.values.reshape(gb[1], gb[3])
+                o = np.zeros(shp)
+                o[ob[0]:ob[0] + ob[1], ob[2]:ob[2] + ob[3]] = sol.new_vals[q]
+                assert rel_err(a, o) < tol, (j, i)
+                assert rel_err(xm[i], sol.x_marg[q]) < tol, (j, i)
+                continue
             assert gb == ob, (j, i)
-            assert rel_err(g.values, sol.new_vals[q]) < 1e-9, (j, i)
-            assert rel_err(xm[i], sol.x_marg[q]) < 1e-9, (j, i)
-        np.testing.assert_allclose(st.transport[sol.members], sol.transport, rtol=1e-9, atol=1e-18)
-        np.testing.assert_allclose(st.kl[sol.members], sol.kl, rtol=1e-9, atol=1e-15)
+            assert rel_err(g.values, sol.new_vals[q]) < tol, (j, i)
+            assert rel_err(xm[i], sol.x_marg[q]) < tol, (j, i)
+        np.testing.assert_allclose(st.transport[sol.members], sol.transport, rtol=tol, atol=1e-18)
+        np.testing.assert_allclose(st.kl[sol.members], sol.kl, rtol=tol, atol=1e-15)
     print(f"oracle time for {len(pick)} cells: {time.perf_counter() - t0:.1f}s; "
           f"windows {[int(ny[k]) for k in pick]}, iterations {[int(iters[k]) for k in pick]}")
