@@ -422,8 +422,8 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
 // ---- fp32 mode of the fast sweeps ----------------------------------------------
 // The same two factorised contractions with the kernel tables, shifted weights and
 // stage intermediates in fp32 (tables rounded from the fp64 values, weights by
-// __expf of the fp64-formed shifted argument, fmaf contractions, __logf of the
-// sum added to the fp64 shift).  Potentials, shifts, the Newton Y-step, the gap
+// expf of the fp64-formed shifted argument, fmaf contractions, logf of the sum
+// added to the fp64 shift).  Potentials, shifts, the Newton Y-step, the gap
 // test and the epilogue stay fp64.  An output whose shifted fp32 sum is below
 // kTinyF may have lost terms to fp32 underflow (< 1.2e-38, so dropped terms are
 // < 1e-5 relative of such a sum for windows up to 1e4 nodes); the whole sweep is
@@ -447,7 +447,7 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     if (threadIdx.x == 0) *sc.flag = 0;
     double B = block_max1(lmax, sc.redm, *sc.par);
     if (!isfinite(B)) B = 0.0;
-    for (int y = threadIdx.x; y < ny; y += DD_NT) wyf[y] = __expf((float)(w.ty[y] - B));
+    for (int y = threadIdx.x; y < ny; y += DD_NT) wyf[y] = expf((float)(w.ty[y] - B));
     __syncthreads();
     *sc.par ^= 1;
     // fp32: 32 words per bank cycle; rotate rows whose stride shares banks
@@ -481,7 +481,7 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
         }
         if (k < ny0) s0 = fmaf(kr[k], T[(int64_t)k * nw1 + x1], s0);
         const float sm = s0 + s1;
-        if (sm >= kTinyF) out[o] = (double)__logf(sm) + B;
+        if (sm >= kTinyF) out[o] = (double)logf(sm) + B;
         else ++bad;
     }
     if (bad) *sc.flag = 1;
@@ -506,7 +506,7 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     if (threadIdx.x == 0) *sc.flag = 0;
     double A = block_max1(lmax, sc.redm, *sc.par);
     if (!isfinite(A)) A = 0.0;
-    for (int x = threadIdx.x; x < nx; x += DD_NT) wxf[x] = __expf((float)(w.tx[x] - A));
+    for (int x = threadIdx.x; x < nx; x += DD_NT) wxf[x] = expf((float)(w.tx[x] - A));
     __syncthreads();
     *sc.par ^= 1;
     for (int o = threadIdx.x; o < nw0 * ny1; o += DD_NT) {
@@ -533,7 +533,7 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
         }
         if (k < nw0) s0 = fmaf(K0f[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
         const float sm = s0 + s1;
-        if (sm >= kTinyF) out[o] = (double)__logf(sm) + A + (w.c0[y0] + w.c1[y1]);
+        if (sm >= kTinyF) out[o] = (double)logf(sm) + A + (w.c0[y0] + w.c1[y1]);
         else ++bad;
     }
     if (bad) *sc.flag = 1;

@@ -234,8 +234,7 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         //   |g''| step^2 / (2 g') <= (1 - sig) step^2 / (2 eps)   (g'' = sig(1-sig)/eps^2),
         // so once step^2/eps <= 2^-52 |nb| it is below one ulp of nb and the confirming
         // evaluation the reference loop spends to observe that is skipped.  The result
-        // differs from running it by at most that ulp (well inside the 1e-9 parity bar);
-        // build with -DDD_NEWTON_CONFIRM to evaluate it anyway.
+        // differs from running it by at most that ulp (well inside the 1e-9 parity bar).
         if (!safeguarded && step * step * inv_eps <= 2.220446049250313e-16 * fabs(nb)) {
             b = nb;
             break;
@@ -249,72 +248,6 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
     return b;
 }
 
-// Two independent nodes advanced in lockstep (same per-node iterates as
-// newton_node): gives the scheduler two transcendental chains per thread.
-struct NewtonState {
-    double z, lm, b, lo, hi;
-    int it;
-    bool done;
-};
-
-__device__ __forceinline__ void newton_init(NewtonState& s, double z, double m, bool has_m,
-                                            double beta0, double eps, double lam, double* out,
-                                            int* deg) {
-    const double ratio = eps * lam / (eps + lam);
-    const bool fz = z > kNegInf;
-    s.done = true;
-    s.it = 0;
-    if (!has_m || !(m > 0)) {
-        if (fz) { *out = -ratio * z; }
-        else { *deg += 1; *out = lam * kDegenerateBetaScale; }
-        return;
-    }
-    if (!fz) { *out = -lam * log(m); return; }
-    s.z = z;
-    s.lm = log(m);
-    const double b1 = -lam * logaddexp(s.lm, z);
-    const double b2 = -ratio * z;
-    s.lo = fmin(b1, b2) - lam;
-    s.hi = fmax(b1, b2) + lam;
-    s.b = fmin(fmax(beta0, s.lo), s.hi);
-    s.done = false;
-}
-
-__device__ __forceinline__ void newton_step(NewtonState& s, double inv_eps, double inv_lam,
-                                            double tol, int max_iters, double* out,
-                                            long long* steps) {
-    const double b = s.b;
-    const double w = b * inv_eps + s.z;
-    double la, sig;
-    const double t = w - s.lm;
-    if (t > 0) {
-        const double e = exp(-t);
-        la = w + log1p(e);
-        sig = 1.0 / (1.0 + e);
-    } else if (t <= 0) {
-        const double e = exp(t);
-        la = (t == 0 ? w + 0.693147180559945309417232121458176568 : s.lm + log1p(e));
-        sig = e / (1.0 + e);
-    } else {
-        la = t;
-        sig = t;
-    }
-    if (s.done) return;
-    if (steps) ++*steps;
-    const double g = la + b * inv_lam;
-    const double gp = sig * inv_eps + inv_lam;
-    const double step = g / gp;
-    const bool active = (fabs(g) > tol) || (fabs(step) > 4e-16 * (1.0 + fabs(b)));
-    if (!active) { s.done = true; *out = b; return; }
-    double nb = b - step;
-    if (!((nb > s.lo) && (nb < s.hi))) {
-        if (g > 0) s.hi = fmin(s.hi, b);
-        else s.lo = fmax(s.lo, b);
-        if ((nb <= s.lo) || (nb >= s.hi)) nb = 0.5 * (s.lo + s.hi);
-    }
-    if (nb == b || ++s.it >= max_iters) { s.done = true; *out = (nb == b) ? b : nb; return; }
-    s.b = nb;
-}
 
 }  // namespace dd
 
