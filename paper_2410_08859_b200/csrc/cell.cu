@@ -680,6 +680,7 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
     const int nyl = rows * ny1;
     const double* lnu = b.lnuw + ybase;
     const double* mg = b.mdens + ybase;
+    const double* lmg = b.lmw + ybase;
 
     // cluster helpers (fixed rank order => deterministic)
     int spar = 0;
@@ -758,6 +759,7 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
         if (diff < -1e-12 * fmax(pw, cs)) ++nclamp;
         const double mm = fmax(diff, 0.0) / nu;
         b.mdens[ybase + yl] = mm;
+        b.lmw[ybase + yl] = log(mm);
         if (mm != 0.0) anym = 1;
         beta[yl] = has_dual ? boxed_at(dbox, dbeta, rr, q) : 0.0;
     }
@@ -919,7 +921,8 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
             int dg = 0;
             const double ob = beta[yl];
             const double nb = newton_node(ty[yl], mg[yl], has_m, ob, eps, lam, b.newton_tol,
-                                          b.newton_max_iters, &dg, &newton_steps);
+                                          b.newton_max_iters, &dg, &newton_steps, nullptr,
+                                          lmg[yl]);
             moved |= (nb != ob) ? 1 : 0;
             beta[yl] = nb;
             ndeg += dg;
@@ -1071,15 +1074,14 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
         if (diff < -1e-12 * fmax(pw, cs)) ++nclamp;
         const double mm = fmax(diff, 0.0) / nu;
         b.mdens[yoff + y] = mm;
+        // log m, taken once per solve for the Newton Y-step of every iteration
+        b.lmw[yoff + y] = log(mm);
         if (mm != 0.0) anym = 1;
         w.beta[y] = epi ? b.beta[yoff + y] : (has_dual ? boxed_at(dbox, dbeta, r, q) : 0.0);
     }
     int n_clamped = (int)block_sum((double)nclamp, red);
     const bool has_m = block_max_i(anym, redi) != 0;
-    // log m of this thread's first two Y nodes: the same nodes every Sinkhorn
-    // iteration, so the Newton step's log is taken once per solve for them
-    const double lmc0 = (tid < ny) ? log(w.m[tid]) : 0.0;
-    const double lmc1 = (tid + DD_NT < ny) ? log(w.m[tid + DD_NT]) : 0.0;
+    const double* lmw = b.lmw + yoff;
 
     // per-axis kernel tables K_a = exp(-(x_a - y_a)^2 / eps) (entries may underflow;
     // the sweeps recompute affected outputs exactly)
@@ -1175,7 +1177,7 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
                 int dg = 0;
                 {
                     const double ob = w.beta[y];
-                    const double lmv = y == tid ? lmc0 : (y == tid + DD_NT ? lmc1 : __builtin_nan(""));
+                    const double lmv = lmw[y];
                     const double nb = newton_node(w.ty[y], w.m[y], has_m, ob, eps, lam,
                                                   b.newton_tol, b.newton_max_iters, &dg,
                                                   &newton_steps, nullptr, lmv);

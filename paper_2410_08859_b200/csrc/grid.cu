@@ -494,6 +494,8 @@ __global__ void __launch_bounds__(DD_NT) cut_plan_kernel(dd_geom g, dd_state s,
     __syncthreads();
     const int nxn = n_sh;
     const int64_t ny = (int64_t)g.ny0 * g.ny1;
+    // num < -750 eps  =>  num / eps < -749.9...  =>  exp(num / eps) == 0 exactly
+    const double zero_cut = -750.0 * eps;
     double xacc[64];
     for (int k = 0; k < 64; ++k) xacc[k] = 0.0;
     double mass = 0.0, tr = 0.0, klp = 0.0, rem = 0.0;
@@ -508,7 +510,11 @@ __global__ void __launch_bounds__(DD_NT) cut_plan_kernel(dd_geom g, dd_state s,
         for (int k = 0; k < nxn; ++k) {
             const double d0 = xs_c0[k] - yc0, d1 = xs_c1[k] - yc1;
             const double cost = d0 * d0 + d1 * d1;
-            const double lr = (xs_a[k] + bt - cost) / eps;
+            const double num = xs_a[k] + bt - cost;
+            // exp(num/eps) is exactly 0 in double below -745.14: such terms add
+            // exact zeros to every sum, so the division and exp are skipped
+            if (num < zero_cut) continue;
+            const double lr = num / eps;
             const double blk = exp(lr) * xs_mu[k] * nu;
             col += blk;
             tr += cost * blk;
@@ -567,7 +573,9 @@ __global__ void __launch_bounds__(DD_NT) cut_plan_kernel(dd_geom g, dd_state s,
         for (int k = 0; k < nxn; ++k) {
             const double d0 = xs_c0[k] - yc0, d1 = xs_c1[k] - yc1;
             const double cost = d0 * d0 + d1 * d1;
-            col += exp((xs_a[k] + bt - cost) / eps) * xs_mu[k] * nu;
+            const double num = xs_a[k] + bt - cost;
+            if (num < zero_cut) continue;
+            col += exp(num / eps) * xs_mu[k] * nu;
         }
         v[t] = col >= trunc ? col : 0.0;
     }

@@ -68,6 +68,18 @@ def _occupancy() -> int:
     return _OCC_CACHE[0]
 
 
+_SM_COUNT: dict = {}
+
+
+def _sm_count(device) -> int:
+    import torch
+
+    key = str(device)
+    if key not in _SM_COUNT:
+        _SM_COUNT[key] = int(torch.cuda.get_device_properties(device).multi_processor_count)
+    return _SM_COUNT[key]
+
+
 def _smem_budget() -> int:
     occ = _occupancy()
     return (220 * 1024) // occ - 1024 * (occ - 1)
@@ -90,6 +102,7 @@ class ExecMode:
     no_cluster: bool = False
     skip_stagnant: bool = True
     smem_budget: int = 0        # bytes per CTA for the size rule (0: the hardware budget)
+    cluster_capped: bool = True  # 2-CTA clusters for cells expected at the cap (few of them)
 
 
 def _env_mode() -> ExecMode:
@@ -670,6 +683,25 @@ class _Batch:
         fits = ws * 8 <= (0 if mode.force_global_ws else budget)
         if mode.force_cluster:
             fits = np.zeros_like(fits)
+        clu = np.zeros(n, dtype=bool)
+        csize = np.zeros(n, dtype=np.int64)
+        csmem = np.zeros(n, dtype=np.int64)
+        # latency: cells whose last solve ran to the cap will again hold the batch
+        # open for max_iters iterations.  When they are few (2 CTAs each fit the SMs
+        # with room to spare) each runs on a 2-CTA cluster, its Y rows split over two
+        # otherwise idle SMs
+        hist = st.iter_hist.get(pt.label)
+        if (hist is not None and mode.cluster_capped and not mode.force_cluster
+                and not mode.no_cluster and not mode.force_global_ws):
+            capped = fits & (hist[ids] >= cfg.max_iters) & (ny0 >= 2)
+            nc = int(capped.sum())
+            if 0 < nc and 2 * nc <= _sm_count(dev):
+                cws = _cluster_ws(pt.nw0, pt.nw1, ny0, ny1, 2) * 8
+                ok = capped & (cws <= budget)
+                csize[ok] = 2
+                csmem[ok] = cws[ok]
+                clu |= ok
+                fits = fits & ~ok
         # cells whose workspace fits run in shared memory (sized for the largest
         # of them); the rest get global-arena slots
         smem_bytes = int(ws[fits].max()) * 8 if fits.any() else 0
@@ -680,9 +712,6 @@ class _Batch:
         # smallest cluster (2, 4, 8, 16 CTAs) whose per-CTA workspace fits;
         # one launch per cluster size
         big = ~fits
-        clu = np.zeros(n, dtype=bool)
-        csize = np.zeros(n, dtype=np.int64)
-        csmem = np.zeros(n, dtype=np.int64)
         if big.any() and not mode.no_cluster and not mode.force_global_ws:
             sizes = (mode.force_cluster,) if mode.force_cluster else CLUSTER_SIZES
             for C in sizes:
@@ -743,6 +772,7 @@ class _Batch:
         self.beta = B.get("beta", tot_y, f64)
         self.mdens = B.get("mdens", tot_y, f64)
         self.lnuw = B.get("lnuw", tot_y, f64)
+        self.lmw = B.get("lmw", tot_y, f64)
         self.lout = B.get("lout", n * pt.nw0 * pt.nw1, f64)
         clu_ids = (np.concatenate([sel for _, sel, _ in groups]).astype(np.int32) if groups
                    else np.zeros(0, np.int32))
@@ -777,7 +807,7 @@ class _Batch:
             delta=cfg.delta, max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
             lout=self.lout.data_ptr(), skip_stagnant=1 if mode.skip_stagnant else 0,
-            order=self.order_d.data_ptr() if n else None,
+            order=self.order_d.data_ptr() if n else None, lmw=self.lmw.data_ptr(),
             precision=1 if cfg.precision == "fp32" else 0)
         self.cfg = cfg
 

@@ -64,10 +64,12 @@ class Level:
     mu: np.ndarray
     nu: np.ndarray
     dp: object = None      # DeviceProblem once staged on the device
+    decs: dict = field(default_factory=dict)   # cell size -> Decomposition (staged pyramids)
 
 
 def stage_pyramid(levels: list, div, eps: float) -> list:
-    """Copy every level's measures to the device once (DeviceProblem per level)."""
+    """Copy every level's measures to the device once (DeviceProblem per level); the
+    partition tables built by the first solve on a level are kept with it."""
     for lv in levels:
         lv.dp = DeviceProblem(TransportProblem(GridMeasure(lv.grid, lv.mu),
                                                GridMeasure(lv.grid, lv.nu), div, eps))
@@ -326,9 +328,15 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
                     progress(lv.grid.dims[0], eps, r)
             duals, duals_geom = (a0, b0), dp.geom
             continue
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore")
-            dec = make_decomposition(prob.mu, cell_size)
+        # a staged pyramid (stage_pyramid) keeps its partition tables with the
+        # device copies of the measures; host pyramids rebuild them every solve
+        dec = lv.decs.get(cell_size) if lv.dp is not None else None
+        if dec is None:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                dec = make_decomposition(prob.mu, cell_size)
+            if lv.dp is not None:
+                lv.decs[cell_size] = dec
         t0 = time.perf_counter()
         if state is None:
             if protocol == "spec":
