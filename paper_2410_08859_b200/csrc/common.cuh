@@ -228,7 +228,12 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         }
         // fixed point of the iteration (the step is below half an ulp of b): every
         // further pass of the reference loop recomputes the same g and step and
-        // leaves b unchanged until max_iters, so stopping here returns the same b
+        // leaves b unchanged until max_iters, so stopping here returns the same b.
+        // Exception (batch coupling of the reference's vectorised loop,
+        // sinkhorn.py:320-326): if a batch-mate leaves its bracket in a later pass,
+        // the reference shrinks every active node's bracket to b and bisects this
+        // stuck node once; it then re-converges to within the tolerance, so the two
+        // results agree to the Newton tolerance, not bitwise, in that case.
         if (nb == b) break;
         // Converged step.  Newton's next correction is at most
         //   |g''| step^2 / (2 g') <= (1 - sig) step^2 / (2 eps)   (g'' = sig(1-sig)/eps^2),

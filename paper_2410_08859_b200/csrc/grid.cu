@@ -333,6 +333,18 @@ int dd_box_gather(int n, const int32_t* box, int bstride, const double* vals, in
     const int nchunks = (n + DD_NT - 1) / DD_NT;
     int4* cb = nullptr;
     cudaError_t e;
+    static thread_local bool pool_kept = false;
+    if (!pool_kept) {
+        // keep freed stream-ordered allocations in the device pool (no OS round trip
+        // for the per-call chunk table)
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_kept = true;
+    }
     if (nchunks > 0) {
         e = cudaMallocAsync((void**)&cb, sizeof(int4) * nchunks, st);
         if (e != cudaSuccess) return dd_set_error(e);

@@ -142,6 +142,11 @@ def run_case(eng, meas, c):
                cell_max_iters=c.get("cell_max_iters", 10_000),
                strategy=c["strategy"], delta=c["delta"], max_iters=c["max_iters"],
                warm=c["warm"], cell_delta_factor=c.get("cell_delta_factor", 0.25))
+    return _outputs(st, rep, out)
+
+
+def _outputs(st, rep, out):
+    """Reference state + report -> fixture arrays (shared by every case)."""
     boxes, vals, offs = [], [], [0]
     for m in st.nu_i:
         b = [x for ax in m.box for x in ax]
@@ -194,6 +199,44 @@ def run_case(eng, meas, c):
     return out
 
 
+def run_ms256(eng, meas):
+    """configs[1] (ms_256) finest stage from the GPU's SPEC handoff.
+
+    tests/golden/ms256_switch_duals.npz (scripts/dump_ms256_switch.py, GPU) holds
+    the duals the device's global Sinkhorn layers 32^2..128^2 prolong to 256^2.
+    The reference's own warm_start_plan (its global Sinkhorn started from those
+    duals instead of zeros, same delta/4 tolerance, then its plan cut) and
+    domdec_solve (staggered, delta 2e-5) produce the fixture.
+    """
+    d = {k: v for k, v in np.load(OUT / "ms256_switch_duals.npz").items()}
+    mu, nu = d["mu"], d["nu"]
+    dx = float(d["dx"])
+    origin = tuple(float(o) for o in d["origin"])
+    grid = meas.Grid(mu.shape, dx=dx, origin=origin)
+    prob = meas.TransportProblem(mu=meas.GridMeasure(grid, mu), nu=meas.GridMeasure(grid, nu),
+                                 div=meas.DivergenceSpec(lam=float(d["lam"])), eps=float(d["eps"]))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        dec = eng.make_decomposition(prob.mu, int(d["s"]))
+    orig = eng.sinkhorn_solve
+
+    def started(kernel, mu_, nu_, m, a0, b0, div, config):
+        return orig(kernel, mu_, nu_, m, d["alpha0"].copy(), d["beta0"].copy(), div, config)
+
+    eng.sinkhorn_solve = started
+    try:
+        ws = eng.warm_start_plan(prob, dec, delta=float(d["warm_delta"]),
+                                 max_iters=int(d["warm_max_iters"]))
+    finally:
+        eng.sinkhorn_solve = orig
+    st, rep = eng.domdec_solve(prob, dec, eng.StrategyConfig(kind="staggered"),
+                               eng.EngineConfig(delta=2e-5), state=ws)
+    out = dict(mu=mu, nu=nu, dx=dx, origin=np.array(origin), lam=float(d["lam"]), eps=prob.eps,
+               s=int(d["s"]), cell_max_iters=10_000, strategy="staggered", delta=2e-5,
+               max_iters=2000, warm=True, cell_delta_factor=0.25)
+    return _outputs(st, rep, out)
+
+
 def kernel_fixtures(sk, meas):
     rng = np.random.default_rng(11)
     # Newton Y-step on a grid including the degenerate extremes
@@ -239,6 +282,14 @@ def main():
     only = set(sys.argv[1:])
     if not only or only & {"kernels"}:
         kernel_fixtures(sk, meas)
+    if "ms256" in only:
+        import time as _t
+        t0 = _t.perf_counter()
+        out = run_ms256(eng, meas)
+        out["ref_seconds"] = _t.perf_counter() - t0
+        np.savez_compressed(OUT / "ms256_final.npz", **out)
+        print("ms256 iters", out["iterations"], "total", out["score"][-1], "seconds",
+              out["ref_seconds"])
     for c in CASES + BASELINE_CASES:
         if not only and c in BASELINE_CASES:
             continue   # slow: generate explicitly by name

@@ -167,3 +167,46 @@ def test_1024_batch_cells_match_oracle(mode):
         np.testing.assert_allclose(st.kl[sol.members], sol.kl, rtol=tol, atol=1e-15)
     print(f"oracle time for {len(pick)} cells: {time.perf_counter() - t0:.1f}s; "
           f"windows {[int(ny[k]) for k in pick]}, iterations {[int(iters[k]) for k in pick]}")
+
+
+def test_ms256_multiscale_matches_reference_on_its_switch_layer():
+    """BASELINE configs[1] end to end: the GPU's SPEC multiscale solve of ms_256
+    against the REFERENCE's warm_start_plan + domdec_solve on the 256^2 switch
+    layer, started from the duals the GPU's global Sinkhorn layers hand over
+    (scripts/dump_ms256_switch.py -> scripts/make_golden.py ms256).  fp64
+    tolerances: marginals and duals 1e-9, objective 1e-10, iterations and
+    actions exact."""
+    import os
+    from _golden import GOLDEN, dense, ref_duals, ref_marginals
+    from _engine_run import box4
+    from paper_2410_08859_b200 import DivergenceSpec, Grid, GridMeasure, TransportProblem
+    from paper_2410_08859_b200.multiscale import multiscale_solve
+    from paper_2410_08859_b200.problems import config_problem_arrays
+
+    if not os.path.exists(os.path.join(GOLDEN, "ms256_final.npz")):
+        pytest.skip("ms256_final fixture not generated")
+    from _golden import load
+    g = load("ms256_final")
+    mu, nu, dx, org, cfg = config_problem_arrays(1, seed=0)
+    assert np.array_equal(mu, g["mu"]) and np.array_equal(nu, g["nu"])
+    h2 = dx * dx
+    prob = TransportProblem(GridMeasure(Grid(mu.shape, dx, org), mu),
+                            GridMeasure(Grid(mu.shape, dx, org), nu),
+                            DivergenceSpec(cfg["lam"]), 2 * h2)
+    st, rep = multiscale_solve(prob, cfg["cell"], cfg["coarsest"], cfg["eps_start_h2"] * h2)
+    r = rep.stages[-1][2]
+    assert r.iterations == int(g["iterations"])
+    assert [t.action for t in r.trace] == [str(a) for a in g["trace_action"]]
+    np.testing.assert_allclose([t.total for t in r.trace], g["trace_total"], rtol=1e-10)
+    shape = mu.shape
+    nu_i = st.nu_i
+    for i, (box, vals) in enumerate(ref_marginals(g)):
+        b = box4(nu_i[i].box)
+        assert b == box, i
+        mine = dense(b, nu_i[i].values.reshape(b[1], b[3]) if b[1] else np.zeros((0, 0)), shape)
+        assert rel_err(mine, dense(box, vals, shape)) < 1e-9, i
+    duals = st.duals
+    for key, (a, bb, b) in ref_duals(g).items():
+        assert rel_err(duals[key].alpha, a) < 1e-9, key
+        assert rel_err(duals[key].beta, b) < 1e-9, key
+    np.testing.assert_allclose(rep.final_score["total"], g["score"][-1], rtol=1e-10)
