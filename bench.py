@@ -365,6 +365,13 @@ def main():
                 "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": int(d2h)},
                 "gpu_launches": int(launches), "clocks": clk.summary()}
+        if world > 1:
+            from paper_2410_08859_b200.engine import _SHARD as sh
+            if sh is not None:
+                line["slab"] = {"halo_and_replicate_bytes_sent_rank0": int(sh.bytes_exchanged),
+                                "note": "point-to-point payload of rank 0 over all timed and "
+                                        "untimed solves; per-batch dense all-reduces (Y snapshot, "
+                                        "blend sums) are ny doubles each"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -398,7 +398,33 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     }
     __syncthreads();
     int bad = 0;
-    for (int o = threadIdx.x; o < ny; o += DD_NT) {
+    // two outputs per pass: their FMA chains and logs are independent, so the
+    // scheduler overlaps the two log latencies (same arithmetic per output)
+    int o = threadIdx.x;
+    for (; o + DD_NT < ny; o += 2 * DD_NT) {
+        const int o2 = o + DD_NT;
+        const int y0 = o / ny1, y1 = o - y0 * ny1;
+        const int z0 = o2 / ny1, z1 = o2 - z0 * ny1;
+        double s0 = 0.0, s1 = 0.0, u0 = 0.0, u1 = 0.0;
+        int k = 0;
+        for (; k + 1 < nw0; k += 2) {
+            s0 = fma(w.K0y[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+            u0 = fma(w.K0y[(int64_t)k * ny0 + z0], T[(int64_t)k * ny1 + z1], u0);
+            s1 = fma(w.K0y[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
+            u1 = fma(w.K0y[(int64_t)(k + 1) * ny0 + z0], T[(int64_t)(k + 1) * ny1 + z1], u1);
+        }
+        if (k < nw0) {
+            s0 = fma(w.K0y[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+            u0 = fma(w.K0y[(int64_t)k * ny0 + z0], T[(int64_t)k * ny1 + z1], u0);
+        }
+        const double sm = s0 + s1, um = u0 + u1;
+        const double ls = log(sm), lu = log(um);
+        if (sm >= kTiny) out[o] = ls + A + (w.c0[y0] + w.c1[y1]);
+        else ++bad;
+        if (um >= kTiny) out[o2] = lu + A + (w.c0[z0] + w.c1[z1]);
+        else ++bad;
+    }
+    for (; o < ny; o += DD_NT) {
         const int y0 = o / ny1, y1 = o - y0 * ny1;
         double s0 = 0.0, s1 = 0.0;
         int k = 0;

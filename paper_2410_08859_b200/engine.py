@@ -102,14 +102,19 @@ class ExecMode:
     no_cluster: bool = False
     skip_stagnant: bool = True
     smem_budget: int = 0        # bytes per CTA for the size rule (0: the hardware budget)
-    cluster_capped: bool = True  # 2-CTA clusters for cells expected at the cap (few of them)
+    # 2-CTA clusters for the few cells expected at the cap (latency).  Off by default:
+    # on ms_1024's 512^2 layer it changed the trajectory (the eps = 4h^2 stage stopped
+    # converging in one sweep and its windows grew) although every golden case
+    # passes through the cluster path; DD_CLUSTER_CAPPED=1 turns it on
+    cluster_capped: bool = False
 
 
 def _env_mode() -> ExecMode:
     return ExecMode(force_cluster=int(_os.environ.get("DD_FORCE_CLUSTER", "0") or 0),
                     force_global_ws=_os.environ.get("DD_FORCE_GLOBAL_WS") == "1",
                     no_cluster=_os.environ.get("DD_NO_CLUSTER") == "1",
-                    skip_stagnant=_os.environ.get("DD_NO_SKIP") != "1")
+                    skip_stagnant=_os.environ.get("DD_NO_SKIP") != "1",
+                    cluster_capped=_os.environ.get("DD_CLUSTER_CAPPED") == "1")
 
 
 _MODE = [_env_mode()]
