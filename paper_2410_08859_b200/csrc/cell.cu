@@ -1037,7 +1037,10 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     // per-cell placement: shared memory when this cell's workspace fits the
     // launch's dynamic allocation, else its slot of the global arena
     if (d[11] & 2) return;   // cell owned by another rank (sharded solve)
-    const bool in_smem = b.smem_mode && lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes;
+    // cells whose Sinkhorn loop ran on a cluster (flag bit 0) take their epilogue in the
+    // global-workspace pass whatever their size (the host may cluster small cells)
+    const bool in_smem = !(d[11] & 1) && b.smem_mode &&
+                         lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes;
     if (in_smem != (kPass == 0)) return;
     // cells whose Sinkhorn loop ran in the cluster kernel: epilogue only
     const bool epi = (d[11] & 1) != 0;
