@@ -116,6 +116,9 @@ typedef struct dd_batch {
     const int32_t* order;      /* nullable [n_cells]: CTA b of the solve kernel takes cell
                                   order[b] (longest-expected-first scheduling) */
     double* lmw;               /* y arena: log m on each cell window (kernel scratch) */
+    int32_t split_smem_bytes;  /* > 0: cells flagged 4 run their Sinkhorn loop in a separate
+                                  two-CTA-per-SM kernel with this much shared memory, then
+                                  their epilogue in the solve kernel */
     int32_t precision;         /* 0: fp64; 1: fp32 mode (the single-CTA cell sweeps run
                                   in fp32: tables, weights, contractions; potentials,
                                   Newton, gap and epilogue fp64; north_star 1e-4) */

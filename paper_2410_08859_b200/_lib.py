@@ -51,7 +51,7 @@ class Batch(C.Structure):
                 ("smem_mode", i32), ("smem_bytes", i32),
                 ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
                 ("newton_tol", dbl), ("trunc", dbl), ("lnuw", vp), ("lout", vp),
-                ("skip_stagnant", i32), ("order", vp), ("lmw", vp), ("precision", i32)]
+                ("skip_stagnant", i32), ("order", vp), ("lmw", vp), ("split_smem_bytes", i32), ("precision", i32)]
 
 
 _SIGS = {

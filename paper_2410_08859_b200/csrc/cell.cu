@@ -1014,8 +1014,12 @@ __global__ void __launch_bounds__(DD_NT, DD_CELL_MIN_BLOCKS) cell_loop_cluster_k
 // kPass 1: the remaining (large-window) cells, workspace in the global arena,
 //          compiled as a separate function so it can run with a max-L1
 //          carveout on a second stream, concurrently with pass 0.
-template <int kPass, bool kF32>
-__global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
+// kLoop: the Sinkhorn loop only (window assembly, tables, loop, capped-cell final
+// sweep), outputs as the cluster kernel leaves them (alpha, beta, lout, cstat); the
+// epilogue then runs in the kPass 0 kernel for cells flagged 4.  Compiled for two
+// CTAs per SM (<= 64 registers): the epilogue's register pressure is not in it.
+template <int kPass, bool kF32, bool kLoop>
+__global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1)))
     cell_solve_kernel(dd_geom g, dd_state s, dd_batch b) {
     extern __shared__ double smem[];
     __shared__ double red[DD_NW + 1];
@@ -1039,11 +1043,15 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
     if (d[11] & 2) return;   // cell owned by another rank (sharded solve)
     // cells whose Sinkhorn loop ran on a cluster (flag bit 0) take their epilogue in the
     // global-workspace pass whatever their size (the host may cluster small cells)
-    const bool in_smem = !(d[11] & 1) && b.smem_mode &&
-                         lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes;
+    if constexpr (kLoop) {
+        if (!(d[11] & 4)) return;          // not a split (loop kernel + epilogue) cell
+    }
+    const bool in_smem = kLoop || (!(d[11] & 1) && b.smem_mode &&
+                                   lay.total * (int64_t)sizeof(double) <= (int64_t)b.smem_bytes);
     if (in_smem != (kPass == 0)) return;
-    // cells whose Sinkhorn loop ran in the cluster kernel: epilogue only
-    const bool epi = (d[11] & 1) != 0;
+    // cells whose Sinkhorn loop ran in the cluster kernel (bit 0) or the loop kernel
+    // (bit 2): epilogue only
+    const bool epi = !kLoop && (d[11] & 5) != 0;
     double* base = in_smem ? smem : (b.work + off[2]);
     Ws w = ws_bind(base, lay);
     w.lnu = b.lnuw + off[0];
@@ -1260,6 +1268,27 @@ __global__ void __launch_bounds__(DD_NT, (kPass == 0 ? DD_CELL_MIN_BLOCKS : 1))
 
         t_loop_d = (double)(clock64() - t_loop0);
         nsteps = block_sum((double)newton_steps, red);
+    }
+    if constexpr (kLoop) {
+        for (int x = tid; x < nx; x += DD_NT) {
+            b.alpha[(int64_t)c * nx + x] = w.alpha[x];
+            b.lout[(int64_t)c * nx + x] = w.L[x];
+        }
+        for (int y = tid; y < ny; y += DD_NT) b.beta[yoff + y] = w.beta[y];
+        if (tid == 0) {
+            double* cs = b.cstat + (int64_t)c * 8;
+            cs[0] = gap;
+            cs[1] = first_gap;
+            cs[2] = (double)iters;
+            cs[3] = converged ? 1.0 : 0.0;
+            cs[4] = (double)n_clamped;
+            cs[5] = (double)newton_clamped;
+            double* c2 = b.cstat2 + (int64_t)c * 8;
+            c2[2] = t_loop_d;
+            c2[3] = nsteps;
+            c2[4] = (double)exec_iters;
+        }
+        return;
     }
 
     // outputs: duals
@@ -2077,24 +2106,24 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaFuncAttributes fa;
-        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel<0, false>);
+        cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel<0, false, false>);
         if (e != cudaSuccess) return dd_set_error(e);
         const int avail = optin - (int)fa.sharedSizeBytes;
         if (smem > avail) return dd_set_error(cudaErrorInvalidValue);
-        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, false>,
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, false, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
         if (e != cudaSuccess) return dd_set_error(e);
-        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, true>,
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, true, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
         if (e != cudaSuccess) return dd_set_error(e);
         configured = avail;
     }
     if (!big_configured) {
-        cudaError_t e = cudaFuncSetAttribute(dd::cell_solve_kernel<1, false>,
+        cudaError_t e = cudaFuncSetAttribute(dd::cell_solve_kernel<1, false, false>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxL1);
         if (e != cudaSuccess) return dd_set_error(e);
-        e = cudaFuncSetAttribute(dd::cell_solve_kernel<1, true>,
+        e = cudaFuncSetAttribute(dd::cell_solve_kernel<1, true, false>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout,
                                  (int)cudaSharedmemCarveoutMaxL1);
         if (e != cudaSuccess) return dd_set_error(e);
@@ -2106,8 +2135,25 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
     }
     const bool f32 = b->precision == 1;
     auto launch_small = [&]() {
-        if (f32) dd::cell_solve_kernel<0, true><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
-        else dd::cell_solve_kernel<0, false><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+        if (b->split_smem_bytes > 0) {
+            // split cells (flag 4): the Sinkhorn loop at two CTAs per SM first, then
+            // their epilogue (with every other shared-memory cell) below
+            static thread_local int split_configured = -1;
+            if (b->split_smem_bytes > split_configured) {
+                cudaFuncSetAttribute(dd::cell_solve_kernel<0, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     b->split_smem_bytes);
+                cudaFuncSetAttribute(dd::cell_solve_kernel<0, true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     b->split_smem_bytes);
+                split_configured = b->split_smem_bytes;
+            }
+            const size_t ss = (size_t)b->split_smem_bytes;
+            if (f32) dd::cell_solve_kernel<0, true, true><<<b->n_cells, DD_NT, ss, st>>>(*g, *s, *b);
+            else dd::cell_solve_kernel<0, false, true><<<b->n_cells, DD_NT, ss, st>>>(*g, *s, *b);
+        }
+        if (f32) dd::cell_solve_kernel<0, true, false><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
+        else dd::cell_solve_kernel<0, false, false><<<b->n_cells, DD_NT, smem, st>>>(*g, *s, *b);
     };
     auto launch_big = [&](cudaStream_t sb) -> cudaError_t {
         for (int k = 0; k < n_groups; ++k) {
@@ -2129,8 +2175,8 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
                                                clu_ids + goff[k]);
             if (e != cudaSuccess) return e;
         }
-        if (f32) dd::cell_solve_kernel<1, true><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
-        else dd::cell_solve_kernel<1, false><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
+        if (f32) dd::cell_solve_kernel<1, true, false><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
+        else dd::cell_solve_kernel<1, false, false><<<b->n_cells, DD_NT, 0, sb>>>(*g, *s, *b);
         return cudaGetLastError();
     };
     if (n_big > 0 && st_big != nullptr && st_big != st) {

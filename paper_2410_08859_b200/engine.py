@@ -107,6 +107,10 @@ class ExecMode:
     # converging in one sweep and its windows grew) although every golden case
     # passes through the cluster path; DD_CLUSTER_CAPPED=1 turns it on
     cluster_capped: bool = False
+    # throughput-bound batches (many cells): shared-memory cells run their Sinkhorn loop
+    # in a separate kernel at two CTAs per SM (<= 64 registers) and the epilogue after
+    split_loop: bool = True
+    force_split: bool = False   # split every fitting shared-memory cell (tests)
 
 
 def _env_mode() -> ExecMode:
@@ -114,7 +118,8 @@ def _env_mode() -> ExecMode:
                     force_global_ws=_os.environ.get("DD_FORCE_GLOBAL_WS") == "1",
                     no_cluster=_os.environ.get("DD_NO_CLUSTER") == "1",
                     skip_stagnant=_os.environ.get("DD_NO_SKIP") != "1",
-                    cluster_capped=_os.environ.get("DD_CLUSTER_CAPPED") == "1")
+                    cluster_capped=_os.environ.get("DD_CLUSTER_CAPPED") == "1",
+                    split_loop=_os.environ.get("DD_NO_SPLIT") != "1")
 
 
 _MODE = [_env_mode()]
@@ -747,6 +752,17 @@ class _Batch:
             groups.append((int(C), sel, int(csmem[sel].max())))
         self.clu_groups = groups
         self.n_clu = int(clu.sum())
+        # split loop: when the batch has many more cells than SMs (throughput-bound),
+        # the shared-memory cells whose workspace fits half an SM run the loop kernel
+        # two CTAs per SM, then their epilogue in the solve kernel (desc flag 4)
+        split = np.zeros(n, dtype=bool)
+        split_smem = 0
+        if (mode.split_loop and not mode.force_cluster and not mode.force_global_ws
+                and (mode.force_split or int(fits.sum()) >= 3 * _sm_count(dev))):
+            half = (220 * 1024) // 2 - 1024
+            split = fits & (ws * 8 <= half)
+            split_smem = int(ws[split].max()) * 8 if split.any() else 0
+        self.n_split = int(split.sum())
         woff = np.concatenate([[0], np.cumsum(gws)[:-1]]).astype(np.int64)
         desc = np.zeros((n, 12), dtype=np.int32)
         desc[:, 0] = ids
@@ -754,7 +770,8 @@ class _Batch:
         desc[:, 5:9] = yb
         desc[:, 9] = nmem
         desc[:, 10] = membase
-        desc[:, 11] = clu.astype(np.int32) | np.where(owned, 0, 2).astype(np.int32)
+        desc[:, 11] = (clu.astype(np.int32) | np.where(owned, 0, 2).astype(np.int32)
+                       | np.where(split & owned, 4, 0).astype(np.int32))
         offs = np.stack([yoff, moff, woff, xoff], axis=1).astype(np.int64)
         mflat = np.concatenate(members).astype(np.int32) if n else np.zeros(0, np.int32)
         self.mflat = mflat
@@ -813,6 +830,7 @@ class _Batch:
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold, lnuw=self.lnuw.data_ptr(),
             lout=self.lout.data_ptr(), skip_stagnant=1 if mode.skip_stagnant else 0,
             order=self.order_d.data_ptr() if n else None, lmw=self.lmw.data_ptr(),
+            split_smem_bytes=split_smem,
             precision=1 if cfg.precision == "fp32" else 0)
         self.cfg = cfg
 

@@ -19,9 +19,12 @@ OBJ_TOL = 1e-10
 DEVICE_CASES = ENGINE_CASES + BASELINE_CASES
 
 # every execution path of the cell solve: shared-memory CTA per cell (default),
-# the global-memory workspace (single CTA), thread-block clusters of 2 and 4 CTAs
+# the global-memory workspace (single CTA), thread-block clusters of 2 and 4 CTAs,
+# and the split loop/epilogue kernels (the default for batches of >= 3x148 cells)
 EXEC_MODES = {"default": {}, "global_ws": {"force_global_ws": True},
-              "cluster2": {"force_cluster": 2}, "cluster4": {"force_cluster": 4}}
+              "cluster2": {"force_cluster": 2}, "cluster4": {"force_cluster": 4},
+              # loop kernel at two CTAs per SM + epilogue in the solve kernel
+              "split": {"force_split": True}}
 
 
 @pytest.fixture(params=sorted(EXEC_MODES))
