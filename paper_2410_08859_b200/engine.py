@@ -109,7 +109,9 @@ class ExecMode:
     cluster_capped: bool = False
     # throughput-bound batches (many cells): shared-memory cells run their Sinkhorn loop
     # in a separate kernel at two CTAs per SM (<= 64 registers) and the epilogue after
-    split_loop: bool = True
+    # measured slower on ms_1024's 1024^2 stage (2.98 -> 3.78 s: 64 registers spill and
+    # a capped cell's latency grows), so opt-in (DD_SPLIT=1); parity-tested either way
+    split_loop: bool = False
     force_split: bool = False   # split every fitting shared-memory cell (tests)
 
 
@@ -119,7 +121,7 @@ def _env_mode() -> ExecMode:
                     no_cluster=_os.environ.get("DD_NO_CLUSTER") == "1",
                     skip_stagnant=_os.environ.get("DD_NO_SKIP") != "1",
                     cluster_capped=_os.environ.get("DD_CLUSTER_CAPPED") == "1",
-                    split_loop=_os.environ.get("DD_NO_SPLIT") != "1")
+                    split_loop=_os.environ.get("DD_SPLIT") == "1")
 
 
 _MODE = [_env_mode()]
@@ -757,7 +759,8 @@ class _Batch:
         # two CTAs per SM, then their epilogue in the solve kernel (desc flag 4)
         split = np.zeros(n, dtype=bool)
         split_smem = 0
-        if (mode.split_loop and not mode.force_cluster and not mode.force_global_ws
+        if ((mode.split_loop or mode.force_split) and not mode.force_cluster
+                and not mode.force_global_ws
                 and (mode.force_split or int(fits.sum()) >= 3 * _sm_count(dev))):
             half = (220 * 1024) // 2 - 1024
             split = fits & (ws * 8 <= half)

@@ -63,8 +63,8 @@ def _capture_1024_stage():
     return captured, mu, nu, dx, org, cfg
 
 
-MODES = {"default": {},          # 1024 cells >= 3 x 148: the split loop/epilogue kernels
-         "no_split": {"split_loop": False},
+MODES = {"default": {},
+         "split": {"split_loop": True},    # 1024 cells >= 3 x 148: loop kernel + epilogue
          "global_ws": {"force_global_ws": True}, "cluster4": {"force_cluster": 4},
          # 48 KB per CTA: the size rule sends the larger windows to 2..16-CTA clusters
          "small_smem": {"smem_budget": 48 * 1024},
@@ -111,7 +111,7 @@ def test_1024_batch_cells_match_oracle(mode):
         set_exec_mode(prev)
     if mode in ("small_smem", "cluster4"):
         assert n_clu > 0, "no cell of the 1024^2 batch took the cluster path"
-    if mode == "default":
+    if mode == "split":
         assert bt.n_split > 0, "the 1024-cell batch did not take the split loop kernel"
     if mode == "small_smem":
         assert len(bt.clu_groups) >= 2, "expected several natural cluster sizes"

@@ -20,7 +20,7 @@ DEVICE_CASES = ENGINE_CASES + BASELINE_CASES
 
 # every execution path of the cell solve: shared-memory CTA per cell (default),
 # the global-memory workspace (single CTA), thread-block clusters of 2 and 4 CTAs,
-# and the split loop/epilogue kernels (the default for batches of >= 3x148 cells)
+# and the split loop/epilogue kernels (opt-in for batches of >= 3x148 cells)
 EXEC_MODES = {"default": {}, "global_ws": {"force_global_ws": True},
               "cluster2": {"force_cluster": 2}, "cluster4": {"force_cluster": 4},
               # loop kernel at two CTAs per SM + epilogue in the solve kernel
