@@ -174,35 +174,8 @@ def prolong_duals(duals, coarse_geom, fine_geom):
     return fa, fb
 
 
-def _seed_iteration_history(st: PlanState, coarse: PlanState, coarse_dec, fine_dec,
-                            parent: np.ndarray) -> None:
-    """Predicted cost of the fine composites for longest-first scheduling: each fine
-    basic cell inherits the last executed iteration count of the coarse partition-A
-    composite holding its parent (cells at the cap stay near the cap one level down:
-    the total-mass mode is inherited); a fine composite takes its members' maximum.
-    Scheduling only — no effect on any result."""
-    if coarse_dec is None:
-        return
-    parts = {p.label: p for p in coarse_dec.composites}
-    hist = coarse.iter_hist.get("A")
-    if hist is None or "A" not in parts:
-        return
-    cpt = _tables(parts["A"])
-    comp_of = np.full(coarse.n_basic + 1, -1, dtype=np.int64)
-    for j in range(cpt.ncomp):
-        m = cpt.mem[j, :cpt.nmem[j]]
-        comp_of[m[m >= 0]] = j
-    cell_hist = np.where(comp_of[parent] >= 0, hist[np.maximum(comp_of[parent], 0)], 0.0)
-    for part in fine_dec.composites:
-        pt = _tables(part)
-        mem = np.where(pt.mem >= 0, pt.mem, 0)
-        vals = np.where(pt.mem >= 0, cell_hist[mem], 0.0)
-        st.iter_hist[pt.label] = vals.max(axis=1).astype(np.float64)
-
-
 def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
-                coarse_duals=None, trunc_threshold: float = 1e-15, dp=None,
-                coarse_dec=None) -> PlanState:
+                coarse_duals=None, trunc_threshold: float = 1e-15, dp=None) -> PlanState:
     """Fine-level state from a solved coarse state (SPEC multiscale.refine_plan).
 
     Each child basic cell keeps its share f_j = mu(X_j)/mu(X_i) of the parent's
@@ -249,7 +222,6 @@ def refine_plan(coarse: PlanState, fine_problem: TransportProblem, fine_dec,
                            _lib.stream_handle()))
     st.sync_boxes()
     st.truncated_mass = coarse.truncated_mass + float(trunc_out.sum().item())
-    _seed_iteration_history(st, coarse, coarse_dec, fine_dec, parent)
     if fa is not None:
         for part in fine_dec.composites:
             pt = _tables(part)
@@ -323,7 +295,6 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
     state = None
     duals = None
     duals_geom = None
-    prev_dec = None
     timings = {"global": 0.0, "warm": 0.0, "refine": 0.0, "domdec": 0.0}
     for li, lv in enumerate(levels):
         eps_list = sched[li] or [None]
@@ -382,8 +353,7 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
                                         dp=lv.dp)
             timings["warm"] += time.perf_counter() - t0
         else:
-            state = refine_plan(state, prob, dec, duals, config.cell.trunc_threshold, dp=lv.dp,
-                                coarse_dec=prev_dec)
+            state = refine_plan(state, prob, dec, duals, config.cell.trunc_threshold, dp=lv.dp)
             timings["refine"] += time.perf_counter() - t0
         for eps in eps_list:
             if eps is None:
@@ -409,7 +379,6 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
                 progress(lv.grid.dims[0], eps, r)
         duals = state.global_duals
         duals_geom = state.dp.geom
-        prev_dec = dec
     timings["total"] = time.perf_counter() - t_all
     rep.timings = timings
     return state, rep
