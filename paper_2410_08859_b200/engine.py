@@ -897,6 +897,19 @@ class BlendScorer:
         self.theta = np.zeros(self.n)
         self.evaluations = 0
 
+    # reference-shaped incremental view (engine.py:458-470), kept on the device
+    def _op(self) -> "_OptState":
+        if getattr(self, "_opt", None) is None:
+            self._opt = _OptState(self)
+        return self._opt
+
+    def set_theta(self, idx: int, theta: float) -> None:
+        self._op().set_theta(int(idx), float(theta))
+        self.theta = self._op().theta
+
+    def minimize_coordinate(self, idx: int, tol: float) -> float:
+        return self._op().minimize_coordinate(int(idx), float(tol))
+
     def energy_at(self, theta_vec) -> float:
         import torch
 
@@ -933,16 +946,22 @@ class BlendScorer:
         return t + self.eps * kl + d1 + self.lam * float(o[0])
 
 
+def _cell_ids(cells) -> list:
+    """Composite ids of the updated cells: the reference passes CellSolution objects
+    (their ``.j``), the device engine passes the ids themselves."""
+    return [int(getattr(c, "j", c)) for c in cells]
+
+
 def get_weights_safe(old_cells, new_cells, part) -> WeightAssignment:
     """theta = 1/K for the K updated cells (engine.py:533-540)."""
-    ids = list(new_cells)
+    ids = _cell_ids(new_cells)
     k = len(ids)
     return WeightAssignment({int(j): 1.0 / k for j in ids})
 
 
 def get_weights_swift(old_cells, new_cells, part, scorer: BlendScorer) -> WeightAssignment:
     """Better of greedy (ones) and safe (1/K); ties to greedy (engine.py:543-554)."""
-    ids = list(new_cells)
+    ids = _cell_ids(new_cells)
     k = len(ids)
     ones, safe = np.ones(k), np.full(k, 1.0 / k)
     vec = ones if scorer.energy_at(ones) <= scorer.energy_at(safe) else safe
@@ -1027,7 +1046,7 @@ def get_weights_opt(old_cells, new_cells, part, scorer: BlendScorer, max_sweeps:
     """Cyclic coordinate descent over theta in [0, 1]^K on the tracked energy,
     seeded with the better of safe and greedy; returns the best of {descent
     iterate, greedy, safe} (engine.py:557-588)."""
-    ids = list(new_cells)
+    ids = _cell_ids(new_cells)
     k = len(ids)
     if scorer.batch.shard is not None:
         raise ValueError("the opt strategy needs per-cell global coordination inside a batch; "
