@@ -279,6 +279,10 @@ int dd_sinkhorn_run(const dd_geom* g, double* alpha, double* beta, const double*
                     double* av, double* px, double* work, int* ctl_i, double* ctl_d, double thr,
                     int k0, int n_iters, int tables_ready, void* stream);
 
+/* fp32-mode diagnostics: out[0..3] = fast-path X / Y sweeps redone by the fp64
+ * stage-wise path, and all fp32 X / Y sweeps, since the last call (then reset). */
+int dd_sweep_fallbacks(unsigned long long* out);
+
 /* Bilinear prolongation of a cell-centred coarse field (nc0 x nc1) to the
  * x2 finer grid (nf0 x nf1); constant beyond the outer coarse centres. */
 int dd_prolong(int nf0, int nf1, int nc0, int nc1, const double* coarse, double* fine,

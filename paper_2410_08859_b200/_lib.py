@@ -23,6 +23,7 @@ EXPORTS = [
     "dd_opt_set", "dd_newton_nodes", "dd_refine", "dd_prolong",
     "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks", "dd_sinkhorn_ws",
     "dd_sinkhorn_run", "dd_assemble_masked", "dd_energy_terms_masked", "dd_blend_parts",
+    "dd_sweep_fallbacks",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -92,6 +93,7 @@ _SIGS = {
                    vp], C.c_int),
     "dd_prolong": ([C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp], C.c_int),
     "dd_sinkhorn_ws": ([C.POINTER(Geom)], i64),
+    "dd_sweep_fallbacks": ([vp], C.c_int),
     "dd_sinkhorn_run": ([C.POINTER(Geom), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, dbl,
                          C.c_int, C.c_int, C.c_int, vp], C.c_int),
     "dd_newton_nodes": ([i64, vp, vp, vp, vp, vp, dbl, C.c_int, vp, vp, vp], C.c_int),
@@ -135,7 +137,7 @@ KERNELS_PER_CALL = {
 
 
 # entry points whose kernel count depends on the arguments
-VARIABLE_LAUNCHES = {"dd_sinkhorn_run", "dd_sinkhorn_ws"}
+VARIABLE_LAUNCHES = {"dd_sinkhorn_run", "dd_sinkhorn_ws", "dd_sweep_fallbacks"}
 
 
 def _sinkhorn_run_launches(args) -> int:
@@ -185,7 +187,8 @@ class _Traced:
                                                                "dd_abi_version", "dd_cell_ws_size",
                                                                "dd_cell_cluster_ws",
                                                                "dd_cell_min_blocks",
-                                                               "dd_sinkhorn_ws"):
+                                                               "dd_sinkhorn_ws",
+                                                               "dd_sweep_fallbacks"):
             return fn
 
         def call(*args):

@@ -456,6 +456,10 @@ __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, doub
 // then redone by the fp64 stage-wise path.  north_star fp32 mode: 1e-4 relative.
 constexpr float kTinyF = 1e-30f;
 
+// sweeps of the fp32 fast path redone by the fp64 stage-wise path: [0] X, [1] Y
+// (read and reset with dd_sweep_fallbacks)
+__device__ unsigned long long g_sweep_fallbacks[4];
+
 __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                                double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
@@ -512,7 +516,11 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     }
     if (bad) *sc.flag = 1;
     __syncthreads();
-    if (*sc.flag) cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+    if (*sc.flag) {
+        if (threadIdx.x == 0) atomicAdd(&g_sweep_fallbacks[0], 1ull);
+        cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+    }
+    if (threadIdx.x == 0) atomicAdd(&g_sweep_fallbacks[2], 1ull);
 }
 
 __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
@@ -564,7 +572,11 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     }
     if (bad) *sc.flag = 1;
     __syncthreads();
-    if (*sc.flag) cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
+    if (*sc.flag) {
+        if (threadIdx.x == 0) atomicAdd(&g_sweep_fallbacks[1], 1ull);
+        cell_lse_y_staged(w, c, nw0, nw1, eps, 0.0, out);
+    }
+    if (threadIdx.x == 0) atomicAdd(&g_sweep_fallbacks[3], 1ull);
 }
 
 template <bool F32>
@@ -2313,3 +2325,12 @@ extern "C" int dd_opt_set(const dd_geom* g, const dd_batch* b, const double* dy,
 
 
 extern "C" int dd_cell_min_blocks(void) { return DD_CELL_MIN_BLOCKS; }
+
+// fp32-mode sweep statistics: out[0..3] = X fallbacks, Y fallbacks, X sweeps, Y sweeps
+// since the last call (diagnostic; counters reset)
+extern "C" int dd_sweep_fallbacks(unsigned long long* out) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, dd::g_sweep_fallbacks, 4 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return dd_set_error(e);
+    unsigned long long z[4] = {0, 0, 0, 0};
+    return dd_set_error(cudaMemcpyToSymbol(dd::g_sweep_fallbacks, z, sizeof(z)));
+}

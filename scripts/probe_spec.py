@@ -23,7 +23,8 @@ if os.environ.get("DD_MS_GDELTA"):
     kw["global_delta"] = float(os.environ["DD_MS_GDELTA"])
 if os.environ.get("DD_MS_PROTOCOL"):
     kw["protocol"] = os.environ["DD_MS_PROTOCOL"]
-print("options", kw, flush=True)
+prec = os.environ.get("DD_MS_PRECISION", "fp64")
+print("options", kw, "precision", prec, flush=True)
 mu, nu, dx, org, cfg = config_problem_arrays(idx, seed=0)
 h2 = dx * dx
 grid = Grid(mu.shape, dx, org)
@@ -50,6 +51,12 @@ E._Batch.solve = solve
 
 
 def prog(n, e, r):
+    if prec == "fp32":
+        import ctypes
+        from paper_2410_08859_b200 import _lib
+        buf = (ctypes.c_ulonglong * 4)()
+        _lib.load().dd_sweep_fallbacks(buf)
+        print(f"  fp32 sweeps: X {buf[0]}/{buf[2]} fell back, Y {buf[1]}/{buf[3]} fell back", flush=True)
     d = r.diagnostics
     print(f"  [stage] N={n} eps/h2={e / h2:.1f} solver={d.get('solver', 'domdec')} iters={r.iterations} "
           f"conv={r.converged} t={r.timings['total']:.2f}s gap={d.get('gap', r.rel_pd_gap):.3e} "
@@ -63,7 +70,9 @@ def prog(n, e, r):
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 st, rep = M.multiscale_solve(prob, cfg["cell"], cfg["coarsest"], cfg["eps_start_h2"] * h2,
-                             config=E.EngineConfig(max_iters=maxit), progress=prog,
+                             config=E.EngineConfig(max_iters=maxit,
+                                                   cell=E.CellSolverConfig(precision=prec)),
+                             progress=prog,
                              **kw)
 torch.cuda.synchronize()
 print(f"TOTAL {time.perf_counter() - t0:.2f}s converged={rep.converged} timings={rep.timings} "
