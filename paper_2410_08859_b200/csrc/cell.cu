@@ -460,17 +460,90 @@ constexpr float kTinyF = 1e-30f;
 // (read and reset with dd_sweep_fallbacks)
 __device__ unsigned long long g_sweep_fallbacks[4];
 
+// Gradient-absorbed fp32 sweeps.  A cell's X-side potentials vary across the 2s x 2s
+// window by (slope of alpha) x (window) / eps -- hundreds to thousands at fine eps --
+// so one global shift leaves the dominant term of many outputs outside fp32's
+// ~87-wide exponent range.  The linear part of that variation is moved into the
+// per-axis tables, exactly (exp(v(x)) = exp(v(x) - s.x) exp(s.x) and exp(s.x) is
+// separable):
+//   X sweep  L[x] = log sum_y w[y] TX0[x0,y0] TX1[x1,y1] + B + th.x,
+//            TXa = exp(-(xa-ya)^2/eps - th_a xa - cXa(ya)), w = exp(bv + cX0 + cX1 - B);
+//   Y sweep  z[y] = log sum_x w[x] TY0[x0,y0] TY1[x1,y1] + A + cY0(y0) + cY1(y1),
+//            TYa = exp(-(xa-ya)^2/eps + ps_a xa - cYa(ya)), w = exp(av - ps.x - A);
+// with th = -slope(alpha)/ratio (the slope of L), ps = slope(alpha)/eps per node
+// index, each column of a table normalised to max 1 (cXa, cYa in fp64).  The tables
+// are rebuilt every sweep from the current alpha.
+struct F32Tables {
+    float* tx0; float* tx1;     // X-sweep tables [x0][y0], [x1][y1]
+    float* ty0; float* ty1;     // Y-sweep tables
+    double* cx0; double* cx1;   // X-sweep column shifts
+    double* cy0; double* cy1;   // Y-sweep column shifts
+};
+
+__device__ __forceinline__ F32Tables f32_tables(const Ws& w, int nw0, int nw1, int ny0, int ny1) {
+    F32Tables t;
+    t.tx0 = reinterpret_cast<float*>(w.K0y);
+    t.ty0 = t.tx0 + (int64_t)nw0 * ny0;
+    t.tx1 = reinterpret_cast<float*>(w.K1y);
+    t.ty1 = t.tx1 + (int64_t)nw1 * ny1;
+    t.cx0 = w.c0;
+    t.cx1 = w.c1;
+    t.cy0 = w.mid + 2 * w.ms;
+    t.cy1 = t.cy0 + ny0;
+    return t;
+}
+
+// per-node-index slopes of alpha along each window axis (0 when not finite); one
+// warp reduces, everyone reads sl[0..1] after the barrier
+__device__ __forceinline__ void alpha_slopes(const double* alpha, int nw0, int nw1, double* sl) {
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        double d0 = 0.0, d1 = 0.0;
+        if (nw0 > 1) for (int x1 = l; x1 < nw1; x1 += 32) d0 += alpha[(int64_t)(nw0 - 1) * nw1 + x1] - alpha[x1];
+        if (nw1 > 1) for (int x0 = l; x0 < nw0; x0 += 32) d1 += alpha[(int64_t)x0 * nw1 + nw1 - 1] - alpha[(int64_t)x0 * nw1];
+        d0 = warp_sum(d0);
+        d1 = warp_sum(d1);
+        if (l == 0) {
+            const double s0 = nw0 > 1 ? d0 / ((double)nw1 * (nw0 - 1)) : 0.0;
+            const double s1 = nw1 > 1 ? d1 / ((double)nw0 * (nw1 - 1)) : 0.0;
+            sl[0] = isfinite(s0) ? s0 : 0.0;
+            sl[1] = isfinite(s1) ? s1 : 0.0;
+        }
+    }
+    __syncthreads();
+}
+
+// table T[xa][ya] = exp(-(xa-ya)^2/eps + s xa - c(ya)), c(ya) = max over xa (fp64)
+__device__ __forceinline__ void build_axis(const double* xc, const double* yc, int nw, int ny,
+                                           double eps, double s, float* T, double* c) {
+    for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        double m = kNegInf;
+        for (int x = 0; x < nw; ++x) m = fmax(m, negsq(xc[x], yc[y], eps) + s * (double)x);
+        c[y] = m;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < nw * ny; o += DD_NT) {
+        const int x = o / ny, y = o - x * ny;
+        T[o] = expf((float)(negsq(xc[x], yc[y], eps) + s * (double)x - c[y]));
+    }
+}
+
 __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                               double* out, SweepScratch sc) {
+                               double ratio, double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    const F32Tables t = f32_tables(w, nw0, nw1, ny0, ny1);
     float* wyf = reinterpret_cast<float*>(w.wy);
-    const float* K1f = reinterpret_cast<const float*>(w.K1y);
-    const float* K0f = reinterpret_cast<const float*>(w.K0y);
     float* T = reinterpret_cast<float*>(w.mid);   // [ny0][nw1]
+    __shared__ double sl[2];
+    alpha_slopes(w.alpha, nw0, nw1, sl);
+    const double th0 = -sl[0] / ratio, th1 = -sl[1] / ratio;   // slopes of L
+    build_axis(w.xc0, w.yc0, nw0, ny0, eps, -th0, t.tx0, t.cx0);
+    build_axis(w.xc1, w.yc1, nw1, ny1, eps, -th1, t.tx1, t.cx1);
     double lmax = kNegInf;
+    __syncthreads();
     for (int y = threadIdx.x; y < ny; y += DD_NT) {
         const int y0 = y / ny1;
-        const double bv = w.beta[y] / eps + w.lnu[y] + (w.c0[y0] + w.c1[y - y0 * ny1]);
+        const double bv = w.beta[y] / eps + w.lnu[y] + (t.cx0[y0] + t.cx1[y - y0 * ny1]);
         w.ty[y] = bv;
         lmax = fmax(lmax, bv);
     }
@@ -486,7 +559,7 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     for (int o = threadIdx.x; o < ny0 * nw1; o += DD_NT) {
         const int y0 = o / nw1, x1 = o - y0 * nw1;
         const float* tr = wyf + (int64_t)y0 * ny1;
-        const float* kr = K1f + (int64_t)x1 * ny1;
+        const float* kr = t.tx1 + (int64_t)x1 * ny1;
         float s0 = 0.f, s1 = 0.f;
         int k = rotate ? x1 % ny1 : 0;
         for (int j = 0; j + 1 < ny1; j += 2) {
@@ -502,7 +575,7 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     int bad = 0;
     for (int o = threadIdx.x; o < nx; o += DD_NT) {
         const int x0 = o / nw1, x1 = o - x0 * nw1;
-        const float* kr = K0f + (int64_t)x0 * ny0;
+        const float* kr = t.tx0 + (int64_t)x0 * ny0;
         float s0 = 0.f, s1 = 0.f;
         int k = 0;
         for (; k + 1 < ny0; k += 2) {
@@ -511,7 +584,7 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
         }
         if (k < ny0) s0 = fmaf(kr[k], T[(int64_t)k * nw1 + x1], s0);
         const float sm = s0 + s1;
-        if (sm >= kTinyF) out[o] = (double)logf(sm) + B;
+        if (sm >= kTinyF) out[o] = (double)logf(sm) + B + (th0 * (double)x0 + th1 * (double)x1);
         else ++bad;
     }
     if (bad) *sc.flag = 1;
@@ -526,14 +599,21 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
 __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                                double ratio, double* out, SweepScratch sc) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
+    const F32Tables t = f32_tables(w, nw0, nw1, ny0, ny1);
     float* wxf = reinterpret_cast<float*>(w.wx);
-    const float* K1f = reinterpret_cast<const float*>(w.K1y);
-    const float* K0f = reinterpret_cast<const float*>(w.K0y);
     float* T = reinterpret_cast<float*>(w.mid);   // [nw0][ny1]
+    for (int x = threadIdx.x; x < nx; x += DD_NT)
+        if (ratio != 0.0) w.alpha[x] = -ratio * w.L[x];
+    __syncthreads();
+    __shared__ double sl[2];
+    alpha_slopes(w.alpha, nw0, nw1, sl);
+    const double ps0 = sl[0] / eps, ps1 = sl[1] / eps;   // slopes of alpha/eps
+    build_axis(w.xc0, w.yc0, nw0, ny0, eps, ps0, t.ty0, t.cy0);
+    build_axis(w.xc1, w.yc1, nw1, ny1, eps, ps1, t.ty1, t.cy1);
     double lmax = kNegInf;
     for (int x = threadIdx.x; x < nx; x += DD_NT) {
-        if (ratio != 0.0) w.alpha[x] = -ratio * w.L[x];
-        const double av = w.alpha[x] / eps + w.lmu[x];
+        const int x0 = x / nw1, x1 = x - x0 * nw1;
+        const double av = w.alpha[x] / eps + w.lmu[x] - (ps0 * (double)x0 + ps1 * (double)x1);
         w.tx[x] = av;
         lmax = fmax(lmax, av);
     }
@@ -549,10 +629,10 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
         float s0 = 0.f, s1 = 0.f;
         int k = 0;
         for (; k + 1 < nw1; k += 2) {
-            s0 = fmaf(tr[k], K1f[(int64_t)k * ny1 + y1], s0);
-            s1 = fmaf(tr[k + 1], K1f[(int64_t)(k + 1) * ny1 + y1], s1);
+            s0 = fmaf(tr[k], t.ty1[(int64_t)k * ny1 + y1], s0);
+            s1 = fmaf(tr[k + 1], t.ty1[(int64_t)(k + 1) * ny1 + y1], s1);
         }
-        if (k < nw1) s0 = fmaf(tr[k], K1f[(int64_t)k * ny1 + y1], s0);
+        if (k < nw1) s0 = fmaf(tr[k], t.ty1[(int64_t)k * ny1 + y1], s0);
         T[o] = s0 + s1;
     }
     __syncthreads();
@@ -562,12 +642,12 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
         float s0 = 0.f, s1 = 0.f;
         int k = 0;
         for (; k + 1 < nw0; k += 2) {
-            s0 = fmaf(K0f[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
-            s1 = fmaf(K0f[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
+            s0 = fmaf(t.ty0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+            s1 = fmaf(t.ty0[(int64_t)(k + 1) * ny0 + y0], T[(int64_t)(k + 1) * ny1 + y1], s1);
         }
-        if (k < nw0) s0 = fmaf(K0f[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
+        if (k < nw0) s0 = fmaf(t.ty0[(int64_t)k * ny0 + y0], T[(int64_t)k * ny1 + y1], s0);
         const float sm = s0 + s1;
-        if (sm >= kTinyF) out[o] = (double)logf(sm) + A + (w.c0[y0] + w.c1[y1]);
+        if (sm >= kTinyF) out[o] = (double)logf(sm) + A + (t.cy0[y0] + t.cy1[y1]);
         else ++bad;
     }
     if (bad) *sc.flag = 1;
@@ -581,8 +661,8 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
 
 template <bool F32>
 __device__ __forceinline__ void sweep_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                                        double* out, SweepScratch sc) {
-    if constexpr (F32) cell_lse_x_f32(w, c, nw0, nw1, eps, out, sc);
+                                        double ratio, double* out, SweepScratch sc) {
+    if constexpr (F32) cell_lse_x_f32(w, c, nw0, nw1, eps, ratio, out, sc);
     else cell_lse_x(w, c, nw0, nw1, eps, out, sc);
 }
 
@@ -1158,15 +1238,11 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
     __syncthreads();
     for (int o = tid; o < nw0 * ny0; o += DD_NT) {
         const int x0 = o / ny0, y0 = o - x0 * ny0;
-        const double kv = exp(negsq(w.xc0[x0], w.yc0[y0], eps) - w.c0[y0]);
-        if constexpr (kF32) reinterpret_cast<float*>(w.K0y)[o] = (float)kv;
-        else w.K0y[o] = kv;
+        if constexpr (!kF32) w.K0y[o] = exp(negsq(w.xc0[x0], w.yc0[y0], eps) - w.c0[y0]);
     }
     for (int o = tid; o < nw1 * ny1; o += DD_NT) {
         const int x1 = o / ny1, y1 = o - x1 * ny1;
-        const double kv = exp(negsq(w.xc1[x1], w.yc1[y1], eps) - w.c1[y1]);
-        if constexpr (kF32) reinterpret_cast<float*>(w.K1y)[o] = (float)kv;
-        else w.K1y[o] = kv;
+        if constexpr (!kF32) w.K1y[o] = exp(negsq(w.xc1[x1], w.yc1[y1], eps) - w.c1[y1]);
     }
     __syncthreads();
     // ---- Sinkhorn loop (sinkhorn.py:361-432 / cells.py:320-348) ----
@@ -1200,7 +1276,7 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
         int par = 0;
         stag_k = 0;
         for (int k = 1; k <= b.max_iters; ++k) {
-            sweep_x<kF32>(w, cw, nw0, nw1, eps, w.L, sc);
+            sweep_x<kF32>(w, cw, nw0, nw1, eps, ratio, w.L, sc);
             if (k >= 2) {
                 double part = 0.0;
                 for (int x = tid; x < nx; x += DD_NT) {
@@ -1258,7 +1334,7 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
         if (!converged) {
             // cap reached: final X sweep and gap for the last (post-Y-step) pair
             // (cells.py:341-348)
-            sweep_x<kF32>(w, cw, nw0, nw1, eps, w.L, sc);
+            sweep_x<kF32>(w, cw, nw0, nw1, eps, ratio, w.L, sc);
             double part = 0.0;
             for (int x = tid; x < nx; x += DD_NT) {
                 const double mu = w.mu[x];
