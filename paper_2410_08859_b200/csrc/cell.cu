@@ -2193,16 +2193,21 @@ static int cell_solve_launch(const dd_geom* g, const dd_state* s, const dd_batch
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncAttributes fa;
+        // (each instantiation has its own static shared memory)
+        cudaFuncAttributes fa, fb;
         cudaError_t e = cudaFuncGetAttributes(&fa, dd::cell_solve_kernel<0, false, false>);
         if (e != cudaSuccess) return dd_set_error(e);
-        const int avail = optin - (int)fa.sharedSizeBytes;
+        e = cudaFuncGetAttributes(&fb, dd::cell_solve_kernel<0, true, false>);
+        if (e != cudaSuccess) return dd_set_error(e);
+        const int avail_a = optin - (int)fa.sharedSizeBytes;
+        const int avail_b = optin - (int)fb.sharedSizeBytes;
+        const int avail = avail_a < avail_b ? avail_a : avail_b;
         if (smem > avail) return dd_set_error(cudaErrorInvalidValue);
         e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, false, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail_a);
         if (e != cudaSuccess) return dd_set_error(e);
         e = cudaFuncSetAttribute(dd::cell_solve_kernel<0, true, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, avail_b);
         if (e != cudaSuccess) return dd_set_error(e);
         configured = avail;
     }
