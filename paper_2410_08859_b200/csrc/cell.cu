@@ -513,18 +513,30 @@ __device__ __forceinline__ void alpha_slopes(const double* alpha, int nw0, int n
     __syncthreads();
 }
 
-// table T[xa][ya] = exp(-(xa-ya)^2/eps + s xa - c(ya)), c(ya) = max over xa (fp64)
+// table T[xa][ya] = exp(-(xa-ya)^2/eps + s xa - c(ya)) with c(ya) the max over the
+// window's xa (fp64).  f(x) = -(x0 + x h - y)^2/eps + s x is a concave parabola in the
+// node index x, maximal at x* = (y - x0)/h + s eps/(2 h^2): the discrete max is at
+// floor(x*) or floor(x*) + 1 clipped to the window, so c costs O(1) per ya.  The table
+// entries need no fp64 division (fp32 accuracy suffices for them).
 __device__ __forceinline__ void build_axis(const double* xc, const double* yc, int nw, int ny,
                                            double eps, double s, float* T, double* c) {
+    const double inv_eps = 1.0 / eps;
+    const double h = nw > 1 ? xc[1] - xc[0] : 1.0;
     for (int y = threadIdx.x; y < ny; y += DD_NT) {
+        const double xs = (yc[y] - xc[0]) / h + s * eps / (2.0 * h * h);
+        int k = (int)floor(fmin(fmax(xs, 0.0), (double)(nw - 1)));
         double m = kNegInf;
-        for (int x = 0; x < nw; ++x) m = fmax(m, negsq(xc[x], yc[y], eps) + s * (double)x);
+        for (int x = k; x <= k + 1 && x < nw; ++x) {
+            const double d = xc[x] - yc[y];
+            m = fmax(m, -(d * d) * inv_eps + s * (double)x);
+        }
         c[y] = m;
     }
     __syncthreads();
     for (int o = threadIdx.x; o < nw * ny; o += DD_NT) {
         const int x = o / ny, y = o - x * ny;
-        T[o] = expf((float)(negsq(xc[x], yc[y], eps) + s * (double)x - c[y]));
+        const double d = xc[x] - yc[y];
+        T[o] = expf((float)(-(d * d) * inv_eps + s * (double)x - c[y]));
     }
 }
 
