@@ -271,6 +271,7 @@ struct SweepScratch {
     double* redm;   // [2*DD_NW] block-max buffers
     int* flag;      // shared underflow flag
     int* par;       // block-max buffer parity
+    double* f32s;   // fp32 mode: slopes the current tables use [X0, X1, Y0, Y1], valid [X, Y]
 };
 
 __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
@@ -548,9 +549,20 @@ __device__ void cell_lse_x_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     float* T = reinterpret_cast<float*>(w.mid);   // [ny0][nw1]
     __shared__ double sl[2];
     alpha_slopes(w.alpha, nw0, nw1, sl);
-    const double th0 = -sl[0] / ratio, th1 = -sl[1] / ratio;   // slopes of L
-    build_axis(w.xc0, w.yc0, nw0, ny0, eps, -th0, t.tx0, t.cx0);
-    build_axis(w.xc1, w.yc1, nw1, ny1, eps, -th1, t.tx1, t.cx1);
+    // the tables are an exact rewrite for any slope; they are rebuilt only when the
+    // slope of L has moved enough to widen the weights' range by more than ~8
+    double th0 = -sl[0] / ratio, th1 = -sl[1] / ratio;   // slopes of L
+    double* cur = sc.f32s;
+    if (cur[4] == 0.0 || fabs(th0 - cur[0]) * (nw0 - 1) > 4.0 ||
+        fabs(th1 - cur[1]) * (nw1 - 1) > 4.0) {
+        build_axis(w.xc0, w.yc0, nw0, ny0, eps, -th0, t.tx0, t.cx0);
+        build_axis(w.xc1, w.yc1, nw1, ny1, eps, -th1, t.tx1, t.cx1);
+        __syncthreads();
+        if (threadIdx.x == 0) { cur[0] = th0; cur[1] = th1; cur[4] = 1.0; }
+    } else {
+        th0 = cur[0];
+        th1 = cur[1];
+    }
     double lmax = kNegInf;
     __syncthreads();
     for (int y = threadIdx.x; y < ny; y += DD_NT) {
@@ -619,9 +631,19 @@ __device__ void cell_lse_y_f32(const Ws& w, const CellWin& c, int nw0, int nw1, 
     __syncthreads();
     __shared__ double sl[2];
     alpha_slopes(w.alpha, nw0, nw1, sl);
-    const double ps0 = sl[0] / eps, ps1 = sl[1] / eps;   // slopes of alpha/eps
-    build_axis(w.xc0, w.yc0, nw0, ny0, eps, ps0, t.ty0, t.cy0);
-    build_axis(w.xc1, w.yc1, nw1, ny1, eps, ps1, t.ty1, t.cy1);
+    double ps0 = sl[0] / eps, ps1 = sl[1] / eps;   // slopes of alpha/eps
+    double* cur = sc.f32s;
+    if (cur[5] == 0.0 || fabs(ps0 - cur[2]) * (nw0 - 1) > 4.0 ||
+        fabs(ps1 - cur[3]) * (nw1 - 1) > 4.0) {
+        build_axis(w.xc0, w.yc0, nw0, ny0, eps, ps0, t.ty0, t.cy0);
+        build_axis(w.xc1, w.yc1, nw1, ny1, eps, ps1, t.ty1, t.cy1);
+        __syncthreads();
+        if (threadIdx.x == 0) { cur[2] = ps0; cur[3] = ps1; cur[5] = 1.0; }
+    } else {
+        ps0 = cur[2];
+        ps1 = cur[3];
+    }
+    __syncthreads();
     double lmax = kNegInf;
     for (int x = threadIdx.x; x < nx; x += DD_NT) {
         const int x0 = x / nw1, x1 = x - x0 * nw1;
@@ -1281,7 +1303,9 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
         __shared__ double redm[2 * DD_NW];
         __shared__ int sweep_flag;
         int mpar = 0;
-        const SweepScratch sc{redm, &sweep_flag, &mpar};
+        __shared__ double f32s[6];
+        if (tid < 6) f32s[tid] = 0.0;   // no fp32 tables built yet for this cell
+        const SweepScratch sc{redm, &sweep_flag, &mpar, f32s};
         __shared__ int ndeg_sh[2];
         __shared__ int moved_sh[2];
         if (tid < 2) { ndeg_sh[tid] = 0; moved_sh[tid] = 0; }
