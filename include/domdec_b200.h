@@ -298,6 +298,139 @@ int dd_reduce_rows(int64_t n_rows, int width, const double* in, double* out, voi
 int dd_grid_kl(int64_t n, const double* y, const double* nu, int clip, double* partial,
                double* out, void* stream);
 
+/* ==== three-axis (3D) path: csrc/vol.cu ====================================
+ *
+ * Problems of up to three axes embedded as 3D grids: a 2D grid (n0, n1) is
+ * (1, n0, n1), a 1D grid (n) is (1, 1, n).  A box is six int32 (off0, ext0,
+ * off1, ext1, off2, ext2); empty when any extent is 0.  The algorithm is the
+ * reference's (same entry points as the 2D path above); the reference's own
+ * Grid rejects 3D (measures.py:76-77) and its SeparableKernel reduces two
+ * axes (sinkhorn.py:159-175) -- the three-axis sweep reduces axis 2, then 1,
+ * then 0, the same order the 2D sweep uses for its two axes.
+ *
+ * Reference interfaces replaced (pkg/src/domdec/):
+ *   dd3_grid_lse       sinkhorn.py:133-175   SeparableKernel.lse_x / lse_y (three axes)
+ *   dd3_prolong        SPEC multiscale       trilinear prolongation of duals
+ *   dd3_cell_solve     cells.py:165-443      make_cell_problems + solve_cell_batch +
+ *                                            balance_cell_masses + _finalize
+ *   dd3_cell_delta     engine.py:388-433     BlendScorer.__init__ per-cell pieces
+ *   dd3_cell_commit    engine.py:726-785     _commit_cell + _stitch_alpha
+ *   dd3_gather         measures.py:410-425   assemble_y_marginal; BlendScorer.energy_at's
+ *                                            y0 + sum theta dy (engine.py:441-456)
+ *   dd3_cell_terms     engine.py:185-196     PlanState.energy per-cell pieces
+ *   dd3_product_init   engine.py:234-257     initial_plan_state (+ cells.py:566)
+ *   dd3_cut_plan       engine.py:294-322     warm_start_plan's plan cut
+ *   dd3_seed_duals     engine.py:325-335     warm_start_plan's dual seeding
+ */
+typedef struct dd3_geom {
+    int32_t nx[3];             /* X grid dims */
+    int32_t ny[3];             /* Y grid dims */
+    int32_t first_axis;        /* first real axis (0 for 3D, 1 for 2D, 2 for 1D) */
+    int32_t pad_;
+    double x_dx, y_dx;
+    double x_org[3], y_org[3];
+    double eps, lam;
+    double nu_total;
+} dd3_geom;
+
+typedef struct dd3_state {
+    const double* mu;          /* X grid masses */
+    const double* nu;          /* Y grid masses */
+    const double* log_mu;      /* log mu (-inf where mu == 0) */
+    const double* log_nu;
+    int32_t n_basic;
+    int32_t block[3];          /* basic block shape */
+    const int32_t* basic_xbox; /* [n_basic*6] */
+    const double* basic_mass;  /* [n_basic] */
+    int32_t* ybox;             /* [n_basic*6] Y-marginal boxes */
+    double* yval;              /* [n_basic*cap] compact row-major values */
+    int64_t cap;
+    double* x_marg;            /* [n_basic*block volume] dense over the block */
+    double* transport;         /* [n_basic] */
+    double* kl;                /* [n_basic] */
+    double* d_alpha;           /* dual store of the partition: [n_comp*nx_win] */
+    int32_t* d_has;            /* [n_comp] */
+    int32_t* d_box;            /* [n_comp*6] */
+    double* d_beta;            /* [n_comp*d_cap] */
+    int64_t d_cap;
+} dd3_state;
+
+/* One batch of composite cells.  desc (int32, 16 per cell):
+ *   j, xbox[6], ybox[6], n_mem, mem_base, flags
+ * offs (int64, 4 per cell): y arena offset (ny entries), member arena offset
+ * (5*n_mem*ny entries: raw split / f, values, tc, tl, mc), workspace offset
+ * (dd3_cell_ws_size doubles), member-x arena offset (n_mem*block entries). */
+typedef struct dd3_batch {
+    int32_t n_cells;
+    int32_t nxw[3];            /* common X window shape */
+    const int32_t* desc;
+    const int64_t* offs;
+    const int32_t* members;
+    const double* snapshot;    /* assembled Y-marginal (Y grid) */
+    double* alpha;             /* [n_cells*nx_win] */
+    double* beta;              /* y arena */
+    double* mdens;             /* y arena: background density m */
+    double* work;              /* workspace arena */
+    double* marena;            /* member arena */
+    double* xarena;            /* member x-marginal arena */
+    int32_t* mbox;             /* [n_members_total*6] new member boxes */
+    double* mstat;             /* [n_members_total*4] transport, kl, truncated, unused */
+    double* cstat;             /* [n_cells*8] gap, first_gap, iters, conv, nu_minus_clamped,
+                                  newton_clamped, balance_fallbacks, target_miss */
+    double* cstat2;            /* [n_cells*8] drift nodes, truncated total, executed
+                                  iterations, sweep fallbacks, 4 unused */
+    double delta;
+    int32_t max_iters;
+    int32_t newton_max_iters;
+    double newton_tol;
+    double trunc;
+} dd3_batch;
+
+/* Workspace doubles of dd3_grid_lse for the geometry. */
+int64_t dd3_grid_ws(const dd3_geom* g);
+/* Separable three-axis log-sum-exp over the full grids (to_x = 1: Y grid -> X grid). */
+int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
+                 void* stream);
+/* Trilinear prolongation of a cell-centred coarse field to the x2 finer grid. */
+int dd3_prolong(const int32_t* nf, const int32_t* nc, const double* coarse, double* fine,
+                void* stream);
+/* Workspace doubles one cell needs (X window w[3], Y window n[3]). */
+int64_t dd3_cell_ws_size(const int32_t* w, const int32_t* n);
+/* Cell batch: windows, Sinkhorn to tolerance, split, balance, truncate, fragments. */
+int dd3_cell_solve(const dd3_geom* g, const dd3_state* s, const dd3_batch* b, void* stream);
+/* Per-cell blend pieces: dy windows (y arena offsets) and cd[c*8] = t_delta, k_delta,
+ * d1_old, d1 at theta = 1, d1 at theta = theta_safe, 3 unused. */
+int dd3_cell_delta(const dd3_geom* g, const dd3_state* s, const dd3_batch* b, double theta_safe,
+                   double* dy, double* cd, void* stream);
+/* Commit theta-blends (per cell theta[c]); stores duals, stitches alpha into alpha_grid
+ * (nullable); errs[c*4] = x_err, y_err, truncated mass added, unused. */
+int dd3_cell_commit(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
+                    const double* theta, double* alpha_grid, double* errs, void* stream);
+/* out (Y grid) = base (nullable: 0) + sum_i scale_i * v_i over item boxes, accumulated in
+ * item order (product rounded before the add).  Item i: box at box + i*bstride, values
+ * at vals + (voff ? voff[i] : i*vstride), compact row-major over its box; scale nullable.
+ * kl_mode 1/2: partial[k] gets per-CTA sums of KL(y | nu) terms (2: y clipped at 0
+ * first), *n_partial their count. */
+int dd3_gather(const dd3_geom* g, int n, const int32_t* box, int bstride, const double* vals,
+               int64_t vstride, const int64_t* voff, const double* scale, const double* base,
+               double* out, int kl_mode, const double* nu, double* partial, int* n_partial,
+               void* stream);
+/* Per basic cell: out[i*4] = transport_i, kl_i, KL(x_marg_i | mu_i), 0. */
+int dd3_cell_terms(const dd3_geom* g, const dd3_state* s, double* out, void* stream);
+/* Product start nu_i = (m_i/|mu|) nu on the full box (cap >= grid size). */
+int dd3_product_init(const dd3_geom* g, const dd3_state* s, double mu_total, void* stream);
+/* Plan cut of global duals along the basic cells (two calls: yval NULL sizes the boxes).
+ * Terms whose log value is below cut_log (e.g. -60) are skipped; tiles of Y nodes are
+ * culled by a bound on that value.  tile_max holds dd3_cut_tiles(g) doubles. */
+int64_t dd3_cut_tiles(const dd3_geom* g);
+int dd3_cut_plan(const dd3_geom* g, const dd3_state* s, const double* alpha, const double* beta,
+                 double trunc, double cut_log, double* tile_max, double* trunc_out,
+                 int32_t* boxes_out, void* stream);
+/* Seed one partition's dual store from global duals (xbox/ybox: [n_comp*6]). */
+int dd3_seed_duals(const dd3_geom* g, const dd3_state* s, int n_comp, const int32_t* nxw,
+                   const int32_t* xbox, const int32_t* ybox, const double* alpha,
+                   const double* beta, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,7 +1,8 @@
 """Oracle kernels: log-sum-exp sweeps, the Newton Y-step, the global solve.
 
 Restates /root/reference/pkg/src/domdec/sinkhorn.py (numpy, CPU, test-only):
-  _lse :57, DenseKernel :91-130, SeparableKernel :133-175,
+  _lse :57, DenseKernel :91-130, SeparableKernel :133-175 (+ its three-axis
+  extension GridKernel3, the same pattern over one more axis),
   y_halfstep_newton :230-333, gap_kl_terms :336-351, sinkhorn_solve :361-432.
 """
 
@@ -85,6 +86,29 @@ class GridKernel:
 
     def lse_y(self, a):
         return self._sweep(np.asarray(a, dtype=np.float64), self.t[0].T, self.t[1].T)
+
+
+class GridKernel3:
+    """Axis-separable sweeps over full 3D grids: the reference's SeparableKernel._sweep
+    (sinkhorn.py:159-175, two axes: last axis first, one _lse per axis) extended by one
+    axis in the same pattern -- the sweep scripts/make_golden.py installs in the
+    reference to produce the 3D fixtures."""
+
+    def __init__(self, x_axes, y_axes, eps: float):
+        self.eps = float(eps)
+        self.t = [-np.subtract.outer(xa, ya) ** 2 / self.eps for xa, ya in zip(x_axes, y_axes)]
+
+    @staticmethod
+    def _sweep(v, t0, t1, t2):
+        a = lse(v[:, :, None, :] + t2[None, None, :, :], axis=3)       # (m0, m1, n2)
+        b = lse(a[:, None, :, :] + t1[None, :, :, None], axis=2)       # (m0, n1, n2)
+        return lse(b[None, :, :, :] + t0[:, :, None, None], axis=1)    # (n0, n1, n2)
+
+    def lse_x(self, b):
+        return self._sweep(np.asarray(b, dtype=np.float64), *self.t)
+
+    def lse_y(self, a):
+        return self._sweep(np.asarray(a, dtype=np.float64), *[t.T for t in self.t])
 
 
 def newton_y(z, m, eps: float, lam: float, beta0, tol: float = 1e-12, max_iters: int = 100):

@@ -24,6 +24,10 @@ EXPORTS = [
     "dd_cell_solve2", "dd_cell_cluster_ws", "dd_cell_min_blocks", "dd_sinkhorn_ws",
     "dd_sinkhorn_run", "dd_assemble_masked", "dd_energy_terms_masked", "dd_blend_parts",
     "dd_sweep_fallbacks",
+    # three-axis path (csrc/vol.cu)
+    "dd3_grid_ws", "dd3_grid_lse", "dd3_prolong", "dd3_cell_ws_size", "dd3_cell_solve",
+    "dd3_cell_delta", "dd3_cell_commit", "dd3_gather", "dd3_cell_terms", "dd3_product_init",
+    "dd3_cut_tiles", "dd3_cut_plan", "dd3_seed_duals",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -55,7 +59,46 @@ class Batch(C.Structure):
                 ("skip_stagnant", i32), ("order", vp), ("lmw", vp), ("split_smem_bytes", i32), ("precision", i32)]
 
 
+class Geom3(C.Structure):
+    _fields_ = [("nx", i32 * 3), ("ny", i32 * 3), ("first_axis", i32), ("pad_", i32),
+                ("x_dx", dbl), ("y_dx", dbl), ("x_org", dbl * 3), ("y_org", dbl * 3),
+                ("eps", dbl), ("lam", dbl), ("nu_total", dbl)]
+
+
+class State3(C.Structure):
+    _fields_ = [("mu", vp), ("nu", vp), ("log_mu", vp), ("log_nu", vp),
+                ("n_basic", i32), ("block", i32 * 3),
+                ("basic_xbox", vp), ("basic_mass", vp), ("ybox", vp), ("yval", vp), ("cap", i64),
+                ("x_marg", vp), ("transport", vp), ("kl", vp),
+                ("d_alpha", vp), ("d_has", vp), ("d_box", vp), ("d_beta", vp), ("d_cap", i64)]
+
+
+class Batch3(C.Structure):
+    _fields_ = [("n_cells", i32), ("nxw", i32 * 3),
+                ("desc", vp), ("offs", vp), ("members", vp), ("snapshot", vp),
+                ("alpha", vp), ("beta", vp), ("mdens", vp), ("work", vp), ("marena", vp),
+                ("xarena", vp), ("mbox", vp), ("mstat", vp), ("cstat", vp), ("cstat2", vp),
+                ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
+                ("newton_tol", dbl), ("trunc", dbl)]
+
+
+G3, S3, B3 = C.POINTER(Geom3), C.POINTER(State3), C.POINTER(Batch3)
+
 _SIGS = {
+    "dd3_grid_ws": ([G3], i64),
+    "dd3_grid_lse": ([G3, vp, vp, C.c_int, vp, vp], C.c_int),
+    "dd3_prolong": ([vp, vp, vp, vp, vp], C.c_int),
+    "dd3_cell_ws_size": ([vp, vp], i64),
+    "dd3_cell_solve": ([G3, S3, B3, vp], C.c_int),
+    "dd3_cell_delta": ([G3, S3, B3, dbl, vp, vp, vp], C.c_int),
+    "dd3_cell_commit": ([G3, S3, B3, vp, vp, vp, vp], C.c_int),
+    "dd3_gather": ([G3, C.c_int, vp, C.c_int, vp, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp],
+                   C.c_int),
+    "dd3_cell_terms": ([G3, S3, vp, vp], C.c_int),
+    "dd3_product_init": ([G3, S3, dbl, vp], C.c_int),
+    "dd3_cut_tiles": ([G3], i64),
+    "dd3_cut_plan": ([G3, S3, vp, vp, dbl, dbl, vp, vp, vp, vp], C.c_int),
+    "dd3_seed_duals": ([G3, S3, C.c_int, vp, vp, vp, vp, vp, vp], C.c_int),
     "dd_last_error": ([], C.c_char_p),
     "dd_device_count": ([], C.c_int),
     "dd_abi_version": ([], C.c_int),
@@ -133,6 +176,9 @@ KERNELS_PER_CALL = {
     "dd_assemble_masked": 2, "dd_energy_terms_masked": 4, "dd_blend_parts": 4,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
+    "dd3_grid_lse": 9, "dd3_prolong": 1, "dd3_cell_solve": 1, "dd3_cell_delta": 1,
+    "dd3_cell_commit": 1, "dd3_gather": 1, "dd3_cell_terms": 1, "dd3_product_init": 1,
+    "dd3_cut_plan": 2, "dd3_seed_duals": 1,
 }
 
 
@@ -149,7 +195,8 @@ class Tracer:
     """Counts calls/kernel launches per entry point and times selected ones with
     CUDA events recorded on the launching (current) stream."""
 
-    def __init__(self, timed=("dd_cell_solve", "dd_cell_solve2", "dd_grid_lse")):
+    def __init__(self, timed=("dd_cell_solve", "dd_cell_solve2", "dd_grid_lse", "dd3_cell_solve",
+                              "dd3_grid_lse")):
         self.timed = set(timed)
         self.calls: dict = {}
         self.events: dict = {}
@@ -188,7 +235,9 @@ class _Traced:
                                                                "dd_cell_cluster_ws",
                                                                "dd_cell_min_blocks",
                                                                "dd_sinkhorn_ws",
-                                                               "dd_sweep_fallbacks"):
+                                                               "dd_sweep_fallbacks",
+                                                               "dd3_grid_ws", "dd3_cut_tiles",
+                                                               "dd3_cell_ws_size"):
             return fn
 
         def call(*args):

@@ -525,6 +525,9 @@ class PlanState:
 def initial_plan_state(problem: TransportProblem, basic: BasicPartition,
                        dp: DeviceProblem | None = None) -> PlanState:
     """Product start nu_i = (|mu_i|/|mu|) nu on the full box (engine.py:234-257)."""
+    if problem.mu.grid.ndim == 3:
+        from .volume import initial_plan_state3
+        return initial_plan_state3(problem, basic, dp)
     st = PlanState(problem, basic, dp, cap=problem.nu.grid.nnodes)
     _lib.check(_lib.lib().dd_product_init(st.dp.geom, st.state_struct(), st.dp.mu_total,
                                           _lib.stream_handle()))
@@ -563,6 +566,11 @@ def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta:
     duals prolonged from the previous layer; ``max_iters=0`` cuts the plan of
     those duals directly)."""
     import torch
+
+    if problem.mu.grid.ndim == 3:
+        from .volume import warm_start_plan3
+        return warm_start_plan3(problem, partitions, delta, max_iters, trunc_threshold, dp,
+                                alpha0, beta0)
 
     dp = dp if dp is not None else DeviceProblem(problem)
     res = sinkhorn_solve(dp, alpha0, beta0, config=SolverConfig(delta=delta, max_iters=max_iters))
@@ -1076,8 +1084,14 @@ class StitchedGapEvaluator:
     """E(state) - D(stitched alpha, polished beta), best pair persisted (engine.py:594-682)."""
 
     def __init__(self, problem: TransportProblem, polish: int = 2, dp: DeviceProblem | None = None):
-        self.dp = dp if dp is not None else DeviceProblem(problem)
-        self.sweeper = GridSweeper(self.dp)
+        if dp is None:
+            if problem.mu.grid.ndim == 3:
+                from .volume import VolumeProblem
+                dp = VolumeProblem(problem)
+            else:
+                dp = DeviceProblem(problem)
+        self.dp = dp
+        self.sweeper = self.dp.make_sweeper()
         self.eps = float(problem.eps)
         self.lam = float(problem.div.lam)
         self.polish = int(polish)
@@ -1326,6 +1340,9 @@ def domdec_solve(problem: TransportProblem, partitions: Decomposition,
                  state: PlanState | None = None, evaluator: StitchedGapEvaluator | None = None):
     """Alternate composite partitions until the duality-gap certificate falls
     below lam * delta * |mu| or the iteration cap (engine.py:938-1037)."""
+    if problem.mu.grid.ndim == 3:
+        from .volume import domdec_solve3
+        return domdec_solve3(problem, partitions, strategy, config, state, evaluator)
     if state is None:
         state = initial_plan_state(problem, partitions.basic)
     lam = problem.div.lam

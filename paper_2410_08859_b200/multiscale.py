@@ -80,6 +80,9 @@ def coarsen(mass: np.ndarray) -> np.ndarray:
     m = np.asarray(mass, dtype=np.float64)
     if m.ndim == 1:
         return m.reshape(-1, 2).sum(axis=1)
+    if m.ndim == 3:
+        n0, n1, n2 = m.shape
+        return m.reshape(n0 // 2, 2, n1 // 2, 2, n2 // 2, 2).sum(axis=(1, 3, 5))
     n0, n1 = m.shape
     return m.reshape(n0 // 2, 2, n1 // 2, 2).sum(axis=(1, 3))
 
@@ -282,6 +285,13 @@ def multiscale_solve(problem: TransportProblem, cell_size: int, n_coarsest: int,
     """
     if protocol not in ("spec", "ladder"):
         raise ValueError(f"unknown multiscale protocol {protocol!r}")
+    if problem.mu.grid.ndim == 3:
+        if protocol != "spec":
+            raise ValueError("the three-axis path runs the SPEC protocol only")
+        from .volume import multiscale_solve3
+        return multiscale_solve3(problem, cell_size, n_coarsest, eps_start, eps_final, strategy,
+                                 config, progress, levels, switch, global_delta,
+                                 global_max_iters, switch_iters)
     t_all = time.perf_counter()
     eps_final = problem.eps if eps_final is None else eps_final
     if levels is None:

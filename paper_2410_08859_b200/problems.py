@@ -36,16 +36,28 @@ class MixtureSpec:
     sigma_hi: float = 0.15
     w_lo: float = 0.5
     w_hi: float = 1.0
+    anisotropic: bool = False   # one sigma per axis (BASELINE configs[4]) instead of one per bump
 
 
 def gaussian_mixture(dims: tuple, dx: float, origin: tuple, spec: MixtureSpec,
                      rng: np.random.Generator) -> np.ndarray:
-    """Floored, normalised isotropic Gaussian mixture on a regular grid."""
+    """Floored, normalised Gaussian mixture (isotropic, or diagonal with
+    ``spec.anisotropic``) on a regular grid."""
     d = len(dims)
     axes = [origin[a] + dx * np.arange(dims[a], dtype=np.float64) for a in range(d)]
     dens = np.zeros(dims, dtype=np.float64)
     for _ in range(spec.n_bumps):
         c = rng.uniform(spec.centre_lo, spec.centre_hi, size=d)
+        if spec.anisotropic:
+            sig = rng.uniform(spec.sigma_lo, spec.sigma_hi, size=d)
+            w = rng.uniform(spec.w_lo, spec.w_hi)
+            q = np.zeros(dims, dtype=np.float64)
+            for a in range(d):
+                shape = [1] * d
+                shape[a] = dims[a]
+                q = q + (((axes[a] - c[a]) ** 2) / (2.0 * sig[a] * sig[a])).reshape(shape)
+            dens += w * np.exp(-q)
+            continue
         sig = rng.uniform(spec.sigma_lo, spec.sigma_hi)
         w = rng.uniform(spec.w_lo, spec.w_hi)
         q = np.zeros(dims, dtype=np.float64)
@@ -71,6 +83,12 @@ BASELINE_CONFIGS = [
     # ladder starts at the coarsest layer's 2 dx^2 = 2 (16 h)^2 = 512 h^2 (SPEC eps_schedule)
     dict(name="ms_2048", n=2048, mu=MixtureSpec(16, 1e-5, 1.0), nu=MixtureSpec(16, 1e-5, 0.7),
          lam=2.0, eps_final_h2=2.0, eps_start_h2=512.0, coarsest=128, cell=8),
+    # configs[4]: 3D 128^3, 4 anisotropic Gaussians (diagonal sigma in [0.05, 0.2]) + 1e-5
+    # floor, masses 1.0 / 1.2, lam 1, eps 32h^2 -> 2h^2, levels 16^3 -> 128^3, 4^3 cells
+    dict(name="vol_128", n=128, dim=3,
+         mu=MixtureSpec(4, 1e-5, 1.0, sigma_lo=0.05, sigma_hi=0.2, anisotropic=True),
+         nu=MixtureSpec(4, 1e-5, 1.2, sigma_lo=0.05, sigma_hi=0.2, anisotropic=True),
+         lam=1.0, eps_final_h2=2.0, eps_start_h2=32.0, coarsest=16, cell=4),
 ]
 
 
@@ -79,9 +97,10 @@ def config_problem_arrays(index: int, seed: int = 0, n: int | None = None):
     cfg = dict(BASELINE_CONFIGS[index])
     n = int(n or cfg["n"])
     dx = 1.0 / n
-    origin = (0.5 * dx, 0.5 * dx)
+    d = int(cfg.get("dim", 2))
+    origin = (0.5 * dx,) * d
     rng = np.random.default_rng(seed)
-    mu = gaussian_mixture((n, n), dx, origin, cfg["mu"], rng)
-    nu = gaussian_mixture((n, n), dx, origin, cfg["nu"], rng)
+    mu = gaussian_mixture((n,) * d, dx, origin, cfg["mu"], rng)
+    nu = gaussian_mixture((n,) * d, dx, origin, cfg["nu"], rng)
     cfg["n"] = n
     return mu, nu, dx, origin, cfg

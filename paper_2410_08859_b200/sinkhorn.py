@@ -65,6 +65,11 @@ class DeviceProblem:
         self.partial = torch.empty(8192, dtype=torch.float64, device=self.device)
         self.sums = torch.zeros(8, dtype=torch.float64, device=self.device)
 
+    device_loop = True   # sinkhorn_solve may run its loop on the device (dd_sinkhorn_run)
+
+    def make_sweeper(self) -> "GridSweeper":
+        return GridSweeper(self)
+
     def empty_x(self):
         import torch
         return torch.empty(self.nx, dtype=torch.float64, device=self.device)
@@ -160,7 +165,7 @@ def mass_balanced_start(dp: DeviceProblem, sweeper: "GridSweeper | None" = None)
 
     g = dp.geom
     eps, lam = g.eps, g.lam
-    sw = sweeper or GridSweeper(dp)
+    sw = sweeper or dp.make_sweeper()
     L0 = sw.lse_x(dp.log_nu)                       # log sum_y e^{-c/eps} nu(y)
     lm = torch.where(dp.mu > 0, dp.log_mu + L0, torch.full_like(L0, -math.inf))
     log_m0 = float(torch.logsumexp(lm, 0).item())
@@ -210,7 +215,7 @@ def sinkhorn_solve(dp: DeviceProblem, alpha0=None, beta0=None, config: SolverCon
     g = dp.geom
     eps, lam = g.eps, g.lam
     ratio = eps * lam / (eps + lam)
-    sw = sweeper or GridSweeper(dp)
+    sw = sweeper or dp.make_sweeper()
     alpha = (torch.zeros(dp.nx, dtype=torch.float64, device=dp.device) if alpha0 is None
              else torch.as_tensor(np.asarray(alpha0, dtype=np.float64).ravel() if not
                                   torch.is_tensor(alpha0) else alpha0.reshape(-1)).to(dp.device).clone())
@@ -227,7 +232,7 @@ def sinkhorn_solve(dp: DeviceProblem, alpha0=None, beta0=None, config: SolverCon
     converged = False
     iterations = 0
     trace = []
-    if not collect_trace and config.max_iters > 0:
+    if not collect_trace and config.max_iters > 0 and dp.device_loop:
         # device-side loop: chunks of iterations enqueued by dd_sinkhorn_run with the
         # stopping test on the device; one host synchronisation per chunk
         lib = _lib.lib()

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/t_smi.log 2>&1
-DD_PROBE_BATCHES=0 DD_MS_PRECISION=fp32 timeout 300 python scripts/probe_spec.py 2 99999 > gpurun_out/t_fp32.log 2>&1
-DD_PROBE_BATCHES=0 timeout 300 python scripts/probe_spec.py 2 99999 > gpurun_out/t_fp64.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -q --timeout 600 -rxX > gpurun_out/t_tests.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_volume.py -q --timeout 300 -x -k "grid_lse3 or global_sinkhorn3" > gpurun_out/v_a.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_volume.py -q --timeout 300 -k "not vol32 and not multiscale" > gpurun_out/v_b.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_volume.py -q --timeout 500 -k "multiscale" > gpurun_out/v_c.log 2>&1
