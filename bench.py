@@ -52,7 +52,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-CONFIGS = {"pr1_64": 0, "ms_256": 1, "ms_1024": 2, "ms_2048": 3}
+CONFIGS = {"pr1_64": 0, "ms_256": 1, "ms_1024": 2, "ms_2048": 3, "vol_128": 4}
 FP64_NOMINAL_TFLOPS = 40.0   # B200 datasheet FP64 (fallback when no measurement is committed)
 SAMPLE_CAP = 100             # cell iteration cap of the CPU sample
 
@@ -215,13 +215,19 @@ def main():
     PRECISION = args.precision
     dtype = "f64" if args.precision == "fp64" else "f32 cell sweeps / f64 state"
     prob, cfg, eps_start = problem(args.config, args.seed)
+    dims = prob.mu.grid.dims
+    nd = len(dims)
+    xs = "x".join(str(n) for n in dims)
+    cellx = "x".join([str(cfg["cell"])] * nd)
+    comp = "x".join(["2"] * nd)
     config_desc = {"workload": f"{args.config}: BASELINE configs[{CONFIGS[args.config]}] "
-                               f"{prob.mu.grid.dims[0]}x{prob.mu.grid.dims[1]} multiscale "
-                               f"{cfg['coarsest']}^2->{prob.mu.grid.dims[0]}^2, "
+                               f"{xs} multiscale "
+                               f"{cfg['coarsest']}^{nd}->{dims[0]}^{nd}, "
                                f"eps {eps_start / prob.mu.grid.dx ** 2:g}h^2->{prob.eps / prob.mu.grid.dx ** 2:g}h^2, "
-                               f"lambda={cfg['lam']}, cells {cfg['cell']}x{cfg['cell']} (2x2 composites), "
+                               f"lambda={cfg['lam']}, cells {cellx} ({comp} composites), "
                                "staggered, delta=2e-5, SPEC multiscale (global Sinkhorn at delta/4 below "
-                               "layer 8 / the finest layer, domdec above)",
+                               "layer 8 / the finest layer, domdec above)"
+                               + (", three-axis path (volume.py, csrc/vol.cu)" if nd == 3 else ""),
                    "grid": list(prob.mu.grid.dims), "cell": cfg["cell"], "lambda": cfg["lam"],
                    "strategy": "staggered", "l2": "flushed (256 MiB write) before every step",
                    "parallelism": (f"row-slab x{world} (each rank solves the composites of its "
@@ -317,8 +323,9 @@ def main():
     t_e2e = float(np.sum(e2e_times)) / len(e2e_times)
     # ---- roofline of the dominant kernel
     tm = tracer.times_ms()
-    solve_ms = tm.get("dd_cell_solve", []) + tm.get("dd_cell_solve2", [])
-    lse_ms = tm.get("dd_grid_lse", [])
+    solve_ms = (tm.get("dd_cell_solve", []) + tm.get("dd_cell_solve2", [])
+                + tm.get("dd3_cell_solve", []))
+    lse_ms = tm.get("dd_grid_lse", []) + tm.get("dd3_grid_lse", [])
     rep = reps[-1]
     flops = sum(r.diagnostics.get("cell_flops", 0.0) for _, _, r in rep.stages)
     n_launch = len(solve_ms) // max(1, args.steps)
@@ -332,7 +339,11 @@ def main():
                    "achieved_gbs": prof.get("dram_gbs"),
                    "fp64_pipe_pct": prof.get("fp64_pipe_pct"),
                    "source": prof.get("source")}
-    roofline = {"bound": "fp64", "kernel": "dd_cell_solve (cell_solve_kernel + cluster variant)",
+    kname = ("dd3_cell_solve (cell_solve3_kernel)" if nd == 3 else
+             "dd_cell_solve (cell_solve_kernel + cluster variant)")
+    if nd == 3:
+        traffic = None   # the committed ncu capture is of the 2D cell kernel
+    roofline = {"bound": "fp64", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None, "peak_source": peak_src,
                 "flops_per_launch": flops / max(n_launch, 1), "launches_per_step": n_launch,

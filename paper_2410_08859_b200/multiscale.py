@@ -71,8 +71,12 @@ def stage_pyramid(levels: list, div, eps: float) -> list:
     """Copy every level's measures to the device once (DeviceProblem per level); the
     partition tables built by the first solve on a level are kept with it."""
     for lv in levels:
-        lv.dp = DeviceProblem(TransportProblem(GridMeasure(lv.grid, lv.mu),
-                                               GridMeasure(lv.grid, lv.nu), div, eps))
+        prob = TransportProblem(GridMeasure(lv.grid, lv.mu), GridMeasure(lv.grid, lv.nu), div, eps)
+        if lv.grid.ndim == 3:
+            from .volume import VolumeProblem
+            lv.dp = VolumeProblem(prob)
+        else:
+            lv.dp = DeviceProblem(prob)
     return levels
 
 
