@@ -388,9 +388,12 @@ typedef struct dd3_batch {
 
 /* Workspace doubles of dd3_grid_lse for the geometry. */
 int64_t dd3_grid_ws(const dd3_geom* g);
-/* Separable three-axis log-sum-exp over the full grids (to_x = 1: Y grid -> X grid). */
+/* Separable three-axis log-sum-exp over the full grids (to_x = 1: Y grid -> X grid).
+ * work holds dd3_grid_ws(g) doubles, including one set of per-axis kernel tables per
+ * direction; tables_ready != 0 reuses the set a previous call with the same geometry,
+ * eps and direction built. */
 int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
-                 void* stream);
+                 int tables_ready, void* stream);
 /* Trilinear prolongation of a cell-centred coarse field to the x2 finer grid. */
 int dd3_prolong(const int32_t* nf, const int32_t* nc, const double* coarse, double* fine,
                 void* stream);

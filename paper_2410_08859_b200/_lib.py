@@ -86,7 +86,7 @@ G3, S3, B3 = C.POINTER(Geom3), C.POINTER(State3), C.POINTER(Batch3)
 
 _SIGS = {
     "dd3_grid_ws": ([G3], i64),
-    "dd3_grid_lse": ([G3, vp, vp, C.c_int, vp, vp], C.c_int),
+    "dd3_grid_lse": ([G3, vp, vp, C.c_int, vp, C.c_int, vp], C.c_int),
     "dd3_prolong": ([vp, vp, vp, vp, vp], C.c_int),
     "dd3_cell_ws_size": ([vp, vp], i64),
     "dd3_cell_solve": ([G3, S3, B3, vp], C.c_int),
@@ -176,7 +176,7 @@ KERNELS_PER_CALL = {
     "dd_assemble_masked": 2, "dd_energy_terms_masked": 4, "dd_blend_parts": 4,
     "dd_cut_plan": 1, "dd_seed_duals": 1, "dd_reduce_rows": 1, "dd_grid_kl": 2, "dd_opt_gh": 1,
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
-    "dd3_grid_lse": 9, "dd3_prolong": 1, "dd3_cell_solve": 1, "dd3_cell_delta": 1,
+    "dd3_grid_lse": 6, "dd3_prolong": 1, "dd3_cell_solve": 1, "dd3_cell_delta": 1,
     "dd3_cell_commit": 1, "dd3_gather": 1, "dd3_cell_terms": 1, "dd3_product_init": 1,
     "dd3_cut_plan": 2, "dd3_seed_duals": 1,
 }
@@ -230,7 +230,7 @@ class _Traced:
     def __getattr__(self, name):
         fn = getattr(self._h, name)
         t = _tracer
-        if t is None or not name.startswith("dd_") or name in ("dd_last_error", "dd_device_count",
+        if t is None or not name.startswith(("dd_", "dd3_")) or name in ("dd_last_error", "dd_device_count",
                                                                "dd_abi_version", "dd_cell_ws_size",
                                                                "dd_cell_cluster_ws",
                                                                "dd_cell_min_blocks",

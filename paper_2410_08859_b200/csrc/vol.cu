@@ -61,11 +61,13 @@ __device__ __forceinline__ double bat(const B3& b, const double* v, int r0, int 
     if (a0 < 0 || a0 >= b.e[0] || a1 < 0 || a1 >= b.e[1] || a2 < 0 || a2 >= b.e[2]) return 0.0;
     return v[((int64_t)a0 * b.e[1] + a1) * b.e[2] + a2];
 }
+// (i0, i1, i2) of a flat row-major index (all window and grid indices are < 2^31)
 __device__ __forceinline__ void unflat(int64_t t, int n1, int n2, int& i0, int& i1, int& i2) {
-    const int64_t q = t / n2;
-    i2 = (int)(t - q * n2);
-    i0 = (int)(q / n1);
-    i1 = (int)(q - (int64_t)i0 * n1);
+    const unsigned u = (unsigned)t;
+    const unsigned q = u / (unsigned)n2;
+    i2 = (int)(u - q * (unsigned)n2);
+    i0 = (int)(q / (unsigned)n1);
+    i1 = (int)(q - (unsigned)i0 * (unsigned)n1);
 }
 
 // block reductions for NT threads (all threads call; all receive the result;
@@ -143,13 +145,13 @@ struct GStage {
     double p_org, p_dx, q_org, q_dx, eps;
 };
 
-// tab[o*K + k] = exp(-(d*d)/eps), d = p_o - q_k
+// tab[k*O + o] = exp(-(d*d)/eps), d = p_o - q_k  (o fastest: coalesced across outputs)
 __global__ void g_table_kernel(int O, int K, double po, double pd, double qo, double qd,
                                double eps, double* tab) {
     const int64_t n = (int64_t)O * K;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int o = (int)(t / K), k = (int)(t - (int64_t)o * K);
+        const int k = (int)(t / O), o = (int)(t - (int64_t)k * O);
         const double d = (po + pd * (double)o) - (qo + qd * (double)k);
         tab[t] = exp(-(d * d) / eps);
     }
@@ -157,6 +159,23 @@ __global__ void g_table_kernel(int O, int K, double po, double pd, double qo, do
 
 __global__ void g_rows_kernel(GStage s) {
     const int64_t rows = (int64_t)s.A * s.B;
+    if (s.B == 1) {
+        // contiguous rows: one warp per row (coalesced)
+        const int lane = threadIdx.x & 31;
+        const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+        const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        for (int64_t r = w0; r < rows; r += nw) {
+            const double* src = s.in + r * s.K;
+            double m = kNegInf;
+            for (int k = lane; k < s.K; k += 32) m = fmax(m, src[k]);
+            m = dd::warp_max_all(m);
+            if (!isfinite(m)) m = 0.0;
+            if (lane == 0) s.rmax[r] = m;
+            double* dst = s.w + r * s.K;
+            for (int k = lane; k < s.K; k += 32) dst[k] = exp(src[k] - m);
+        }
+        return;
+    }
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = t / s.B, b = t - a * s.B;
@@ -180,9 +199,9 @@ __global__ void g_contract_kernel(GStage s) {
         const int o = (int)(r / s.B);
         const int64_t b = r - (int64_t)o * s.B;
         const double* w = s.w + a * s.K * s.B + b;
-        const double* tb = s.tab + (int64_t)o * s.K;
+        const double* tb = s.tab + o;
         double S = 0.0;
-        for (int k = 0; k < s.K; ++k) S = fma(w[(int64_t)k * s.B], tb[k], S);
+        for (int k = 0; k < s.K; ++k) S = fma(w[(int64_t)k * s.B], tb[(int64_t)k * s.O], S);
         double res;
         if (S >= kTiny) {
             res = log(S) + s.rmax[a * s.B + b];
@@ -283,21 +302,43 @@ struct Cell {
     double *mu, *lmu, *alpha, *L, *av, *lnu, *m, *lm, *beta, *z, *kn[3], *c[3], *s1, *s2;
 };
 
+// Mixed-radix position (i0, i1, i2) over dims (., n1, n2) of the flat index
+// t = (i0*n1 + i1)*n2 + i2, advanced by NT per step without divisions (the block
+// loops below visit t = threadIdx.x, threadIdx.x + NT, ...).
+struct Step3 {
+    int i0, i1, i2, s0, s1, s2, n1, n2;
+    __device__ __forceinline__ Step3(int t, int n1_, int n2_) : n1(n1_), n2(n2_) {
+        const unsigned q = (unsigned)t / (unsigned)n2;
+        i2 = t - (int)q * n2;
+        i0 = (int)(q / (unsigned)n1);
+        i1 = (int)q - i0 * n1;
+        const unsigned qs = (unsigned)NT / (unsigned)n2;
+        s2 = NT - (int)qs * n2;
+        s0 = (int)(qs / (unsigned)n1);
+        s1 = (int)qs - s0 * n1;
+    }
+    __device__ __forceinline__ void next() {
+        i2 += s2;
+        int c = i2 >= n2;
+        if (c) i2 -= n2;
+        i1 += s1 + c;
+        c = i1 >= n1;
+        if (c) i1 -= n1;
+        i0 += s0 + c;
+    }
+};
+
 // One in-CTA contraction stage: out[(a*O+o)*B+b] = sum_k in[(a*K+k)*B+b] * T[k*tk + o*to]
 __device__ __forceinline__ void cstage(const double* __restrict__ in, int A, int K, int B, int O,
                                        const double* __restrict__ T, int tk, int to,
                                        double* __restrict__ out) {
-    const int64_t n = (int64_t)A * O * B;
-    const int64_t ob = (int64_t)O * B;
-    for (int64_t t = threadIdx.x; t < n; t += NT) {
-        const int64_t a = t / ob;
-        const int64_t r = t - a * ob;
-        const int o = (int)(r / B);
-        const int64_t b = r - (int64_t)o * B;
-        const double* src = in + a * K * B + b;
-        const double* tp = T + (int64_t)o * to;
+    const int n = A * O * B;
+    Step3 p(threadIdx.x, O, B);
+    for (int t = threadIdx.x; t < n; t += NT, p.next()) {
+        const double* src = in + (p.i0 * K) * B + p.i2;
+        const double* tp = T + p.i1 * to;
         double S = 0.0;
-        for (int k = 0; k < K; ++k) S = fma(src[(int64_t)k * B], tp[(int64_t)k * tk], S);
+        for (int k = 0; k < K; ++k) S = fma(src[k * B], tp[k * tk], S);
         out[t] = S;
     }
     __syncthreads();
@@ -307,25 +348,21 @@ __device__ __forceinline__ void cstage(const double* __restrict__ in, int A, int
 __device__ __forceinline__ void xstage(const double* __restrict__ in, int A, int K, int B, int O,
                                        double po, double pdx, int poff, double qo, double qdx,
                                        int qoff, double eps, double* __restrict__ out) {
-    const int64_t n = (int64_t)A * O * B;
-    const int64_t ob = (int64_t)O * B;
-    for (int64_t t = threadIdx.x; t < n; t += NT) {
-        const int64_t a = t / ob;
-        const int64_t r = t - a * ob;
-        const int o = (int)(r / B);
-        const int64_t b = r - (int64_t)o * B;
-        const double* src = in + a * K * B + b;
-        const double p = po + pdx * (double)(poff + o);
+    const int n = A * O * B;
+    Step3 q(threadIdx.x, O, B);
+    for (int t = threadIdx.x; t < n; t += NT, q.next()) {
+        const double* src = in + (q.i0 * K) * B + q.i2;
+        const double p = po + pdx * (double)(poff + q.i1);
         double m = kNegInf;
         for (int k = 0; k < K; ++k) {
             const double d = p - (qo + qdx * (double)(qoff + k));
-            m = fmax(m, src[(int64_t)k * B] + (-(d * d) / eps));
+            m = fmax(m, src[k * B] + (-(d * d) / eps));
         }
         if (!isfinite(m)) m = 0.0;
         double acc = 0.0;
         for (int k = 0; k < K; ++k) {
             const double d = p - (qo + qdx * (double)(qoff + k));
-            acc += exp(src[(int64_t)k * B] + (-(d * d) / eps) - m);
+            acc += exp(src[k * B] + (-(d * d) / eps) - m);
         }
         out[t] = log(acc) + m;
     }
@@ -343,19 +380,21 @@ struct Sh {
 // Fast path writes L; returns 1 if an output needed the exact path (then redone).
 __device__ int sweep_x(const Cell& C, const dd3_geom& g, Sh& sh) {
     const double eps = g.eps;
+    const int ny = (int)C.ny, nx = (int)C.nx;
     // b' = b + sum_a c_a(y_a) into z (scratch), and its max
     double mx = kNegInf;
-    for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
-        int y0, y1, y2;
-        unflat(y, C.n[1], C.n[2], y0, y1, y2);
-        const double b = C.beta[y] / eps + C.lnu[y];
-        const double bp = b + (C.c[0][y0] + C.c[1][y1] + C.c[2][y2]);
-        C.z[y] = bp;
-        mx = fmax(mx, bp);
+    {
+        Step3 p(threadIdx.x, C.n[1], C.n[2]);
+        for (int y = threadIdx.x; y < ny; y += NT, p.next()) {
+            const double b = C.beta[y] / eps + C.lnu[y];
+            const double bp = b + (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]);
+            C.z[y] = bp;
+            mx = fmax(mx, bp);
+        }
     }
     double M = bmax(mx, sh.red);
     if (!isfinite(M)) M = 0.0;
-    for (int64_t y = threadIdx.x; y < C.ny; y += NT) C.z[y] = exp(C.z[y] - M);
+    for (int y = threadIdx.x; y < ny; y += NT) C.z[y] = exp(C.z[y] - M);
     if (threadIdx.x == 0) sh.flag = 0;
     __syncthreads();
     // U1[y0,y1,x2] = sum_y2 w * Kn2[x2][y2]; U2[y0,x1,x2]; S[x0,x1,x2]
@@ -363,14 +402,14 @@ __device__ int sweep_x(const Cell& C, const dd3_geom& g, Sh& sh) {
     cstage(C.s1, C.n[0], C.n[1], C.w[2], C.w[1], C.kn[1], 1, C.n[1], C.s2);
     int bad = 0;
     {
-        const int64_t n = C.nx;
-        const int64_t ob = (int64_t)C.w[1] * C.w[2];
-        for (int64_t t = threadIdx.x; t < n; t += NT) {
-            const int o = (int)(t / ob);
-            const int64_t b = t - (int64_t)o * ob;
+        const int ob = C.w[1] * C.w[2];
+        const int n0 = C.n[0];
+        Step3 p(threadIdx.x, 1, ob);
+        for (int t = threadIdx.x; t < nx; t += NT, p.next()) {
+            const double* s2 = C.s2 + p.i2;
+            const double* kt = C.kn[0] + p.i0 * n0;
             double S = 0.0;
-            for (int k = 0; k < C.n[0]; ++k)
-                S = fma(C.s2[(int64_t)k * ob + b], C.kn[0][(int64_t)o * C.n[0] + k], S);
+            for (int k = 0; k < n0; ++k) S = fma(s2[k * ob], kt[k], S);
             if (!(S >= kTiny)) bad = 1;
             C.L[t] = log(S) + M;
         }
@@ -379,7 +418,7 @@ __device__ int sweep_x(const Cell& C, const dd3_geom& g, Sh& sh) {
     __syncthreads();
     if (!sh.flag) return 0;
     // exact stage-wise path on b = beta/eps + lnu
-    for (int64_t y = threadIdx.x; y < C.ny; y += NT) C.z[y] = C.beta[y] / eps + C.lnu[y];
+    for (int y = threadIdx.x; y < ny; y += NT) C.z[y] = C.beta[y] / eps + C.lnu[y];
     __syncthreads();
     const int* xo = C.xb.o;
     const int* yo = C.yb.o;
@@ -395,8 +434,9 @@ __device__ int sweep_x(const Cell& C, const dd3_geom& g, Sh& sh) {
 // Y sweep: z[y] = log sum_x exp(a[x] - c(x,y)/eps), a = alpha/eps + lmu (built into av).
 __device__ int sweep_y(const Cell& C, const dd3_geom& g, Sh& sh) {
     const double eps = g.eps;
+    const int ny = (int)C.ny, nx = (int)C.nx;
     double mx = kNegInf;
-    for (int64_t x = threadIdx.x; x < C.nx; x += NT) {
+    for (int x = threadIdx.x; x < nx; x += NT) {
         const double a = C.alpha[x] / eps + C.lmu[x];
         C.av[x] = a;
         mx = fmax(mx, a);
@@ -404,7 +444,7 @@ __device__ int sweep_y(const Cell& C, const dd3_geom& g, Sh& sh) {
     double M = bmax(mx, sh.red);
     if (!isfinite(M)) M = 0.0;
     // shifted weights into L (rebuilt by the next X sweep)
-    for (int64_t x = threadIdx.x; x < C.nx; x += NT) C.L[x] = exp(C.av[x] - M);
+    for (int x = threadIdx.x; x < nx; x += NT) C.L[x] = exp(C.av[x] - M);
     if (threadIdx.x == 0) sh.flag = 0;
     __syncthreads();
     // T1[x0,x1,y2] = sum_x2 w * Kn2[x2][y2]; T2[x0,y1,y2]; S[y0,y1,y2]
@@ -412,16 +452,16 @@ __device__ int sweep_y(const Cell& C, const dd3_geom& g, Sh& sh) {
     cstage(C.s1, C.w[0], C.w[1], C.n[2], C.n[1], C.kn[1], C.n[1], 1, C.s2);
     int bad = 0;
     {
-        const int64_t ob = (int64_t)C.n[1] * C.n[2];
-        for (int64_t t = threadIdx.x; t < C.ny; t += NT) {
-            const int o = (int)(t / ob);
-            const int64_t b = t - (int64_t)o * ob;
-            const int y1 = (int)(b / C.n[2]), y2 = (int)(b - (int64_t)y1 * C.n[2]);
+        const int ob = C.n[1] * C.n[2];
+        const int n0 = C.n[0], w0 = C.w[0];
+        Step3 p(threadIdx.x, C.n[1], C.n[2]);
+        for (int t = threadIdx.x; t < ny; t += NT, p.next()) {
+            const double* s2 = C.s2 + (p.i1 * C.n[2] + p.i2);
+            const double* kt = C.kn[0] + p.i0;
             double S = 0.0;
-            for (int k = 0; k < C.w[0]; ++k)
-                S = fma(C.s2[(int64_t)k * ob + b], C.kn[0][(int64_t)k * C.n[0] + o], S);
+            for (int k = 0; k < w0; ++k) S = fma(s2[k * ob], kt[k * n0], S);
             if (!(S >= kTiny)) bad = 1;
-            C.z[t] = log(S) + M + (C.c[0][o] + C.c[1][y1] + C.c[2][y2]);
+            C.z[t] = log(S) + M + (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]);
         }
     }
     if (bad) sh.flag = 1;
@@ -479,7 +519,11 @@ __device__ __forceinline__ void member_block(const dd3_state& s, const Cell& C, 
     }
 }
 
-__global__ void __launch_bounds__(NT) cell_solve3_kernel(dd3_geom g, dd3_state s, dd3_batch b) {
+#ifndef DD3_MIN_BLOCKS
+#define DD3_MIN_BLOCKS 2   // resident cell CTAs per SM (2: <= 128 registers, no spills)
+#endif
+__global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geom g, dd3_state s,
+                                                                         dd3_batch b) {
     __shared__ Sh sh;
     __shared__ double smem_d[64 * 6];
     const int c = blockIdx.x;
@@ -1599,11 +1643,11 @@ extern "C" int64_t dd3_grid_ws(const dd3_geom* g) {
     const GridWs w = grid_ws_parts(g);
     int64_t tab = 0;
     for (int a = 0; a < 3; ++a) tab += (int64_t)g->nx[a] * g->ny[a];
-    return 2 * w.wmax + w.t1 + w.t2 + tab + 16;
+    return 2 * w.wmax + w.t1 + w.t2 + 2 * tab + 16;
 }
 
 extern "C" int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
-                            void* stream) {
+                            int tables_ready, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int* in = to_x ? g->ny : g->nx;
     const int* on = to_x ? g->nx : g->ny;
@@ -1615,13 +1659,16 @@ extern "C" int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int
     double* rmax = w + ws.wmax;
     double* T1 = rmax + ws.wmax;
     double* T2 = T1 + ws.t1;
+    int64_t tabn = 0;
+    for (int a = 0; a < 3; ++a) tabn += (int64_t)g->nx[a] * g->ny[a];
     double* tab[3];
-    tab[0] = T2 + ws.t2;
+    tab[0] = T2 + ws.t2 + (to_x ? 0 : tabn);     // one table set per direction
     tab[1] = tab[0] + (int64_t)on[0] * in[0];
     tab[2] = tab[1] + (int64_t)on[1] * in[1];
-    for (int a = 0; a < 3; ++a)
-        v3::g_table_kernel<<<v3_blocks((int64_t)on[a] * in[a]), v3::NT, 0, st>>>(
-            on[a], in[a], on_org[a], on_dx, in_org[a], in_dx, g->eps, tab[a]);
+    if (!tables_ready)
+        for (int a = 0; a < 3; ++a)
+            v3::g_table_kernel<<<v3_blocks((int64_t)on[a] * in[a]), v3::NT, 0, st>>>(
+                on[a], in[a], on_org[a], on_dx, in_org[a], in_dx, g->eps, tab[a]);
     // axis 2: (in0*in1, in2, 1) -> (in0*in1, on2, 1); axis 1: (in0, in1, on2) -> (in0, on1,
     // on2); axis 0: (1, in0, on1*on2) -> (1, on0, on1*on2)  (sinkhorn.py:159-175 order)
     const v3::GStage stages[3] = {
@@ -1633,7 +1680,7 @@ extern "C" int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int
          in_dx, g->eps}};
     for (int k = 0; k < 3; ++k) {
         const v3::GStage& S = stages[k];
-        v3::g_rows_kernel<<<v3_blocks((int64_t)S.A * S.B), v3::NT, 0, st>>>(S);
+        v3::g_rows_kernel<<<v3_blocks((int64_t)S.A * S.B * (S.B == 1 ? 32 : 1)), v3::NT, 0, st>>>(S);
         v3::g_contract_kernel<<<v3_blocks((int64_t)S.A * S.O * S.B), v3::NT, 0, st>>>(S);
     }
     return dd_set_error(cudaGetLastError());

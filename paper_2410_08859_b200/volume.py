@@ -134,11 +134,15 @@ class GridSweeper3:
         n = int(_lib.lib().dd3_grid_ws(dp.geom))
         self.work = torch.empty(n, dtype=torch.float64, device=dp.device)
         self.sweeps = 0
+        self._tab_eps = {0: None, 1: None}   # eps each direction's tables were built for
 
     def _sweep(self, v, to_x: int, out=None):
         out = out if out is not None else (self.dp.empty_x() if to_x else self.dp.empty_y())
+        eps = float(self.dp.geom.eps)
+        ready = 1 if self._tab_eps[to_x] == eps else 0
         _lib.check(_lib.lib().dd3_grid_lse(self.dp.geom, v.data_ptr(), out.data_ptr(), to_x,
-                                           self.work.data_ptr(), _lib.stream_handle()))
+                                           self.work.data_ptr(), ready, _lib.stream_handle()))
+        self._tab_eps[to_x] = eps
         self.sweeps += 1
         return out
 
