@@ -283,6 +283,17 @@ class _DualStore:
         nb.view(self.ncomp, new)[:, :self.dcap] = self.beta.view(self.ncomp, self.dcap)
         self.beta, self.dcap = nb, new
 
+    def resize(self, cap: int):
+        """Exactly ``cap`` beta entries per cell (>= the current capacity); ranks of a
+        sharded solve agree on one size before their stores are summed."""
+        import torch
+
+        if cap == self.dcap:
+            return
+        nb = torch.zeros(self.ncomp * cap, dtype=torch.float64, device=self.beta.device)
+        nb.view(self.ncomp, cap)[:, :self.dcap] = self.beta.view(self.ncomp, self.dcap)
+        self.beta, self.dcap = nb, cap
+
     def clone(self):
         c = object.__new__(_DualStore)
         c.ncomp, c.nx, c.dcap = self.ncomp, self.nx, self.dcap

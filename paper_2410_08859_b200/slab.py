@@ -66,6 +66,18 @@ def basic_owners(members: np.ndarray, nmem: np.ndarray, comp_owner: np.ndarray,
     return own
 
 
+def _box_width(plan) -> int:
+    """4 for the 2D path's boxes, 6 for the three-axis path's."""
+    return 6 if getattr(plan, "box_width", 4) == 6 else 4
+
+
+def _box_sizes(b: np.ndarray) -> np.ndarray:
+    """Entries of each box row (o0, e0, o1, e1[, o2, e2])."""
+    b = np.asarray(b, dtype=np.int64).reshape(len(b), -1)
+    n = b[:, 1] * b[:, 3]
+    return n * b[:, 5] if b.shape[1] == 6 else n
+
+
 def halo_sets(prev_owner: np.ndarray, new_owner: np.ndarray, rank: int):
     """Basic cells this rank sends ({peer: ids}) and receives ({peer: ids})."""
     send, recv = {}, {}
@@ -165,15 +177,16 @@ class ShardSpec:
         import torch
 
         dev = plan.ybox.device
-        boxes = plan.ybox.view(-1, 4)
+        bw = _box_width(plan)
+        boxes = plan.ybox.view(-1, bw)
         sb = {q: boxes[torch.as_tensor(ids, device=dev)].clone() for q, ids in send.items()}
-        rb = {r: torch.empty((len(ids), 4), dtype=torch.int32, device=dev)
+        rb = {r: torch.empty((len(ids), bw), dtype=torch.int32, device=dev)
               for r, ids in recv.items()}
         self._p2p(sb, rb)
         need = 1
         for r, ids in recv.items():
             b = rb[r].cpu().numpy()
-            need = max(need, int((b[:, 1].astype(np.int64) * b[:, 3]).max(initial=1)))
+            need = max(need, int(_box_sizes(b).max(initial=1)))
         plan.ensure_cap(need)
         bs = plan.bs
         vals = plan.yval.view(plan.n_basic, plan.cap)
@@ -181,8 +194,8 @@ class ShardSpec:
 
         def pack(ids, bx):
             parts = []
-            for i, b in zip(ids, bx):
-                parts.append(vals[int(i), :int(b[1]) * int(b[3])])
+            for i, k in zip(ids, _box_sizes(bx)):
+                parts.append(vals[int(i), :int(k)])
                 parts.append(xm[int(i)])
             t = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.float64, device=dev)
             frag = torch.stack([plan.transport_d[torch.as_tensor(ids, device=dev)],
@@ -193,14 +206,14 @@ class ShardSpec:
         rp = {}
         for r, ids in recv.items():
             b = rb[r].cpu().numpy()
-            n = int((b[:, 1].astype(np.int64) * b[:, 3]).sum()) + len(ids) * bs + 2 * len(ids)
+            n = int(_box_sizes(b).sum()) + len(ids) * bs + 2 * len(ids)
             rp[r] = torch.empty(n, dtype=torch.float64, device=dev)
         self._p2p(sp, rp)
         for r, ids in recv.items():
             b = rb[r].cpu().numpy()
             buf, o = rp[r], 0
-            for i, bx in zip(ids, b):
-                k = int(bx[1]) * int(bx[3])
+            for i, k in zip(ids, _box_sizes(b)):
+                k = int(k)
                 vals[int(i), :k] = buf[o:o + k]
                 o += k
                 xm[int(i)] = buf[o:o + bs]
@@ -232,14 +245,14 @@ class ShardSpec:
             if comp is None:
                 continue
             dcap = int(self.reduce_np([store.dcap], "max", plan.ybox.device)[0])
-            store.ensure(dcap)
+            store.resize(dcap)        # the same size on every rank before the sums
             keep = torch.from_numpy(comp == self.rank).to(store.alpha.device)
             a = store.alpha.view(store.ncomp, store.nx)
             bt = store.beta.view(store.ncomp, store.dcap)
             a.mul_(keep[:, None].to(a.dtype))
             bt.mul_(keep[:, None].to(bt.dtype))
             store.has.mul_(keep.to(store.has.dtype))
-            store.box.view(store.ncomp, 4).mul_(keep[:, None].to(store.box.dtype))
+            store.box.view(store.ncomp, -1).mul_(keep[:, None].to(store.box.dtype))
             for t in (store.alpha, store.beta, store.has, store.box):
                 self.all_reduce(t)
         own = plan.owner

@@ -20,7 +20,8 @@ is the fixed-order assembly; ``dd3_grid_lse`` the full-grid three-axis sweep of
 the global Sinkhorn solver and the stopping certificate.
 
 Strategies: ``staggered`` (the reference default), ``fast`` and ``safe``.
-Slab sharding is a 2D-path feature (``slab.py``); this path runs on one device.
+Multi-GPU: under ``engine.set_shard()`` the solve is slab-sharded along the first
+real axis (z-slabs for 3D, configs[4]) with the 2D path's slab layer (slab.py).
 There is no CPU path: every call goes through libdomdec_b200.
 """
 
@@ -153,6 +154,27 @@ class GridSweeper3:
         return self._sweep(a, 0, out)
 
 
+def _shard():
+    """The active slab sharding (engine.set_shard) when it spans more than one rank."""
+    from . import engine
+
+    sh = engine._SHARD
+    return sh if (sh is not None and sh.world > 1) else None
+
+
+def _slab_layout3(st: "PlanState3", pt: "_PartTables3"):
+    """(composite owner, basic-cell owner) under the active sharding: slabs of the first
+    real grid axis (z for 3D), cut as in slab.py (``ShardSpec.layout``)."""
+    import types
+
+    lat = st.basic.lattice_dims
+    nd = len(lat)
+    a0 = 3 - nd if nd > 1 else 1        # first two real axes of the 6-int boxes
+    rows, cols = (lat[0], lat[1]) if nd > 1 else (1, lat[0])
+    view = types.SimpleNamespace(xbox=pt.xbox[:, 2 * a0:2 * a0 + 4], mem=pt.mem, nmem=pt.nmem)
+    return _shard().layout(view, (st.block[a0], st.block[a0 + 1]), st.n_basic, rows, cols)
+
+
 def _i32(vals) -> ctypes.Array:
     v = [int(x) for x in vals]
     return (ctypes.c_int32 * len(v))(*v)
@@ -214,6 +236,17 @@ class _Store3:
         nb.view(self.ncomp, new)[:, :self.dcap] = self.beta.view(self.ncomp, self.dcap)
         self.beta, self.dcap = nb, new
 
+    def resize(self, cap: int):
+        """Exactly ``cap`` beta entries per cell (>= the current capacity); ranks of a
+        sharded solve agree on one size before their stores are summed."""
+        import torch
+
+        if cap == self.dcap:
+            return
+        nb = torch.zeros(self.ncomp * cap, dtype=torch.float64, device=self.beta.device)
+        nb.view(self.ncomp, cap)[:, :self.dcap] = self.beta.view(self.ncomp, self.dcap)
+        self.beta, self.dcap = nb, cap
+
     def clone(self):
         c = object.__new__(_Store3)
         c.ncomp, c.nx, c.dcap = self.ncomp, self.nx, self.dcap
@@ -270,6 +303,27 @@ class PlanState3:
         self.global_duals = None
         self.buf = _Bufs(dev)
         self.terms = torch.zeros(nb * 4, dtype=torch.float64, device=dev)
+        # slab mode (engine.set_shard): owning rank of each basic cell (None: all here)
+        self.owner = None
+        self._mask_d = None
+        self.comp_owner: dict = {}
+
+    box_width = 6
+
+    def set_owner(self, owner) -> None:
+        """Slab mode: the owning rank of every basic cell (None: all current here)."""
+        import torch
+
+        sh = _shard()
+        self.owner = None if owner is None else np.asarray(owner, dtype=np.int64).copy()
+        if self.owner is None or sh is None:
+            self._mask_d = None
+        else:
+            m = (self.owner == sh.rank).astype(np.float64)
+            self._mask_d = torch.from_numpy(m).to(self.dp.device)
+
+    def _sharded(self) -> bool:
+        return _shard() is not None and self._mask_d is not None
 
     def state_struct(self, store: _Store3 | None = None) -> _lib.State3:
         dp = self.dp
@@ -310,31 +364,55 @@ class PlanState3:
         self.ybox_h = self.ybox.view(-1, 6).cpu().numpy().copy()
 
     # ---- energy (engine.py:182-196)
-    def assemble_device(self, out=None, kl: bool = False):
-        """Fixed-order sum of the basic-cell marginals (measures.py:410-425); with kl,
-        also the per-tile partial sums of KL(y | nu) in dp.partial (count returned)."""
+    def assemble_device(self, out=None):
+        """Fixed-order sum of the basic-cell marginals (measures.py:410-425).  Slab
+        mode: each rank sums its own basic cells (mask as item scale) and one dense
+        all-reduce completes the grid."""
         out = out if out is not None else self.dp.empty_y()
-        npart = ctypes.c_int(0)
+        sharded = self._sharded()
         _lib.check(_lib.lib().dd3_gather(
             self.dp.geom, self.n_basic, self.ybox.data_ptr(), 6, self.yval.data_ptr(), self.cap,
-            None, None, None, out.data_ptr(), 1 if kl else 0, self.dp.nu.data_ptr(),
-            self._partial(out).data_ptr(), ctypes.byref(npart), _lib.stream_handle()))
-        return (out, npart.value) if kl else out
+            None, self._mask_d.data_ptr() if sharded else None, None, out.data_ptr(), 0, None,
+            None, None, _lib.stream_handle()))
+        if sharded:
+            _shard().all_reduce(out[:self.dp.ny])
+        return out
 
     def _partial(self, y):
         return self.buf.get("partial", self.dp.ny // 32 + 4096, y.dtype)
 
+    def grid_kl(self, y, clip: bool = False, base=None) -> float:
+        """KL(y | nu) over the Y grid (y clipped at 0 first with ``clip``); with
+        ``base`` the argument is base + y."""
+        import torch
+
+        sy = self.dp.shape_y
+        full = self.buf.get("fullbox", 6, torch.int32)
+        full[:6] = torch.tensor([0, sy[0], 0, sy[1], 0, sy[2]], dtype=torch.int32)
+        part = self._partial(y)
+        npart = ctypes.c_int(0)
+        _lib.check(_lib.lib().dd3_gather(
+            self.dp.geom, 1, full.data_ptr(), 6, y.data_ptr(), 0, None, None,
+            base.data_ptr() if base is not None else None, None, 2 if clip else 1,
+            self.dp.nu.data_ptr(), part.data_ptr(), ctypes.byref(npart), _lib.stream_handle()))
+        return float(part[:npart.value].sum().item())
+
     def cell_terms(self) -> np.ndarray:
+        """Per basic cell [transport, kl, KL(x_marg | mu), 0]; slab mode: every rank's
+        owned rows summed (other rows are zero), so all ranks hold the full table."""
         _lib.check(_lib.lib().dd3_cell_terms(self.dp.geom, self.state_struct(),
                                              self.terms.data_ptr(), _lib.stream_handle()))
-        return self.terms.view(self.n_basic, 4).cpu().numpy()
+        t = self.terms.view(self.n_basic, 4).cpu().numpy().copy()
+        if self._sharded():
+            t[self.owner != _shard().rank] = 0.0
+            t = _shard().reduce_np(t.ravel(), "sum", self.dp.device).reshape(self.n_basic, 4)
+        return t
 
     def energy(self):
         from .engine import ScoreBreakdown
 
-        y, npart = self.assemble_device(self.buf.get("energy_y", self.dp.ny, self.dp.mu.dtype),
-                                        kl=True)
-        d2 = float(self._partial(y)[:npart].sum().item())
+        y = self.assemble_device(self.buf.get("energy_y", self.dp.ny, self.dp.mu.dtype))
+        d2 = self.grid_kl(y)
         t = self.cell_terms()
         lam, eps = self.problem.div.lam, self.problem.eps
         d1 = float(np.cumsum(t[:, 2])[-1]) if self.n_basic else 0.0   # sequential (engine.py:187)
@@ -423,6 +501,8 @@ class PlanState3:
         c.stores = {k: v.clone() for k, v in self.stores.items()}
         c.buf = _Bufs(self.dp.device)
         c.terms = self.terms.clone()
+        c.owner = None if self.owner is None else self.owner.copy()
+        c.comp_owner = dict(self.comp_owner)
         return c
 
 
@@ -627,9 +707,15 @@ class _Batch3:
 class BlendScorer3:
     """Tracked energy of uniformly weighted blends of one batch (engine.py:378-456):
     per-cell scalars from ``dd3_cell_delta`` combined on the host in the reference's
-    order, and the Y-side KL of clip(snapshot + theta sum dy) from ``dd3_gather``."""
+    order, and the Y-side KL of clip(snapshot + theta sum dy) from ``dd3_gather``.
 
-    def __init__(self, plan: PlanState3, batch: _Batch3, snapshot, theta_safe: float):
+    Slab mode: ``batch`` holds this rank's cells of the staggered batch; ``pos`` are
+    their positions in the whole batch of ``n_all`` cells.  The per-cell scalars are
+    summed into the whole batch's table and sum_c theta dy_c is all-reduced, so every
+    rank takes the same decision."""
+
+    def __init__(self, plan: PlanState3, batch: _Batch3, snapshot, theta_safe: float,
+                 pos=None, n_all: int | None = None):
         import torch
 
         self.plan, self.batch, self.snapshot = plan, batch, snapshot
@@ -644,7 +730,14 @@ class BlendScorer3:
         _lib.check(_lib.lib().dd3_cell_delta(plan.dp.geom, plan.state_struct(batch.store),
                                              batch.batch, float(theta_safe), self.dy.data_ptr(),
                                              cd.data_ptr(), _lib.stream_handle()))
-        self.cd = cd[:batch.n * 8].view(batch.n, 8).cpu().numpy().copy()
+        mine = cd[:batch.n * 8].view(batch.n, 8).cpu().numpy().copy()
+        self.sharded = pos is not None
+        if self.sharded:
+            full = np.zeros((n_all, 8))
+            full[pos] = mine
+            mine = _shard().reduce_np(full.ravel(), "sum", dev).reshape(n_all, 8)
+        self.cd = mine
+        self.n_all = len(self.cd)
         self.theta_safe = float(theta_safe)
         self.dev = dev
 
@@ -658,19 +751,28 @@ class BlendScorer3:
             col = 3 if th == 1.0 else 4
             if th not in (1.0, self.theta_safe):
                 raise ValueError("BlendScorer3 evaluates theta in {0, 1, theta_safe}")
-            for c in range(b.n):
+            for c in range(self.n_all):
                 t += th * self.cd[c, 0]
                 kl += th * self.cd[c, 1]
                 d1 += self.cd[c, col] - self.cd[c, 2]
-        scale = torch.full((b.n,), th, dtype=torch.float64, device=self.dev)
+        scale = torch.full((max(b.n, 1),), th, dtype=torch.float64, device=self.dev)
         y = p.buf.get("blend_y", p.dp.ny, torch.float64)
-        part = p._partial(y)
-        npart = ctypes.c_int(0)
-        _lib.check(_lib.lib().dd3_gather(
-            p.dp.geom, b.n, b.ybox_d.data_ptr(), 6, self.dy.data_ptr(), 0, b.yoff_d.data_ptr(),
-            scale.data_ptr(), self.snapshot.data_ptr(), y.data_ptr(), 2, p.dp.nu.data_ptr(),
-            part.data_ptr(), ctypes.byref(npart), _lib.stream_handle()))
-        d2 = self.lam * float(part[:npart.value].sum().item())
+        if not self.sharded:
+            part = p._partial(y)
+            npart = ctypes.c_int(0)
+            _lib.check(_lib.lib().dd3_gather(
+                p.dp.geom, b.n, b.ybox_d.data_ptr(), 6, self.dy.data_ptr(), 0,
+                b.yoff_d.data_ptr(), scale.data_ptr(), self.snapshot.data_ptr(), y.data_ptr(), 2,
+                p.dp.nu.data_ptr(), part.data_ptr(), ctypes.byref(npart), _lib.stream_handle()))
+            d2 = self.lam * float(part[:npart.value].sum().item())
+        else:
+            # rank-local sum_c theta dy_c, all-reduced, then KL(clip(snapshot + sum))
+            _lib.check(_lib.lib().dd3_gather(
+                p.dp.geom, b.n, b.ybox_d.data_ptr(), 6, self.dy.data_ptr(), 0,
+                b.yoff_d.data_ptr(), scale.data_ptr(), None, y.data_ptr(), 0, None, None, None,
+                _lib.stream_handle()))
+            _shard().all_reduce(y[:p.dp.ny])
+            d2 = self.lam * p.grid_kl(y, clip=True, base=self.snapshot)
         return t + self.eps * kl + d1 + d2
 
 
@@ -681,16 +783,24 @@ def _absorb(stats, batch: _Batch3) -> None:
     w = batch.pt.nxw
     n = [batch.ybox[:, 2 * a + 1].astype(np.float64) for a in range(3)]
     fl = cell_lse_flops3(w, n[0], n[1], n[2])
-    stats.cell_flops += float((c2[:, 2] * fl).sum())
-    stats.entry_gap += float(c1[:, 1].sum())
-    stats.balance_fallbacks += int(c1[:, 6].sum())
-    stats.nu_minus_clamped += int(c1[:, 4].sum())
-    stats.nonconverged_cells += int((c1[:, 3] == 0).sum())
-    stats.nu_j_drift_nodes += int(c2[:, 0].sum())
-    stats.cell_iterations += int(c1[:, 2].sum())
-    stats.newton_clamped = max(stats.newton_clamped, int(c1[:, 5].max(initial=0)))
-    stats.balance_target_miss = max(stats.balance_target_miss, float(c1[:, 7].max(initial=0.0)))
-    stats.sweep_fallbacks = getattr(stats, "sweep_fallbacks", 0) + int(c2[:, 3].sum())
+    sums = np.array([(c2[:, 2] * fl).sum(), c1[:, 1].sum(), c1[:, 6].sum(), c1[:, 4].sum(),
+                     (c1[:, 3] == 0).sum(), c2[:, 0].sum(), c1[:, 2].sum(), c2[:, 3].sum()],
+                    dtype=np.float64)
+    maxs = np.array([c1[:, 5].max(initial=0), c1[:, 7].max(initial=0.0)], dtype=np.float64)
+    sh = _shard()
+    if sh is not None:
+        sums = sh.reduce_np(sums, "sum", batch.st.dp.device)
+        maxs = sh.reduce_np(maxs, "max", batch.st.dp.device)
+    stats.cell_flops += float(sums[0])
+    stats.entry_gap += float(sums[1])
+    stats.balance_fallbacks += int(sums[2])
+    stats.nu_minus_clamped += int(sums[3])
+    stats.nonconverged_cells += int(sums[4])
+    stats.nu_j_drift_nodes += int(sums[5])
+    stats.cell_iterations += int(sums[6])
+    stats.sweep_fallbacks = getattr(stats, "sweep_fallbacks", 0) + int(sums[7])
+    stats.newton_clamped = max(stats.newton_clamped, int(maxs[0]))
+    stats.balance_target_miss = max(stats.balance_target_miss, float(maxs[1]))
 
 
 def cell_lse_flops3(w, n0, n1, n2):
@@ -703,7 +813,13 @@ def cell_lse_flops3(w, n0, n1, n2):
 
 
 def iteration_parallel3(plan: PlanState3, part: CompositePartition, strategy, config, stats):
-    """Snapshot, batch solve, weighted commit (engine.py:839-922), on the device."""
+    """Snapshot, batch solve, weighted commit (engine.py:839-922), on the device.
+
+    Slab mode (``engine.set_shard``): every rank solves and commits the composites
+    of its slab (slabs of the first real axis, z for 3D); the boundary layer's basic
+    cells move to their new owner before each partition sweep (halo exchange); the
+    snapshot, the blend energies, the residuals and the stitched alpha are reduced
+    over the ranks (slab.py)."""
     import torch
 
     if strategy.kind not in STRATEGIES_3D:
@@ -714,46 +830,62 @@ def iteration_parallel3(plan: PlanState3, part: CompositePartition, strategy, co
     batches = pt.batches if strategy.kind == "staggered" else [np.arange(pt.ncomp)]
     if stats.alpha is None:
         stats.alpha = torch.zeros(plan.dp.nx, dtype=torch.float64, device=plan.dp.device)
+    sh = _shard()
+    comp_owner = None
+    if sh is not None:
+        comp_owner, basic_owner = _slab_layout3(plan, pt)
+        sh.halo_exchange(plan, basic_owner)
+        plan.comp_owner[pt.label] = comp_owner
     actions = []
     for batch in batches:
+        batch = np.asarray(batch, dtype=np.int64)
         t0 = time.perf_counter()
         snapshot = plan.assemble_device(plan.buf.get("snapshot", plan.dp.ny, torch.float64))
         stats.assemble_time += time.perf_counter() - t0
         t0 = time.perf_counter()
-        bt = _Batch3(plan, pt, batch, snapshot, cfg)
+        pos = None
+        ids = batch
+        if sh is not None:
+            pos = np.flatnonzero(comp_owner[batch] == sh.rank)
+            ids = batch[pos]
+        bt = _Batch3(plan, pt, ids, snapshot, cfg)
         bt.solve()
         _absorb(stats, bt)
         stats.solve_time += time.perf_counter() - t0
         t0 = time.perf_counter()
-        kb = bt.n
+        kb = len(batch)
         if strategy.kind == "fast":
-            theta = np.ones(kb)
+            th = 1.0
             actions.append("greedy")
         elif strategy.kind == "safe":
-            theta = np.full(kb, 1.0 / kb)
+            th = 1.0 / kb
             actions.append("safe")
         else:
-            scorer = BlendScorer3(plan, bt, snapshot, 1.0 / kb)
+            scorer = BlendScorer3(plan, bt, snapshot, 1.0 / kb, pos, kb)
             e_base = scorer.energy_at(0.0)
             e_greedy = scorer.energy_at(1.0)
             e_safe = scorer.energy_at(1.0 / kb)
             allowance = strategy.leniency * max(0.0, e_base - e_safe)
             if e_greedy <= e_base + allowance:
-                theta = np.ones(kb)
+                th = 1.0
                 actions.append("greedy")
             else:
-                theta = np.full(kb, 1.0 / kb)
+                th = 1.0 / kb
                 actions.append("safe-fallback")
                 stats.safe_fallbacks += 1
         stats.score_time += time.perf_counter() - t0
         t0 = time.perf_counter()
-        e = bt.commit(theta, stats.alpha)
+        e = bt.commit(np.full(bt.n, th), stats.alpha)
         es = e[:, :3].sum(axis=0)
+        if sh is not None:
+            es = sh.reduce_np(es, "sum", plan.dp.device)
         stats.x_err += float(es[0])
         stats.y_err += float(es[1])
         plan.truncated_mass += float(es[2])
         stats.truncated_mass += float(es[2])
         stats.commit_time += time.perf_counter() - t0
+    if sh is not None:
+        sh.all_reduce(stats.alpha)   # each rank stitched its own composites' blocks
     if len(actions) == 1:
         stats.action = actions[0]
     else:
@@ -821,6 +953,8 @@ def domdec_solve3(problem: TransportProblem, partitions: Decomposition, strategy
         if last_gap / lam <= config.delta * mu_total:
             converged = True
             break
+    if _shard() is not None:
+        _shard().replicate(state)     # the whole plan current on every rank again
     timings["total"] = time.perf_counter() - t_all
     diag["truncated_mass"] = state.truncated_mass
     report = SolveReport(converged=converged, iterations=len(trace), final_score=_score_dict(sb),

@@ -67,3 +67,47 @@ def test_one_dimensional_problems_slab_along_the_lattice():
     comp, basic = sp.layout(pt, (1, 2), dec.basic.n_cells, 1, lat[0])
     assert set(comp.tolist()) == {0, 1}
     assert np.array_equal(basic[:16], np.zeros(16)) and np.array_equal(basic[16:], np.ones(16))
+
+
+def test_three_axis_zslab_layout_halo_is_the_boundary_layer():
+    """configs[4]-shaped decomposition (16^3, 4^3 cells, 2^3 composites) sharded over 2
+    ranks along z: A composites never straddle the slab boundary, B composites that do
+    belong to the lower rank, and the basic cells changing owner between the A and
+    B sweeps are exactly the boundary z-layer of the block lattice."""
+    import warnings
+
+    import numpy as np
+
+    from paper_2410_08859_b200 import DivergenceSpec, Grid, GridMeasure, TransportProblem
+    from paper_2410_08859_b200.decomposition import make_decomposition
+    from paper_2410_08859_b200.slab import ShardSpec, halo_sets
+    from paper_2410_08859_b200.volume import _PartTables3
+
+    n, s = 16, 4
+    mu = np.ones((n, n, n))
+    prob = TransportProblem(GridMeasure(Grid((n, n, n), 1 / n, (0.0,) * 3), mu),
+                            GridMeasure(Grid((n, n, n), 1 / n, (0.0,) * 3), mu),
+                            DivergenceSpec(1.0), 1e-3)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        dec = make_decomposition(prob.mu, s)
+    sh = object.__new__(ShardSpec)
+    sh.world, sh.rank, sh._cache = 2, 0, {}
+    import types
+    owners = {}
+    for part in dec.composites:
+        pt = _PartTables3(part)
+        view = types.SimpleNamespace(xbox=pt.xbox[:, 0:4], mem=pt.mem, nmem=pt.nmem)
+        comp, basic = sh.layout(view, (s, s), dec.basic.n_basic if hasattr(dec.basic, "n_basic")
+                                else dec.basic.n_cells, 4, 4)
+        owners[part.label] = (pt, comp, basic)
+    pos = dec.basic.positions           # (n_cells, 3) block-lattice coordinates
+    pa, ca, ba = owners["A"]
+    pb, cb, bb = owners["B"]
+    assert set(np.unique(ba)) == {0, 1} and set(np.unique(bb)) == {0, 1}
+    # A: z-slab {0,1} -> rank 0, {2,3} -> rank 1
+    assert np.array_equal(ba, (pos[:, 0] >= 2).astype(np.int64))
+    moved = np.flatnonzero(ba != bb)
+    assert set(pos[moved, 0].tolist()) == {2}      # the boundary layer z = 2 only
+    send, recv = halo_sets(ba, bb, 1)
+    assert list(send) == [0] and np.array_equal(np.sort(send[0]), np.sort(moved))
