@@ -30,7 +30,11 @@ extern "C" int dd_set_error(cudaError_t e);
 
 namespace v3 {
 
-constexpr int NT = 256;
+constexpr int NT = 256;      // threads per CTA of the grid / blend / commit / start kernels
+#ifndef DD3_CELL_NT
+#define DD3_CELL_NT 512      // threads per CTA of the cell solve (the whole SM for one cell:
+#endif                       // batches end on their longest cells, so latency rules)
+constexpr int CELL_NT = DD3_CELL_NT;
 constexpr int NW = NT / 32;
 constexpr double kTiny = 1e-290;
 constexpr double kNegInf = -__builtin_huge_val();
@@ -72,6 +76,7 @@ __device__ __forceinline__ void unflat(int64_t t, int n1, int n2, int& i0, int& 
 
 // block reductions for NT threads (all threads call; all receive the result;
 // fixed order, so deterministic)
+template <int T = NT>
 __device__ __forceinline__ double bsum(double v, double* red) {
     v = dd::warp_sum(v);
     __syncthreads();
@@ -79,9 +84,10 @@ __device__ __forceinline__ double bsum(double v, double* red) {
     __syncthreads();
     double t = 0.0;
 #pragma unroll
-    for (int k = 0; k < NW; ++k) t += red[k];
+    for (int k = 0; k < (T / 32); ++k) t += red[k];
     return t;
 }
+template <int T = NT>
 __device__ __forceinline__ double bmax(double v, double* red) {
     v = dd::warp_max(v);
     __syncthreads();
@@ -89,9 +95,10 @@ __device__ __forceinline__ double bmax(double v, double* red) {
     __syncthreads();
     double t = red[0];
 #pragma unroll
-    for (int k = 1; k < NW; ++k) t = fmax(t, red[k]);
+    for (int k = 1; k < (T / 32); ++k) t = fmax(t, red[k]);
     return t;
 }
+template <int T = NT>
 __device__ __forceinline__ int bmin_i(int v, int* red) {
     v = dd::warp_min_i(v);
     __syncthreads();
@@ -99,9 +106,10 @@ __device__ __forceinline__ int bmin_i(int v, int* red) {
     __syncthreads();
     int t = red[0];
 #pragma unroll
-    for (int k = 1; k < NW; ++k) t = min(t, red[k]);
+    for (int k = 1; k < (T / 32); ++k) t = min(t, red[k]);
     return t;
 }
+template <int T = NT>
 __device__ __forceinline__ int bmax_i(int v, int* red) {
     v = dd::warp_max_i(v);
     __syncthreads();
@@ -109,7 +117,7 @@ __device__ __forceinline__ int bmax_i(int v, int* red) {
     __syncthreads();
     int t = red[0];
 #pragma unroll
-    for (int k = 1; k < NW; ++k) t = max(t, red[k]);
+    for (int k = 1; k < (T / 32); ++k) t = max(t, red[k]);
     return t;
 }
 
@@ -303,8 +311,9 @@ struct Cell {
 };
 
 // Mixed-radix position (i0, i1, i2) over dims (., n1, n2) of the flat index
-// t = (i0*n1 + i1)*n2 + i2, advanced by NT per step without divisions (the block
-// loops below visit t = threadIdx.x, threadIdx.x + NT, ...).
+// t = (i0*n1 + i1)*n2 + i2, advanced by T per step without divisions (the block
+// loops below visit t = threadIdx.x, threadIdx.x + T, ...).
+template <int T>
 struct Step3 {
     int i0, i1, i2, s0, s1, s2, n1, n2;
     __device__ __forceinline__ Step3(int t, int n1_, int n2_) : n1(n1_), n2(n2_) {
@@ -312,8 +321,8 @@ struct Step3 {
         i2 = t - (int)q * n2;
         i0 = (int)(q / (unsigned)n1);
         i1 = (int)q - i0 * n1;
-        const unsigned qs = (unsigned)NT / (unsigned)n2;
-        s2 = NT - (int)qs * n2;
+        const unsigned qs = (unsigned)T / (unsigned)n2;
+        s2 = T - (int)qs * n2;
         s0 = (int)(qs / (unsigned)n1);
         s1 = (int)qs - s0 * n1;
     }
@@ -328,15 +337,16 @@ struct Step3 {
     }
 };
 
-// One in-CTA contraction stage: out[(a*O+o)*B+b] = sum_k in[(a*K+k)*B+b] * T[k*tk + o*to]
+// One in-CTA contraction stage: out[(a*O+o)*B+b] = sum_k in[(a*K+k)*B+b] * tab[k*tk + o*to]
+template <int T>
 __device__ __forceinline__ void cstage(const double* __restrict__ in, int A, int K, int B, int O,
-                                       const double* __restrict__ T, int tk, int to,
+                                       const double* __restrict__ tab, int tk, int to,
                                        double* __restrict__ out) {
     const int n = A * O * B;
-    Step3 p(threadIdx.x, O, B);
-    for (int t = threadIdx.x; t < n; t += NT, p.next()) {
+    Step3<T> p(threadIdx.x, O, B);
+    for (int t = threadIdx.x; t < n; t += T, p.next()) {
         const double* src = in + (p.i0 * K) * B + p.i2;
-        const double* tp = T + p.i1 * to;
+        const double* tp = tab + p.i1 * to;
         double S = 0.0;
         for (int k = 0; k < K; ++k) S = fma(src[k * B], tp[k * tk], S);
         out[t] = S;
@@ -345,12 +355,13 @@ __device__ __forceinline__ void cstage(const double* __restrict__ in, int A, int
 }
 
 // Exact stage: out[(a*O+o)*B+b] = log sum_k exp(in[(a*K+k)*B+b] - (p_o - q_k)^2 / eps)
+template <int T>
 __device__ __forceinline__ void xstage(const double* __restrict__ in, int A, int K, int B, int O,
                                        double po, double pdx, int poff, double qo, double qdx,
                                        int qoff, double eps, double* __restrict__ out) {
     const int n = A * O * B;
-    Step3 q(threadIdx.x, O, B);
-    for (int t = threadIdx.x; t < n; t += NT, q.next()) {
+    Step3<T> q(threadIdx.x, O, B);
+    for (int t = threadIdx.x; t < n; t += T, q.next()) {
         const double* src = in + (q.i0 * K) * B + q.i2;
         const double p = po + pdx * (double)(poff + q.i1);
         double m = kNegInf;
@@ -370,42 +381,43 @@ __device__ __forceinline__ void xstage(const double* __restrict__ in, int A, int
 }
 
 struct Sh {
-    double red[NW];
-    int redi[NW];
+    double red[32];
+    int redi[32];
     int flag;
     int ndeg;
 };
 
 // X sweep: L[x] = log sum_y exp(b[y] - c(x,y)/eps), b = beta/eps + lnu.
 // Fast path writes L; returns 1 if an output needed the exact path (then redone).
+template <int T>
 __device__ int sweep_x(const Cell& C, const dd3_geom& g, Sh& sh) {
     const double eps = g.eps;
     const int ny = (int)C.ny, nx = (int)C.nx;
     // b' = b + sum_a c_a(y_a) into z (scratch), and its max
     double mx = kNegInf;
     {
-        Step3 p(threadIdx.x, C.n[1], C.n[2]);
-        for (int y = threadIdx.x; y < ny; y += NT, p.next()) {
+        Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+        for (int y = threadIdx.x; y < ny; y += T, p.next()) {
             const double b = C.beta[y] / eps + C.lnu[y];
             const double bp = b + (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]);
             C.z[y] = bp;
             mx = fmax(mx, bp);
         }
     }
-    double M = bmax(mx, sh.red);
+    double M = bmax<T>(mx, sh.red);
     if (!isfinite(M)) M = 0.0;
-    for (int y = threadIdx.x; y < ny; y += NT) C.z[y] = exp(C.z[y] - M);
+    for (int y = threadIdx.x; y < ny; y += T) C.z[y] = exp(C.z[y] - M);
     if (threadIdx.x == 0) sh.flag = 0;
     __syncthreads();
     // U1[y0,y1,x2] = sum_y2 w * Kn2[x2][y2]; U2[y0,x1,x2]; S[x0,x1,x2]
-    cstage(C.z, C.n[0] * C.n[1], C.n[2], 1, C.w[2], C.kn[2], 1, C.n[2], C.s1);
-    cstage(C.s1, C.n[0], C.n[1], C.w[2], C.w[1], C.kn[1], 1, C.n[1], C.s2);
+    cstage<T>(C.z, C.n[0] * C.n[1], C.n[2], 1, C.w[2], C.kn[2], 1, C.n[2], C.s1);
+    cstage<T>(C.s1, C.n[0], C.n[1], C.w[2], C.w[1], C.kn[1], 1, C.n[1], C.s2);
     int bad = 0;
     {
         const int ob = C.w[1] * C.w[2];
         const int n0 = C.n[0];
-        Step3 p(threadIdx.x, 1, ob);
-        for (int t = threadIdx.x; t < nx; t += NT, p.next()) {
+        Step3<T> p(threadIdx.x, 1, ob);
+        for (int t = threadIdx.x; t < nx; t += T, p.next()) {
             const double* s2 = C.s2 + p.i2;
             const double* kt = C.kn[0] + p.i0 * n0;
             double S = 0.0;
@@ -418,44 +430,45 @@ __device__ int sweep_x(const Cell& C, const dd3_geom& g, Sh& sh) {
     __syncthreads();
     if (!sh.flag) return 0;
     // exact stage-wise path on b = beta/eps + lnu
-    for (int y = threadIdx.x; y < ny; y += NT) C.z[y] = C.beta[y] / eps + C.lnu[y];
+    for (int y = threadIdx.x; y < ny; y += T) C.z[y] = C.beta[y] / eps + C.lnu[y];
     __syncthreads();
     const int* xo = C.xb.o;
     const int* yo = C.yb.o;
-    xstage(C.z, C.n[0] * C.n[1], C.n[2], 1, C.w[2], g.x_org[2], g.x_dx, xo[2], g.y_org[2],
+    xstage<T>(C.z, C.n[0] * C.n[1], C.n[2], 1, C.w[2], g.x_org[2], g.x_dx, xo[2], g.y_org[2],
            g.y_dx, yo[2], eps, C.s1);
-    xstage(C.s1, C.n[0], C.n[1], C.w[2], C.w[1], g.x_org[1], g.x_dx, xo[1], g.y_org[1], g.y_dx,
+    xstage<T>(C.s1, C.n[0], C.n[1], C.w[2], C.w[1], g.x_org[1], g.x_dx, xo[1], g.y_org[1], g.y_dx,
            yo[1], eps, C.s2);
-    xstage(C.s2, 1, C.n[0], C.w[1] * C.w[2], C.w[0], g.x_org[0], g.x_dx, xo[0], g.y_org[0],
+    xstage<T>(C.s2, 1, C.n[0], C.w[1] * C.w[2], C.w[0], g.x_org[0], g.x_dx, xo[0], g.y_org[0],
            g.y_dx, yo[0], eps, C.L);
     return 1;
 }
 
 // Y sweep: z[y] = log sum_x exp(a[x] - c(x,y)/eps), a = alpha/eps + lmu (built into av).
+template <int T>
 __device__ int sweep_y(const Cell& C, const dd3_geom& g, Sh& sh) {
     const double eps = g.eps;
     const int ny = (int)C.ny, nx = (int)C.nx;
     double mx = kNegInf;
-    for (int x = threadIdx.x; x < nx; x += NT) {
+    for (int x = threadIdx.x; x < nx; x += T) {
         const double a = C.alpha[x] / eps + C.lmu[x];
         C.av[x] = a;
         mx = fmax(mx, a);
     }
-    double M = bmax(mx, sh.red);
+    double M = bmax<T>(mx, sh.red);
     if (!isfinite(M)) M = 0.0;
     // shifted weights into L (rebuilt by the next X sweep)
-    for (int x = threadIdx.x; x < nx; x += NT) C.L[x] = exp(C.av[x] - M);
+    for (int x = threadIdx.x; x < nx; x += T) C.L[x] = exp(C.av[x] - M);
     if (threadIdx.x == 0) sh.flag = 0;
     __syncthreads();
     // T1[x0,x1,y2] = sum_x2 w * Kn2[x2][y2]; T2[x0,y1,y2]; S[y0,y1,y2]
-    cstage(C.L, C.w[0] * C.w[1], C.w[2], 1, C.n[2], C.kn[2], C.n[2], 1, C.s1);
-    cstage(C.s1, C.w[0], C.w[1], C.n[2], C.n[1], C.kn[1], C.n[1], 1, C.s2);
+    cstage<T>(C.L, C.w[0] * C.w[1], C.w[2], 1, C.n[2], C.kn[2], C.n[2], 1, C.s1);
+    cstage<T>(C.s1, C.w[0], C.w[1], C.n[2], C.n[1], C.kn[1], C.n[1], 1, C.s2);
     int bad = 0;
     {
         const int ob = C.n[1] * C.n[2];
         const int n0 = C.n[0], w0 = C.w[0];
-        Step3 p(threadIdx.x, C.n[1], C.n[2]);
-        for (int t = threadIdx.x; t < ny; t += NT, p.next()) {
+        Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+        for (int t = threadIdx.x; t < ny; t += T, p.next()) {
             const double* s2 = C.s2 + (p.i1 * C.n[2] + p.i2);
             const double* kt = C.kn[0] + p.i0;
             double S = 0.0;
@@ -469,19 +482,20 @@ __device__ int sweep_y(const Cell& C, const dd3_geom& g, Sh& sh) {
     if (!sh.flag) return 0;
     const int* xo = C.xb.o;
     const int* yo = C.yb.o;
-    xstage(C.av, C.w[0] * C.w[1], C.w[2], 1, C.n[2], g.y_org[2], g.y_dx, yo[2], g.x_org[2],
+    xstage<T>(C.av, C.w[0] * C.w[1], C.w[2], 1, C.n[2], g.y_org[2], g.y_dx, yo[2], g.x_org[2],
            g.x_dx, xo[2], eps, C.s1);
-    xstage(C.s1, C.w[0], C.w[1], C.n[2], C.n[1], g.y_org[1], g.y_dx, yo[1], g.x_org[1], g.x_dx,
+    xstage<T>(C.s1, C.w[0], C.w[1], C.n[2], C.n[1], g.y_org[1], g.y_dx, yo[1], g.x_org[1], g.x_dx,
            xo[1], eps, C.s2);
-    xstage(C.s2, 1, C.w[0], C.n[1] * C.n[2], C.n[0], g.y_org[0], g.y_dx, yo[0], g.x_org[0],
+    xstage<T>(C.s2, 1, C.w[0], C.n[1] * C.n[2], C.n[0], g.y_org[0], g.y_dx, yo[0], g.x_org[0],
            g.x_dx, xo[0], eps, C.z);
     return 1;
 }
 
 // lam-free gap sum (sinkhorn.py:336-351) over the X window
+template <int T>
 __device__ double gap_sum(const Cell& C, const dd3_geom& g, Sh& sh) {
     double s = 0.0;
-    for (int64_t x = threadIdx.x; x < C.nx; x += NT) {
+    for (int64_t x = threadIdx.x; x < C.nx; x += T) {
         const double mu = C.mu[x];
         if (mu > 0) {
             const double a = C.alpha[x];
@@ -491,7 +505,7 @@ __device__ double gap_sum(const Cell& C, const dd3_geom& g, Sh& sh) {
             s += px * (lr + a / g.lam) - px + ref;
         }
     }
-    return bsum(s, sh.red);
+    return bsum<T>(s, sh.red);
 }
 
 __device__ __forceinline__ double coord(const double* org, double dx, int a, int idx) {
@@ -522,8 +536,9 @@ __device__ __forceinline__ void member_block(const dd3_state& s, const Cell& C, 
 #ifndef DD3_MIN_BLOCKS
 #define DD3_MIN_BLOCKS 2   // resident cell CTAs per SM (2: <= 128 registers, no spills)
 #endif
-__global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geom g, dd3_state s,
-                                                                         dd3_batch b) {
+template <int T>
+__global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
+    cell_solve3_kernel(dd3_geom g, dd3_state s, dd3_batch b) {
     __shared__ Sh sh;
     __shared__ double smem_d[64 * 6];
     const int c = blockIdx.x;
@@ -550,7 +565,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
     const int has = s.d_has[j];
     // X window (cells.py:188 extract_window, fill 0 off the grid)
     double ms = 0.0;
-    for (int64_t x = threadIdx.x; x < C.nx; x += NT) {
+    for (int64_t x = threadIdx.x; x < C.nx; x += T) {
         int x0, x1, x2;
         unflat(x, C.w[1], C.w[2], x0, x1, x2);
         const int r0 = C.xb.o[0] + x0, r1 = C.xb.o[1] + x1, r2 = C.xb.o[2] + x2;
@@ -565,12 +580,12 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         C.alpha[x] = has ? s.d_alpha[(int64_t)j * C.nx + x] : 0.0;
         ms += mu;
     }
-    const double mass = bsum(ms, sh.red);
+    const double mass = bsum<T>(ms, sh.red);
     // member blocks and the old member boxes
     int* mlo = (int*)smem_d;                     // [64*3]
     int* mbe = mlo + 64 * 3;                     // [64*3]
     __shared__ int32_t sobox[64 * 6];
-    for (int k = threadIdx.x; k < n_mem; k += NT) {
+    for (int k = threadIdx.x; k < n_mem; k += T) {
         const int i = b.members[mb + k];
         member_block(s, C, i, mlo + 3 * k, mbe + 3 * k);
         for (int q = 0; q < 6; ++q) sobox[k * 6 + q] = s.ybox[(int64_t)i * 6 + q];
@@ -589,7 +604,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
     if (has) db = ldbox(s.d_box + (int64_t)j * 6);
     const double* dbeta = s.d_beta + (int64_t)j * s.d_cap;
     int nclamp = 0;
-    for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
+    for (int64_t y = threadIdx.x; y < C.ny; y += T) {
         int y0, y1, y2;
         unflat(y, C.n[1], C.n[2], y0, y1, y2);
         const int r0 = C.yb.o[0] + y0, r1 = C.yb.o[1] + y1, r2 = C.yb.o[2] + y2;
@@ -615,7 +630,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
     // per-axis Y-normalised tables Kn_a[x_a][y_a] = exp(-(d^2)/eps - c_a(y_a)),
     // c_a(y_a) = max over x_a of -(d^2)/eps
     for (int a = 0; a < 3; ++a) {
-        for (int ya = threadIdx.x; ya < C.n[a]; ya += NT) {
+        for (int ya = threadIdx.x; ya < C.n[a]; ya += T) {
             const double yc = coord(g.y_org, g.y_dx, a, C.yb.o[a] + ya);
             double cm = kNegInf;
             for (int xa = 0; xa < C.w[a]; ++xa) {
@@ -629,14 +644,14 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
             }
         }
     }
-    const int nclamped = (int)bsum((double)nclamp, sh.red);   // (barrier)
+    const int nclamped = (int)bsum<T>((double)nclamp, sh.red);   // (barrier)
     if (!(mass > 0)) {
         // zero-mass cell: untouched, converged (cells.py:245-264)
-        for (int64_t x = threadIdx.x; x < C.nx; x += NT) b.alpha[(int64_t)c * C.nx + x] = C.alpha[x];
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) b.beta[yoff + y] = C.beta[y];
-        for (int64_t t = threadIdx.x; t < 2 * (int64_t)n_mem * C.ny; t += NT) R[t] = 0.0;
-        for (int64_t t = threadIdx.x; t < (int64_t)n_mem * bs; t += NT) b.xarena[xoff + t] = 0.0;
-        for (int k = threadIdx.x; k < n_mem; k += NT) {
+        for (int64_t x = threadIdx.x; x < C.nx; x += T) b.alpha[(int64_t)c * C.nx + x] = C.alpha[x];
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) b.beta[yoff + y] = C.beta[y];
+        for (int64_t t = threadIdx.x; t < 2 * (int64_t)n_mem * C.ny; t += T) R[t] = 0.0;
+        for (int64_t t = threadIdx.x; t < (int64_t)n_mem * bs; t += T) b.xarena[xoff + t] = 0.0;
+        for (int k = threadIdx.x; k < n_mem; k += T) {
             for (int q = 0; q < 6; ++q) b.mbox[(int64_t)(mb + k) * 6 + q] = 0;
             for (int q = 0; q < 4; ++q) b.mstat[(int64_t)(mb + k) * 4 + q] = 0.0;
         }
@@ -653,19 +668,19 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
     bool conv = false, have_first = false;
     int iters = 0, ndeg_max = 0, nfb = 0;
     for (int k = 1; k <= b.max_iters; ++k) {
-        nfb += sweep_x(C, g, sh);
+        nfb += sweep_x<T>(C, g, sh);
         if (k >= 2) {
-            const double gg = lam * gap_sum(C, g, sh);
+            const double gg = lam * gap_sum<T>(C, g, sh);
             if (!have_first) { first_g = gg; have_first = true; }
             if (gg / lam <= thr) { gap = gg; conv = true; break; }
         }
-        for (int64_t x = threadIdx.x; x < C.nx; x += NT) C.alpha[x] = -ratio * C.L[x];
+        for (int64_t x = threadIdx.x; x < C.nx; x += T) C.alpha[x] = -ratio * C.L[x];
         __syncthreads();
-        nfb += sweep_y(C, g, sh);
+        nfb += sweep_y<T>(C, g, sh);
         if (threadIdx.x == 0) sh.ndeg = 0;
         __syncthreads();
         int nd = 0;
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) {
             int deg = 0;
             C.beta[y] = dd::newton_node(C.z[y], C.m[y], true, C.beta[y], eps, lam, b.newton_tol,
                                         b.newton_max_iters, &deg, nullptr, nullptr, C.lm[y]);
@@ -677,18 +692,18 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         iters = k;
     }
     if (!conv) {
-        nfb += sweep_x(C, g, sh);
-        const double gg = lam * gap_sum(C, g, sh);
+        nfb += sweep_x<T>(C, g, sh);
+        const double gg = lam * gap_sum<T>(C, g, sh);
         gap = gg;
         if (!have_first) first_g = gg;
         conv = gg / lam <= thr;
     }
     // ---- epilogue: split by members (cells.py:350-393)
     // mu_bar = exp(-alpha'/lam) mu, alpha' = -ratio L (the extra X half-step)
-    for (int64_t x = threadIdx.x; x < C.nx; x += NT)
+    for (int64_t x = threadIdx.x; x < C.nx; x += T)
         C.av[x] = exp(-(-ratio * C.L[x]) / lam) * C.mu[x];
     __syncthreads();
-    for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
+    for (int64_t y = threadIdx.x; y < C.ny; y += T) {
         int y0, y1, y2;
         unflat(y, C.n[1], C.n[2], y0, y1, y2);
         const double bt = C.beta[y] / eps;
@@ -727,15 +742,15 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         const int* be = mbe + 3 * k;
         const int nb = be[0] * be[1] * be[2];
         double p = 0.0;
-        for (int t = threadIdx.x; t < nb; t += NT) {
+        for (int t = threadIdx.x; t < nb; t += T) {
             int t0, t1, t2;
             unflat(t, be[1], be[2], t0, t1, t2);
             p += C.av[((int64_t)(lo[0] + t0) * C.w[1] + lo[1] + t1) * C.w[2] + lo[2] + t2];
         }
-        const double mbar = bsum(p, sh.red);
+        const double mbar = bsum<T>(p, sh.red);
         double q = 0.0;
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) q += V[(int64_t)k * C.ny + y];
-        const double mk = bsum(q, sh.red);
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) q += V[(int64_t)k * C.ny + y];
+        const double mk = bsum<T>(q, sh.red);
         if (threadIdx.x == 0) { s_mbar[k] = mbar; s_mass[k] = mk; }
     }
     __syncthreads();
@@ -757,7 +772,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
     const bool moved = s_moved != 0;
     if (moved) {
         // column sums before (sequential over members) into z
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) {
             double cs = V[y];
             for (int k = 1; k < n_mem; ++k) cs = __dadd_rn(cs, V[(int64_t)k * C.ny + y]);
             C.z[y] = cs;
@@ -807,12 +822,12 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         }
         __syncthreads();
         // clip, then restore every column's sum bitwise (cells.py:505-545)
-        for (int64_t t = threadIdx.x; t < (int64_t)n_mem * C.ny; t += NT) V[t] = fmax(V[t], 0.0);
+        for (int64_t t = threadIdx.x; t < (int64_t)n_mem * C.ny; t += T) V[t] = fmax(V[t], 0.0);
         __syncthreads();
     }
     int drift = 0;
     if (moved) {
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) {
             const double target = C.z[y];
             double* col = V + y;
             const int64_t st = C.ny;
@@ -848,13 +863,13 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
             if (!ok) ++drift;
         }
     }
-    const int drift_nodes = (int)bsum((double)drift, sh.red);
+    const int drift_nodes = (int)bsum<T>((double)drift, sh.red);
     // balance_target_miss
     double miss = 0.0;
     for (int k = 0; k < n_mem; ++k) {
         double q = 0.0;
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) q += V[(int64_t)k * C.ny + y];
-        const double mk = bsum(q, sh.red);
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) q += V[(int64_t)k * C.ny + y];
+        const double mk = bsum<T>(q, sh.red);
         miss = fmax(miss, fabs(mk - s_tgt[k]) / fmax(s_tgt[k], 1e-300));
     }
     // ---- finalize (cells.py:396-443): truncate, fragments, x-marginals
@@ -867,7 +882,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         double rem = 0.0, s_ftc = 0.0, s_emc = 0.0, s_ftl = 0.0, s_xl = 0.0, s_fin = 0.0,
                s_ext = 0.0;
         int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = -1, hi1 = -1, hi2 = -1;
-        for (int64_t y = threadIdx.x; y < C.ny; y += NT) {
+        for (int64_t y = threadIdx.x; y < C.ny; y += T) {
             int y0, y1, y2;
             unflat(y, C.n[1], C.n[2], y0, y1, y2);
             const double v = Vk[y];
@@ -899,15 +914,15 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
             Vk[y] = fin;
             Rk[y] = f;
         }
-        rem = bsum(rem, sh.red);
-        s_ftc = bsum(s_ftc, sh.red);
-        s_emc = bsum(s_emc, sh.red);
-        s_ftl = bsum(s_ftl, sh.red);
-        s_xl = bsum(s_xl, sh.red);
-        s_fin = bsum(s_fin, sh.red);
-        s_ext = bsum(s_ext, sh.red);
-        lo0 = bmin_i(lo0, sh.redi); lo1 = bmin_i(lo1, sh.redi); lo2 = bmin_i(lo2, sh.redi);
-        hi0 = bmax_i(hi0, sh.redi); hi1 = bmax_i(hi1, sh.redi); hi2 = bmax_i(hi2, sh.redi);
+        rem = bsum<T>(rem, sh.red);
+        s_ftc = bsum<T>(s_ftc, sh.red);
+        s_emc = bsum<T>(s_emc, sh.red);
+        s_ftl = bsum<T>(s_ftl, sh.red);
+        s_xl = bsum<T>(s_xl, sh.red);
+        s_fin = bsum<T>(s_fin, sh.red);
+        s_ext = bsum<T>(s_ext, sh.red);
+        lo0 = bmin_i<T>(lo0, sh.redi); lo1 = bmin_i<T>(lo1, sh.redi); lo2 = bmin_i<T>(lo2, sh.redi);
+        hi0 = bmax_i<T>(hi0, sh.redi); hi1 = bmax_i<T>(hi1, sh.redi); hi2 = bmax_i<T>(hi2, sh.redi);
         trunc_total += rem;
         if (threadIdx.x == 0) {
             int32_t* nb = b.mbox + (int64_t)(mb + k) * 6;
@@ -928,7 +943,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         const int* lo = mlo + 3 * k;
         const int* be = mbe + 3 * k;
         const int nbk = be[0] * be[1] * be[2];
-        const int P = max(1, NT / max(nbk, 1));
+        const int P = max(1, T / max(nbk, 1));
         const int rowi = threadIdx.x / P, part = threadIdx.x - rowi * P;
         double acc = 0.0;
         int64_t xw = -1;
@@ -950,8 +965,8 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
                 }
             }
         }
-        // rows beyond NT are handled below, one thread per row
-        __shared__ double part_sum[NT];
+        // rows beyond T are handled below, one thread per row
+        __shared__ double part_sum[T];
         __syncthreads();
         part_sum[threadIdx.x] = acc;
         __syncthreads();
@@ -961,7 +976,7 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
             if (s_ext != 0.0) xm = xm + C.mu[xw] * (s_ext / mass_i);
             b.xarena[xoff + (int64_t)k * bs + rowi] = C.mu[xw] > 0 ? xm : 0.0;
         }
-        for (int rr = NT; rr < nbk; rr += NT) {   // blocks above NT nodes: one thread per row
+        for (int rr = T; rr < nbk; rr += T) {   // blocks above T nodes: one thread per row
             const int row = rr + threadIdx.x;
             if (row < nbk) {
                 int t0, t1, t2;
@@ -987,8 +1002,8 @@ __global__ void __launch_bounds__(NT, DD3_MIN_BLOCKS) cell_solve3_kernel(dd3_geo
         __syncthreads();
     }
     // outputs: duals, per-cell statistics
-    for (int64_t x = threadIdx.x; x < C.nx; x += NT) b.alpha[(int64_t)c * C.nx + x] = C.alpha[x];
-    for (int64_t y = threadIdx.x; y < C.ny; y += NT) b.beta[yoff + y] = C.beta[y];
+    for (int64_t x = threadIdx.x; x < C.nx; x += T) b.alpha[(int64_t)c * C.nx + x] = C.alpha[x];
+    for (int64_t y = threadIdx.x; y < C.ny; y += T) b.beta[yoff + y] = C.beta[y];
     if (threadIdx.x == 0) {
         cst[0] = gap; cst[1] = first_g; cst[2] = iters; cst[3] = conv ? 1.0 : 0.0;
         cst[4] = nclamped; cst[5] = ndeg_max; cst[6] = s_fb; cst[7] = miss;
@@ -1702,8 +1717,9 @@ extern "C" int64_t dd3_cell_ws_size(const int32_t* w, const int32_t* n) {
 extern "C" int dd3_cell_solve(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
                               void* stream) {
     if (b->n_cells <= 0) return 0;
-    cudaFuncSetCacheConfig(v3::cell_solve3_kernel, cudaFuncCachePreferL1);
-    v3::cell_solve3_kernel<<<b->n_cells, v3::NT, 0, (cudaStream_t)stream>>>(*g, *s, *b);
+    cudaFuncSetCacheConfig(v3::cell_solve3_kernel<v3::CELL_NT>, cudaFuncCachePreferL1);
+    v3::cell_solve3_kernel<v3::CELL_NT>
+        <<<b->n_cells, v3::CELL_NT, 0, (cudaStream_t)stream>>>(*g, *s, *b);
     return dd_set_error(cudaGetLastError());
 }
 
