@@ -1595,6 +1595,229 @@ __global__ void __launch_bounds__(NT) cut_plan3_kernel(dd3_geom g, dd3_state s,
     if (threadIdx.x < 6) s.ybox[(int64_t)i * 6 + threadIdx.x] = boxes_out[(int64_t)i * 6 + threadIdx.x];
 }
 
+// Factorised plan cut (same outputs as cut_plan3_kernel, to rounding).  With
+// a(x) = alpha/eps + log mu on the block's retained nodes, A = max a, and Y-normalised
+// per-axis tables Kn_a = exp(-d_a^2/eps - c_a(y_a)) (c_a = the column max), every term is
+//   exp((alpha + beta - c)/eps) mu nu = F(y) t(x, y),
+//   F(y) = exp(beta/eps + log nu + A + sum_a c_a(y_a)),  t = exp(a - A) prod_a Kn_a,
+// so a node's column sum, transport and entropy pieces are table products and FMAs
+// instead of one exp per term.  A node whose normalised sum S = sum_x t is below kTiny
+// (its dominant terms may have underflowed) or whose scale F would overflow takes the
+// per-term exact path of cut_plan3_kernel.  Tables live in dynamic shared memory:
+// per axis block_a x ny_a entries of Kn_a and d_a^2, and ny_a column shifts.
+struct CutTabs {
+    const double* K[3];
+    const double* D[3];
+    const double* c[3];
+    int n[3];
+};
+
+__device__ __forceinline__ bool cut_fast(const CutTabs& T, const double* xs_ex, const double* xs_ae,
+                                         const int* xi0, const int* xi1, const int* xi2, int nxn,
+                                         double A, double eps, int y0, int y1, int y2, double bt,
+                                         double lnu, bool stats, double& col, double& trc,
+                                         double& klc, double* xacc) {
+    const double logF = bt / eps + lnu + A + (T.c[0][y0] + T.c[1][y1] + T.c[2][y2]);
+    if (!(logF <= 700.0)) return false;
+    const double* K0 = T.K[0] + y0;
+    const double* K1 = T.K[1] + y1;
+    const double* K2 = T.K[2] + y2;
+    const int n0 = T.n[0], n1 = T.n[1], n2 = T.n[2];
+    double S = 0.0;
+    for (int k = 0; k < nxn; ++k)
+        S += xs_ex[k] * K0[xi0[k] * n0] * K1[xi1[k] * n1] * K2[xi2[k] * n2];
+    if (!(S >= kTiny)) return false;
+    const double F = exp(logF);
+    col = F * S;
+    if (!stats) return true;
+    const double* D0 = T.D[0] + y0;
+    const double* D1 = T.D[1] + y1;
+    const double* D2 = T.D[2] + y2;
+    double Sc = 0.0, Sa = 0.0;
+    for (int k = 0; k < nxn; ++k) {
+        const int i0 = xi0[k] * n0, i1 = xi1[k] * n1, i2 = xi2[k] * n2;
+        const double t = xs_ex[k] * K0[i0] * K1[i1] * K2[i2];
+        Sc = fma(t, D0[i0] + D1[i1] + D2[i2], Sc);
+        Sa = fma(t, xs_ae[k], Sa);
+        xacc[k] = fma(t, F, xacc[k]);
+    }
+    trc = F * Sc;
+    klc = F * Sa + col * (bt / eps) - trc / eps;   // sum_x blk (alpha + beta - c) / eps
+    return true;
+}
+
+__global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
+                                                        const double* alpha, const double* beta,
+                                                        double trunc, double cut_log,
+                                                        const double* tmax, double* trunc_out,
+                                                        int32_t* boxes_out) {
+    extern __shared__ double dsm[];
+    __shared__ double red[NW];
+    __shared__ int redi[NW];
+    __shared__ double xs_a[64], xs_lm[64], xs_mu[64], xs_c0[64], xs_c1[64], xs_c2[64];
+    __shared__ double xs_ex[64], xs_ae[64];
+    __shared__ int xs_t[64], xs_i0[64], xs_i1[64], xs_i2[64];
+    __shared__ int n_sh;
+    __shared__ double s_amax;
+    const int i = blockIdx.x;
+    const B3 bx = ldbox(s.basic_xbox + (int64_t)i * 6);
+    const int bs = s.block[0] * s.block[1] * s.block[2];
+    const double eps = g.eps;
+    if (threadIdx.x == 0) {
+        int n = 0;
+        double am = kNegInf;
+        for (int t = 0; t < bs && n < 64; ++t) {
+            int t0, t1, t2;
+            unflat(t, bx.e[1], bx.e[2], t0, t1, t2);
+            const int xi0 = bx.o[0] + t0, xi1 = bx.o[1] + t1, xi2 = bx.o[2] + t2;
+            const int64_t id = ((int64_t)xi0 * g.nx[1] + xi1) * g.nx[2] + xi2;
+            const double mu = s.mu[id];
+            if (mu > 0) {
+                xs_a[n] = alpha[id];
+                xs_lm[n] = log(mu);
+                xs_mu[n] = mu;
+                xs_c0[n] = coord(g.x_org, g.x_dx, 0, xi0);
+                xs_c1[n] = coord(g.x_org, g.x_dx, 1, xi1);
+                xs_c2[n] = coord(g.x_org, g.x_dx, 2, xi2);
+                xs_i0[n] = t0; xs_i1[n] = t1; xs_i2[n] = t2;
+                xs_t[n] = t;
+                xs_ae[n] = alpha[id] / eps;
+                am = fmax(am, alpha[id] / eps + xs_lm[n]);
+                ++n;
+            }
+        }
+        n_sh = n;
+        s_amax = am;
+        for (int k = 0; k < n; ++k) xs_ex[k] = exp(xs_ae[k] + xs_lm[k] - am);
+    }
+    // per-axis tables over the whole Y axis: Kn_a, d_a^2, column shifts
+    CutTabs T;
+    {
+        double* p = dsm;
+        for (int a = 0; a < 3; ++a) { T.n[a] = g.ny[a]; T.K[a] = p; p += bx.e[a] * g.ny[a]; }
+        for (int a = 0; a < 3; ++a) { T.D[a] = p; p += bx.e[a] * g.ny[a]; }
+        for (int a = 0; a < 3; ++a) { T.c[a] = p; p += g.ny[a]; }
+        for (int a = 0; a < 3; ++a) {
+            double* K = const_cast<double*>(T.K[a]);
+            double* D = const_cast<double*>(T.D[a]);
+            double* cc = const_cast<double*>(T.c[a]);
+            for (int ya = threadIdx.x; ya < g.ny[a]; ya += NT) {
+                const double yc = coord(g.y_org, g.y_dx, a, ya);
+                double cm = kNegInf;
+                for (int xa = 0; xa < bx.e[a]; ++xa) {
+                    const double d = coord(g.x_org, g.x_dx, a, bx.o[a] + xa) - yc;
+                    cm = fmax(cm, -(d * d) / eps);
+                }
+                cc[ya] = cm;
+                for (int xa = 0; xa < bx.e[a]; ++xa) {
+                    const double d = coord(g.x_org, g.x_dx, a, bx.o[a] + xa) - yc;
+                    K[xa * g.ny[a] + ya] = exp(-(d * d) / eps - cm);
+                    D[xa * g.ny[a] + ya] = d * d;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int nxn = n_sh;
+    const double amax = s_amax;
+    double xlo[3], xhi[3];
+    for (int a = 0; a < 3; ++a) {
+        xlo[a] = coord(g.x_org, g.x_dx, a, bx.o[a]);
+        xhi[a] = coord(g.x_org, g.x_dx, a, bx.o[a] + bx.e[a] - 1);
+    }
+    const int tn0 = (g.ny[0] + kCutTile - 1) / kCutTile, tn1 = (g.ny[1] + kCutTile - 1) / kCutTile,
+              tn2 = (g.ny[2] + kCutTile - 1) / kCutTile;
+    const int64_t ntile = (int64_t)tn0 * tn1 * tn2;
+    double xacc[64];
+    for (int k = 0; k < 64; ++k) xacc[k] = 0.0;
+    double mass = 0.0, tr = 0.0, klp = 0.0, rem = 0.0;
+    int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = -1, hi1 = -1, hi2 = -1;
+    for (int64_t t = threadIdx.x; t < ntile; t += NT) {
+        int ta0, ta1, ta2;
+        unflat(t, tn1, tn2, ta0, ta1, ta2);
+        const int yl0 = ta0 * kCutTile, yl1 = ta1 * kCutTile, yl2 = ta2 * kCutTile;
+        const int yh0 = min(g.ny[0], yl0 + kCutTile) - 1, yh1 = min(g.ny[1], yl1 + kCutTile) - 1,
+                  yh2 = min(g.ny[2], yl2 + kCutTile) - 1;
+        const double g0 = gap1(xlo[0], xhi[0], coord(g.y_org, g.y_dx, 0, yl0), coord(g.y_org, g.y_dx, 0, yh0));
+        const double g1 = gap1(xlo[1], xhi[1], coord(g.y_org, g.y_dx, 1, yl1), coord(g.y_org, g.y_dx, 1, yh1));
+        const double g2 = gap1(xlo[2], xhi[2], coord(g.y_org, g.y_dx, 2, yl2), coord(g.y_org, g.y_dx, 2, yh2));
+        const double d2 = g0 * g0 + g1 * g1 + g2 * g2;
+        if (amax + tmax[t] - d2 / eps < cut_log - 1.0) continue;
+        for (int y0 = yl0; y0 <= yh0; ++y0)
+            for (int y1 = yl1; y1 <= yh1; ++y1)
+                for (int y2 = yl2; y2 <= yh2; ++y2) {
+                    const int64_t id = ((int64_t)y0 * g.ny[1] + y1) * g.ny[2] + y2;
+                    const double nu = s.nu[id];
+                    const double lnu = s.log_nu[id];
+                    const double bt = beta[id];
+                    double col, trc = 0.0, klc = 0.0;
+                    if (cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0, y1, y2,
+                                 bt, lnu, true, col, trc, klc, xacc)) {
+                        tr += trc;
+                        klp += klc;
+                    } else {
+                        col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
+                                      coord(g.y_org, g.y_dx, 0, y0), coord(g.y_org, g.y_dx, 1, y1),
+                                      coord(g.y_org, g.y_dx, 2, y2), nu, lnu, bt, cut_log, &tr,
+                                      &klp, xacc);
+                    }
+                    mass += col;
+                    if (col >= trunc) {
+                        lo0 = min(lo0, y0); hi0 = max(hi0, y0);
+                        lo1 = min(lo1, y1); hi1 = max(hi1, y1);
+                        lo2 = min(lo2, y2); hi2 = max(hi2, y2);
+                    } else {
+                        rem += col;
+                    }
+                }
+    }
+    mass = bsum(mass, red);
+    tr = bsum(tr, red);
+    klp = bsum(klp, red);
+    rem = bsum(rem, red);
+    lo0 = bmin_i(lo0, redi); lo1 = bmin_i(lo1, redi); lo2 = bmin_i(lo2, redi);
+    hi0 = bmax_i(hi0, redi); hi1 = bmax_i(hi1, redi); hi2 = bmax_i(hi2, redi);
+    for (int k = threadIdx.x; k < bs; k += NT) s.x_marg[(int64_t)i * bs + k] = 0.0;
+    __syncthreads();
+    for (int k = 0; k < nxn; ++k) {
+        const double v = bsum(xacc[k], red);
+        if (threadIdx.x == 0) s.x_marg[(int64_t)i * bs + xs_t[k]] = v;
+    }
+    __syncthreads();
+    int ne0 = 0, ne1 = 0, ne2 = 0;
+    if (hi0 >= 0) { ne0 = hi0 - lo0 + 1; ne1 = hi1 - lo1 + 1; ne2 = hi2 - lo2 + 1; }
+    if (threadIdx.x == 0) {
+        double mmu = 0.0;
+        for (int k = 0; k < nxn; ++k) mmu += xs_mu[k];
+        s.transport[i] = tr;
+        s.kl[i] = klp - mass + mmu * g.nu_total;
+        trunc_out[i] = rem;
+        int32_t* ob = boxes_out + (int64_t)i * 6;
+        ob[0] = hi0 >= 0 ? lo0 : 0; ob[1] = ne0;
+        ob[2] = hi0 >= 0 ? lo1 : 0; ob[3] = ne1;
+        ob[4] = hi0 >= 0 ? lo2 : 0; ob[5] = ne2;
+    }
+    const int64_t nn = (int64_t)ne0 * ne1 * ne2;
+    if (s.yval == nullptr || nn > s.cap) return;
+    double* v = s.yval + (int64_t)i * s.cap;
+    double dummy[1];
+    for (int64_t t = threadIdx.x; t < nn; t += NT) {
+        int a0, a1, a2;
+        unflat(t, ne1, ne2, a0, a1, a2);
+        const int y0 = lo0 + a0, y1 = lo1 + a1, y2 = lo2 + a2;
+        const int64_t id = ((int64_t)y0 * g.ny[1] + y1) * g.ny[2] + y2;
+        double col, trc, klc;
+        if (!cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0, y1, y2, beta[id],
+                      s.log_nu[id], false, col, trc, klc, dummy))
+            col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
+                          coord(g.y_org, g.y_dx, 0, y0), coord(g.y_org, g.y_dx, 1, y1),
+                          coord(g.y_org, g.y_dx, 2, y2), s.nu[id], s.log_nu[id], beta[id],
+                          cut_log, nullptr, nullptr, nullptr);
+        v[t] = col >= trunc ? col : 0.0;
+    }
+    if (threadIdx.x < 6) s.ybox[(int64_t)i * 6 + threadIdx.x] = boxes_out[(int64_t)i * 6 + threadIdx.x];
+}
+
 __global__ void __launch_bounds__(NT) seed_duals3_kernel(dd3_geom g, dd3_state s, int w0, int w1,
                                                          int w2, const int32_t* xbox,
                                                          const int32_t* ybox, const double* alpha,
@@ -1781,8 +2004,19 @@ extern "C" int dd3_cut_plan(const dd3_geom* g, const dd3_state* s, const double*
     cudaStream_t st = (cudaStream_t)stream;
     v3::cut_tiles_kernel<<<v3_blocks(dd3_cut_tiles(g)), v3::NT, 0, st>>>(*g, beta, s->log_nu,
                                                                           tile_max);
-    v3::cut_plan3_kernel<<<s->n_basic, v3::NT, 0, st>>>(*g, *s, alpha, beta, trunc, cut_log,
-                                                         tile_max, trunc_out, boxes_out);
+    // factorised kernel when its per-axis tables fit shared memory (block_a x ny_a each)
+    int64_t tab = 0;
+    for (int a = 0; a < 3; ++a) tab += 2 * (int64_t)s->block[a] * g->ny[a] + g->ny[a];
+    const int64_t smem = tab * (int64_t)sizeof(double);
+    if (smem <= 160 * 1024 && s->block[0] * s->block[1] * s->block[2] <= 64) {
+        cudaFuncSetAttribute(v3::cut_plan3f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        v3::cut_plan3f_kernel<<<s->n_basic, v3::NT, (size_t)smem, st>>>(
+            *g, *s, alpha, beta, trunc, cut_log, tile_max, trunc_out, boxes_out);
+    } else {
+        v3::cut_plan3_kernel<<<s->n_basic, v3::NT, 0, st>>>(*g, *s, alpha, beta, trunc, cut_log,
+                                                             tile_max, trunc_out, boxes_out);
+    }
     return dd_set_error(cudaGetLastError());
 }
 

@@ -570,7 +570,12 @@ def warm_start_plan3(problem: TransportProblem, partitions: Decomposition, delta
     dp = dp if dp is not None else VolumeProblem(problem)
     if cut_log is None:
         cut_log = -60.0 if dp.ny >= 64 ** 3 else -800.0
+    import torch as _t
+    _t.cuda.synchronize()
+    t0 = time.perf_counter()
     res = sinkhorn_solve(dp, alpha0, beta0, config=SolverConfig(delta=delta, max_iters=max_iters))
+    _t.cuda.synchronize()
+    t1 = time.perf_counter()
     st = PlanState3(problem, partitions.basic, dp, cap=1)
     L = _lib.lib()
     trunc_out = torch.zeros(st.n_basic, dtype=torch.float64, device=dp.device)
@@ -589,6 +594,8 @@ def warm_start_plan3(problem: TransportProblem, partitions: Decomposition, delta
                               _lib.stream_handle()))
     st.sync_boxes()
     st.truncated_mass = float(trunc_out.sum().item())
+    st.warm_timing = {"presolve_s": t1 - t0, "presolve_iters": int(res.iterations),
+                      "cut_s": time.perf_counter() - t1}
     _seed_stores(st, partitions, res.alpha, res.beta)
     st.global_duals = (res.alpha.clone(), res.beta.clone())
     st.presolve = res
@@ -1052,6 +1059,7 @@ def multiscale_solve3(problem: TransportProblem, cell_size: int, n_coarsest: int
         state = warm_start_plan3(prob, dec, delta=gdelta, max_iters=switch_iters, dp=dp,
                                  alpha0=a0, beta0=b0)
         timings["warm"] += time.perf_counter() - t0
+        timings.update({f"warm_{k}": v for k, v in getattr(state, "warm_timing", {}).items()})
         for eps in eps_list:
             prob = TransportProblem(prob.mu, prob.nu, problem.div, eps)
             state.problem = prob
