@@ -76,40 +76,58 @@ class CompositePartition:
         return [i for i in self.cells[j] if i < self.n_basic]
 
 
+def _blocks(arr: np.ndarray, s: int) -> np.ndarray:
+    """(n_blocks, s^d) view-copy of an s^d-blocked array: blocks in row-major lattice
+    order, nodes row-major inside each block (the order of itertools.product loops)."""
+    d = arr.ndim
+    lat = tuple(n // s for n in arr.shape)
+    shp = []
+    for n in lat:
+        shp += [n, s]
+    perm = tuple(range(0, 2 * d, 2)) + tuple(range(1, 2 * d, 2))
+    return arr.reshape(shp).transpose(perm).reshape(int(np.prod(lat)), s ** d)
+
+
 def build_basic_partition(mu: GridMeasure, s: int) -> BasicPartition:
+    """s^d blocks of the grid, zero-mass blocks dropped (partitions.py:77-118); built with
+    whole-array operations (the same cells, order, node lists and masses as a
+    block-by-block loop)."""
     grid = mu.grid
     dims = grid.dims
     if s < 1 or any(n % s for n in dims):
         raise ValueError(f"cell size {s} must divide the grid dims {dims}")
     lat = tuple(n // s for n in dims)
-    flat = np.arange(mu.mass.size).reshape(dims)
-    lattice_to_cell = np.full(lat, -1, dtype=np.int64)
-    nodes, boxes, masses, positions = [], [], [], []
-    n_dropped = 0
-    for pos in product(*[range(n) for n in lat]):
-        sl = tuple(slice(p * s, p * s + s) for p in pos)
-        blk = mu.mass[sl]
-        keep = blk > 0
-        if not keep.any():
-            n_dropped += 1
-            continue
-        lattice_to_cell[pos] = len(nodes)
-        nodes.append(flat[sl][keep].ravel())
-        boxes.append(tuple((p * s, s) for p in pos))
-        masses.append(float(blk.sum()))
-        positions.append(pos)
+    mass = np.asarray(mu.mass)
+    flat = np.arange(mass.size).reshape(dims)
+    blk_mass = _blocks(mass, s)
+    blk_ids = _blocks(flat, s)
+    keep = blk_mass > 0
+    live = keep.any(axis=1)
+    n_dropped = int((~live).sum())
     if n_dropped:
-        logger.warning("dropped %d of %d zero-mass basic cells", n_dropped, n_dropped + len(nodes))
-    if not nodes:
+        logger.warning("dropped %d of %d zero-mass basic cells", n_dropped, len(live))
+    if not live.any():
         raise ValueError("no basic cell has positive mass")
-    cell_of_node = np.full(mu.mass.size, -1, dtype=np.int64)
-    for c, ids in enumerate(nodes):
-        cell_of_node[ids] = c
+    which = np.flatnonzero(live)
+    lattice_to_cell = np.full(len(live), -1, dtype=np.int64)
+    lattice_to_cell[which] = np.arange(len(which))
+    lattice_to_cell = lattice_to_cell.reshape(lat)
+    kept = keep[which]
+    counts = kept.sum(axis=1)
+    ids = blk_ids[which][kept]
+    nodes = np.split(ids, np.cumsum(counts)[:-1])
+    # block masses: numpy sums a strided block through a contiguous buffer, so the row
+    # sums equal the reference's float(block.sum()) bitwise (checked in the host tests)
+    sl_mass = blk_mass[which].sum(axis=1)
+    positions = np.stack(np.unravel_index(which, lat), axis=1).astype(np.int64)
+    boxes = [tuple((p, s) for p in row) for row in (positions * s).tolist()]
+    cell_of_node = np.full(mass.size, -1, dtype=np.int64)
+    cell_of_node[ids] = np.repeat(np.arange(len(which)), counts)
     return BasicPartition(
         grid=grid, s=s, cell_of_node=cell_of_node, nodes_of_cell=nodes, cell_boxes=boxes,
         lattice_dims=lat, lattice_to_cell=lattice_to_cell,
-        positions=np.array(positions, dtype=np.int64).reshape(len(nodes), len(dims)),
-        masses=np.asarray(masses, dtype=np.float64),
+        positions=positions.reshape(len(which), len(dims)),
+        masses=np.asarray(sl_mass, dtype=np.float64),
     )
 
 
@@ -123,25 +141,27 @@ def build_staggered_batches(part: CompositePartition, ndim: int) -> list:
 
 
 def _group(basic: BasicPartition, starts: list, label: str) -> CompositePartition:
+    """Composite cells of 2^d blocks at the given per-axis starts (partitions.py:121-157):
+    member slots row-major over the 2-per-axis window, padding ids numbered in slot order
+    over every window (kept or not), windows without a real member dropped."""
     s, lat, d = basic.s, basic.lattice_dims, basic.ndim
-    pad = basic.n_cells
-    cells, boxes, positions = [], [], []
-    for cpos in product(*[range(len(st)) for st in starts]):
-        origin = tuple(starts[a][cpos[a]] for a in range(d))
-        slots, real = [], 0
-        for off in product(range(2), repeat=d):
-            b = tuple(o + k for o, k in zip(origin, off))
-            cid = int(basic.lattice_to_cell[b]) if all(0 <= p < n for p, n in zip(b, lat)) else -1
-            if cid < 0:
-                slots.append(pad)
-                pad += 1
-            else:
-                slots.append(cid)
-                real += 1
-        if real:
-            cells.append(slots)
-            boxes.append(tuple((o * s, 2 * s) for o in origin))
-            positions.append(cpos)
+    grids = np.meshgrid(*[np.asarray(st, dtype=np.int64) for st in starts], indexing="ij")
+    origin = np.stack([g.ravel() for g in grids], axis=1)                # (nc, d)
+    cgrid = np.meshgrid(*[np.arange(len(st)) for st in starts], indexing="ij")
+    cpos = np.stack([g.ravel() for g in cgrid], axis=1)
+    offs = np.array(list(product(range(2), repeat=d)), dtype=np.int64)   # (2^d, d)
+    b = origin[:, None, :] + offs[None, :, :]                           # (nc, 2^d, d)
+    inside = np.all((b >= 0) & (b < np.asarray(lat)), axis=2)
+    bc = np.clip(b, 0, np.asarray(lat) - 1)
+    cid = np.where(inside, basic.lattice_to_cell[tuple(bc[..., a] for a in range(d))], -1)
+    pad_flag = cid < 0
+    pad_ids = basic.n_cells + np.cumsum(pad_flag.ravel()).reshape(pad_flag.shape) - 1
+    slots = np.where(pad_flag, pad_ids, cid)
+    real = (~pad_flag).sum(axis=1)
+    keep = np.flatnonzero(real > 0)
+    cells = slots[keep].tolist()
+    boxes = [tuple((int(o) * s, 2 * s) for o in origin[j]) for j in keep]
+    positions = [tuple(int(x) for x in cpos[j]) for j in keep]
     part = CompositePartition(label, cells, boxes, positions, [], basic.n_cells)
     return CompositePartition(label, cells, boxes, positions, build_staggered_batches(part, d),
                               basic.n_cells)

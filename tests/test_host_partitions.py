@@ -92,3 +92,30 @@ def test_staggered_batches_have_no_adjacent_cells(lat, seed):
 def test_make_decomposition_single_partition():
     dec = make_decomposition(measure((16, 16)), 4, single_partition=True)
     assert len(dec.composites) == 1 and dec.composites[0].label == "A"
+
+
+@pytest.mark.parametrize("shape,s", [((64, 64), 8), ((16, 16, 16), 4), ((12, 8), 4), ((32,), 2)])
+def test_vectorised_basic_partition_matches_block_loop(shape, s):
+    """The whole-array builder gives the block-by-block loop's cells, node lists and
+    masses bitwise (partitions.py:77-118 restated as a loop)."""
+    rng = np.random.default_rng(7)
+    m = rng.uniform(0.0, 1.0, shape) ** 3
+    m[rng.uniform(size=shape) < 0.1] = 0.0
+    mu = GridMeasure(Grid(shape, 1.0 / shape[-1], (0.0,) * len(shape)), m)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        basic = build_basic_partition(mu, s)
+    lat = tuple(n // s for n in shape)
+    flat = np.arange(m.size).reshape(shape)
+    nodes, masses, boxes = [], [], []
+    for pos in itertools.product(*(range(n) for n in lat)):
+        sl = tuple(slice(p * s, p * s + s) for p in pos)
+        keep = m[sl] > 0
+        if not keep.any():
+            continue
+        nodes.append(flat[sl][keep].ravel())
+        masses.append(float(m[sl].sum()))
+        boxes.append(tuple((p * s, s) for p in pos))
+    assert basic.cell_boxes == boxes
+    assert np.array_equal(basic.masses, np.array(masses))
+    assert all(np.array_equal(a, b) for a, b in zip(basic.nodes_of_cell, nodes))
