@@ -310,6 +310,7 @@ int dd_grid_kl(int64_t n, const double* y, const double* nu, int clip, double* p
  *
  * Reference interfaces replaced (pkg/src/domdec/):
  *   dd3_grid_lse       sinkhorn.py:133-175   SeparableKernel.lse_x / lse_y (three axes)
+ *   dd3_sinkhorn_run   sinkhorn.py:361-432   sinkhorn_solve (device-side iteration loop)
  *   dd3_prolong        SPEC multiscale       trilinear prolongation of duals
  *   dd3_cell_solve     cells.py:165-443      make_cell_problems + solve_cell_batch +
  *                                            balance_cell_masses + _finalize
@@ -394,6 +395,15 @@ int64_t dd3_grid_ws(const dd3_geom* g);
  * eps and direction built. */
 int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
                  int tables_ready, void* stream);
+/* Global unbalanced Sinkhorn on the device over three axes (dd_sinkhorn_run's contract):
+ * iterations k0 .. k0+n_iters-1 enqueued without host synchronisation, stopping test on
+ * the device (ctl_i[0] stopped, ctl_i[1] iterations, ctl_d[0] gap); work holds
+ * dd3_sinkhorn_ws(g) doubles (grid-LSE tables built when tables_ready == 0). */
+int64_t dd3_sinkhorn_ws(const dd3_geom* g);
+int dd3_sinkhorn_run(const dd3_geom* g, double* alpha, double* beta, const double* mu,
+                     const double* log_mu, const double* log_nu, double* L, double* z, double* bv,
+                     double* av, double* px, double* work, int* ctl_i, double* ctl_d, double thr,
+                     int k0, int n_iters, int tables_ready, void* stream);
 /* Trilinear prolongation of a cell-centred coarse field to the x2 finer grid. */
 int dd3_prolong(const int32_t* nf, const int32_t* nc, const double* coarse, double* fine,
                 void* stream);

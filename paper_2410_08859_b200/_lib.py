@@ -27,7 +27,7 @@ EXPORTS = [
     # three-axis path (csrc/vol.cu)
     "dd3_grid_ws", "dd3_grid_lse", "dd3_prolong", "dd3_cell_ws_size", "dd3_cell_solve",
     "dd3_cell_delta", "dd3_cell_commit", "dd3_gather", "dd3_cell_terms", "dd3_product_init",
-    "dd3_cut_tiles", "dd3_cut_plan", "dd3_seed_duals",
+    "dd3_cut_tiles", "dd3_cut_plan", "dd3_seed_duals", "dd3_sinkhorn_ws", "dd3_sinkhorn_run",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -99,6 +99,9 @@ _SIGS = {
     "dd3_cut_tiles": ([G3], i64),
     "dd3_cut_plan": ([G3, S3, vp, vp, dbl, dbl, vp, vp, vp, vp], C.c_int),
     "dd3_seed_duals": ([G3, S3, C.c_int, vp, vp, vp, vp, vp, vp], C.c_int),
+    "dd3_sinkhorn_ws": ([G3], i64),
+    "dd3_sinkhorn_run": ([G3, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, dbl, C.c_int,
+                          C.c_int, C.c_int, vp], C.c_int),
     "dd_last_error": ([], C.c_char_p),
     "dd_device_count": ([], C.c_int),
     "dd_abi_version": ([], C.c_int),
@@ -183,12 +186,18 @@ KERNELS_PER_CALL = {
 
 
 # entry points whose kernel count depends on the arguments
-VARIABLE_LAUNCHES = {"dd_sinkhorn_run", "dd_sinkhorn_ws", "dd_sweep_fallbacks"}
+VARIABLE_LAUNCHES = {"dd_sinkhorn_run", "dd_sinkhorn_ws", "dd_sweep_fallbacks", "dd3_sinkhorn_run",
+                     "dd3_sinkhorn_ws"}
 
 
 def _sinkhorn_run_launches(args) -> int:
     k0, n, tables_ready = int(args[15]), int(args[16]), int(args[17])
     return 10 * n + 2 * (n - (1 if k0 == 1 else 0)) + (0 if tables_ready else 4)
+
+
+def _sinkhorn3_run_launches(args) -> int:
+    k0, n, tables_ready = int(args[15]), int(args[16]), int(args[17])
+    return 16 * n + 2 * (n - (1 if k0 == 1 else 0)) + (0 if tables_ready else 6)
 
 
 class Tracer:
@@ -237,6 +246,7 @@ class _Traced:
                                                                "dd_sinkhorn_ws",
                                                                "dd_sweep_fallbacks",
                                                                "dd3_grid_ws", "dd3_cut_tiles",
+                                                               "dd3_sinkhorn_ws",
                                                                "dd3_cell_ws_size"):
             return fn
 
@@ -244,6 +254,8 @@ class _Traced:
             t.calls[name] = t.calls.get(name, 0) + 1
             if name == "dd_sinkhorn_run":
                 t.extra += _sinkhorn_run_launches(args)
+            elif name == "dd3_sinkhorn_run":
+                t.extra += _sinkhorn3_run_launches(args)
             if name in t.timed:
                 import torch
                 a = torch.cuda.Event(enable_timing=True)

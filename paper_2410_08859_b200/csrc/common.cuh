@@ -261,3 +261,14 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
 int dd_box_gather(int n, const int32_t* box, int bstride, const double* vals, int64_t vstride,
                   const int64_t* voff, int voff_stride, const double* scale, int ny0, int ny1,
                   const double* base, double* out, cudaStream_t st);
+
+// Stop-aware element-wise pieces of one global Sinkhorn iteration (grid.cu), for the
+// three-axis device loop (vol.cu); library-internal.
+int dd_sk_axpb(int64_t n, const double* a, double s, const double* b, double* out, int divide,
+               const int* stop, cudaStream_t st);
+int dd_sk_gap(int64_t nx, const double* alpha, const double* L, const double* mu, double eps,
+              double lam, double* px, double* partial, double thr, int* ctl_i, double* ctl_d,
+              cudaStream_t st);
+int dd_sk_newton(int64_t ny, const double* z, double ratio, double lam, double* beta, int* ctl_i,
+                 int k, cudaStream_t st);
+int64_t dd_sk_partial_doubles();

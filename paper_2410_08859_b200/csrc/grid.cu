@@ -898,6 +898,32 @@ extern "C" int dd_sinkhorn_run(const dd_geom* g, double* alpha, double* beta, co
     return 0;
 }
 
+// Library-internal (vol.cu, the three-axis device loop): the element-wise pieces of one
+// global Sinkhorn iteration, with the device stop flag of dd_sinkhorn_run.
+int dd_sk_axpb(int64_t n, const double* a, double s, const double* b, double* out, int divide,
+               const int* stop, cudaStream_t st) {
+    dd::axpb_kernel<<<grid_blocks(n), DD_NT, 0, st>>>(n, a, s, b, out, divide, stop);
+    return dd_set_error(cudaGetLastError());
+}
+
+int dd_sk_gap(int64_t nx, const double* alpha, const double* L, const double* mu, double eps,
+              double lam, double* px, double* partial, double thr, int* ctl_i, double* ctl_d,
+              cudaStream_t st) {
+    dd::terms_kernel<<<dd::kRedBlocks, DD_NT, 0, st>>>(0, nx, 0, alpha, L, mu, nullptr, nullptr,
+                                                      nullptr, eps, lam, px, partial, ctl_i);
+    dd::sk_check_kernel<<<1, DD_NT, 0, st>>>(partial, lam, thr, ctl_i, ctl_d);
+    return dd_set_error(cudaGetLastError());
+}
+
+int dd_sk_newton(int64_t ny, const double* z, double ratio, double lam, double* beta, int* ctl_i,
+                 int k, cudaStream_t st) {
+    dd::newton_global_kernel<<<grid_blocks(ny), DD_NT, 0, st>>>(ny, z, ratio, lam, beta, nullptr,
+                                                                ctl_i, ctl_i + 1, k);
+    return dd_set_error(cudaGetLastError());
+}
+
+int64_t dd_sk_partial_doubles() { return 3 * (int64_t)dd::kRedBlocks; }
+
 extern "C" int dd_axpb(int64_t n, const double* a, double s, const double* b, double* out,
                        int divide, void* stream) {
     dd::axpb_kernel<<<grid_blocks(n), DD_NT, 0, (cudaStream_t)stream>>>(n, a, s, b, out, divide);

@@ -151,6 +151,7 @@ struct GStage {
     const double* tab;  // exp table [O*K]
     int A, K, B, O;
     double p_org, p_dx, q_org, q_dx, eps;
+    const int* stop;    // nullable: device flag of the device-side Sinkhorn loop
 };
 
 // tab[k*O + o] = exp(-(d*d)/eps), d = p_o - q_k  (o fastest: coalesced across outputs)
@@ -166,6 +167,7 @@ __global__ void g_table_kernel(int O, int K, double po, double pd, double qo, do
 }
 
 __global__ void g_rows_kernel(GStage s) {
+    if (s.stop && *s.stop) return;
     const int64_t rows = (int64_t)s.A * s.B;
     if (s.B == 1) {
         // contiguous rows: one warp per row (coalesced)
@@ -198,6 +200,7 @@ __global__ void g_rows_kernel(GStage s) {
 }
 
 __global__ void g_contract_kernel(GStage s) {
+    if (s.stop && *s.stop) return;
     const int64_t n = (int64_t)s.A * s.O * s.B;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -1884,9 +1887,8 @@ extern "C" int64_t dd3_grid_ws(const dd3_geom* g) {
     return 2 * w.wmax + w.t1 + w.t2 + 2 * tab + 16;
 }
 
-extern "C" int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
-                            int tables_ready, void* stream) {
-    cudaStream_t st = (cudaStream_t)stream;
+static int grid_lse3(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
+                     int tables_ready, const int* stop, cudaStream_t st) {
     const int* in = to_x ? g->ny : g->nx;
     const int* on = to_x ? g->nx : g->ny;
     const double* in_org = to_x ? g->y_org : g->x_org;
@@ -1911,17 +1913,56 @@ extern "C" int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int
     // on2); axis 0: (1, in0, on1*on2) -> (1, on0, on1*on2)  (sinkhorn.py:159-175 order)
     const v3::GStage stages[3] = {
         {v, T1, w, rmax, tab[2], in[0] * in[1], in[2], 1, on[2], on_org[2], on_dx, in_org[2],
-         in_dx, g->eps},
+         in_dx, g->eps, stop},
         {T1, T2, w, rmax, tab[1], in[0], in[1], on[2], on[1], on_org[1], on_dx, in_org[1], in_dx,
-         g->eps},
+         g->eps, stop},
         {T2, out, w, rmax, tab[0], 1, in[0], on[1] * on[2], on[0], on_org[0], on_dx, in_org[0],
-         in_dx, g->eps}};
+         in_dx, g->eps, stop}};
     for (int k = 0; k < 3; ++k) {
         const v3::GStage& S = stages[k];
         v3::g_rows_kernel<<<v3_blocks((int64_t)S.A * S.B * (S.B == 1 ? 32 : 1)), v3::NT, 0, st>>>(S);
         v3::g_contract_kernel<<<v3_blocks((int64_t)S.A * S.O * S.B), v3::NT, 0, st>>>(S);
     }
     return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd3_grid_lse(const dd3_geom* g, const double* v, double* out, int to_x, double* work,
+                            int tables_ready, void* stream) {
+    return grid_lse3(g, v, out, to_x, work, tables_ready, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int64_t dd3_sinkhorn_ws(const dd3_geom* g) {
+    return dd3_grid_ws(g) + dd_sk_partial_doubles() + 16;
+}
+
+// Global unbalanced Sinkhorn iterations k0 .. k0+n_iters-1 enqueued without host
+// synchronisation (dd_sinkhorn_run over three axes): the stopping test runs on the device
+// (ctl_i[0]), every later launch of the chunk is a no-op once it is set.
+extern "C" int dd3_sinkhorn_run(const dd3_geom* g, double* alpha, double* beta, const double* mu,
+                                const double* log_mu, const double* log_nu, double* L, double* z,
+                                double* bv, double* av, double* px, double* work, int* ctl_i,
+                                double* ctl_d, double thr, int k0, int n_iters, int tables_ready,
+                                void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nx = (int64_t)g->nx[0] * g->nx[1] * g->nx[2];
+    const int64_t ny = (int64_t)g->ny[0] * g->ny[1] * g->ny[2];
+    double* partial = work + dd3_grid_ws(g);
+    const double eps = g->eps, lam = g->lam;
+    const double ratio = eps * lam / (eps + lam);
+    const int* stop = ctl_i;
+    int rc;
+    for (int k = k0; k < k0 + n_iters; ++k) {
+        const int ready = (tables_ready || k > k0) ? 1 : 0;
+        if ((rc = dd_sk_axpb(ny, beta, eps, log_nu, bv, 1, stop, st))) return rc;
+        if ((rc = grid_lse3(g, bv, L, 1, work, ready, stop, st))) return rc;
+        if (k >= 2 && (rc = dd_sk_gap(nx, alpha, L, mu, eps, lam, px, partial, thr, ctl_i, ctl_d, st)))
+            return rc;
+        if ((rc = dd_sk_axpb(nx, L, -ratio, nullptr, alpha, 0, stop, st))) return rc;
+        if ((rc = dd_sk_axpb(nx, alpha, eps, log_mu, av, 1, stop, st))) return rc;
+        if ((rc = grid_lse3(g, av, z, 0, work, ready, stop, st))) return rc;
+        if ((rc = dd_sk_newton(ny, z, ratio, lam, beta, ctl_i, k, st))) return rc;
+    }
+    return 0;
 }
 
 extern "C" int dd3_prolong(const int32_t* nf, const int32_t* nc, const double* coarse, double* fine,

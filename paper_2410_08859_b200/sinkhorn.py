@@ -70,6 +70,12 @@ class DeviceProblem:
     def make_sweeper(self) -> "GridSweeper":
         return GridSweeper(self)
 
+    def sinkhorn_ws(self) -> int:
+        return int(_lib.lib().dd_sinkhorn_ws(self.geom))
+
+    def sinkhorn_run(self, *args) -> int:
+        return _lib.lib().dd_sinkhorn_run(self.geom, *args)
+
     def empty_x(self):
         import torch
         return torch.empty(self.nx, dtype=torch.float64, device=self.device)
@@ -235,19 +241,18 @@ def sinkhorn_solve(dp: DeviceProblem, alpha0=None, beta0=None, config: SolverCon
     if not collect_trace and config.max_iters > 0 and dp.device_loop:
         # device-side loop: chunks of iterations enqueued by dd_sinkhorn_run with the
         # stopping test on the device; one host synchronisation per chunk
-        lib = _lib.lib()
-        ws = torch.empty(int(lib.dd_sinkhorn_ws(g)), dtype=torch.float64, device=dp.device)
+        ws = torch.empty(dp.sinkhorn_ws(), dtype=torch.float64, device=dp.device)
         ctl_i = torch.zeros(2, dtype=torch.int32, device=dp.device)
         ctl_d = torch.zeros(1, dtype=torch.float64, device=dp.device)
         k, chunk, tables = 1, 16, 0
         while k <= config.max_iters:
             n = min(chunk, config.max_iters - k + 1)
-            _lib.check(lib.dd_sinkhorn_run(g, alpha.data_ptr(), beta.data_ptr(), dp.mu.data_ptr(),
-                                           dp.log_mu.data_ptr(), dp.log_nu.data_ptr(),
-                                           L.data_ptr(), z.data_ptr(), bv.data_ptr(),
-                                           av.data_ptr(), px.data_ptr(), ws.data_ptr(),
-                                           ctl_i.data_ptr(), ctl_d.data_ptr(), float(thr), k, n,
-                                           tables, _lib.stream_handle()))
+            _lib.check(dp.sinkhorn_run(alpha.data_ptr(), beta.data_ptr(), dp.mu.data_ptr(),
+                                       dp.log_mu.data_ptr(), dp.log_nu.data_ptr(),
+                                       L.data_ptr(), z.data_ptr(), bv.data_ptr(),
+                                       av.data_ptr(), px.data_ptr(), ws.data_ptr(),
+                                       ctl_i.data_ptr(), ctl_d.data_ptr(), float(thr), k, n,
+                                       tables, _lib.stream_handle()))
             tables = 1
             c = ctl_i.cpu().numpy()
             if c[0]:

@@ -72,7 +72,7 @@ class VolumeProblem:
     Duck-types :class:`sinkhorn.DeviceProblem` for the global solver and the
     certificate (``make_sweeper`` gives the three-axis sweep)."""
 
-    device_loop = False   # sinkhorn_solve runs its host loop over dd3_grid_lse
+    device_loop = True    # sinkhorn_solve runs its loop on the device (dd3_sinkhorn_run)
 
     def __init__(self, problem: TransportProblem, device=None):
         import torch
@@ -115,6 +115,12 @@ class VolumeProblem:
 
     def make_sweeper(self) -> "GridSweeper3":
         return GridSweeper3(self)
+
+    def sinkhorn_ws(self) -> int:
+        return int(_lib.lib().dd3_sinkhorn_ws(self.geom))
+
+    def sinkhorn_run(self, *args) -> int:
+        return _lib.lib().dd3_sinkhorn_run(self.geom, *args)
 
     def empty_x(self):
         import torch
