@@ -433,6 +433,7 @@ int dd3_cell_terms(const dd3_geom* g, const dd3_state* s, double* out, void* str
 /* Product start nu_i = (m_i/|mu|) nu on the full box (cap >= grid size). */
 int dd3_product_init(const dd3_geom* g, const dd3_state* s, double mu_total, void* stream);
 /* Plan cut of global duals along the basic cells (two calls: yval NULL sizes the boxes).
+ * tile_max is the workspace: dd3_cut_tiles(g) doubles.
  * Terms whose log value is below cut_log (e.g. -60) are skipped; tiles of Y nodes are
  * culled by a bound on that value.  tile_max holds dd3_cut_tiles(g) doubles. */
 int64_t dd3_cut_tiles(const dd3_geom* g);

@@ -1649,16 +1649,36 @@ __device__ __forceinline__ bool cut_fast(const CutTabs& T, const double* xs_ex, 
     return true;
 }
 
-__global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
+// bv = beta / eps + log nu (the global X sweep's input for the separable cut's X-marginals)
+__global__ void cut_bv_kernel(int64_t n, const double* beta, const double* log_nu, double eps,
+                              double* bv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bv[i] = beta[i] / eps + log_nu[i];
+}
+
+// Separable plan cut.  Per basic cell: the 4^3 Y tiles whose bound clears cut_log give a
+// candidate Y box; over it the column sums S(y) = sum_x t(x, y) and the cost-weighted sums
+// Sc(y) = sum_x t c are three-stage contractions of the block weights exp(a - A) against
+// the Y-normalised tables (axis 2, then 1, then 0; Sc through the d_a^2-weighted tables),
+// so a node costs a few FMAs.  col(y) = F(y) S(y), transport = sum F Sc; the X-marginal of
+// the cut is mu exp(alpha/eps + L) with L the global X sweep of beta/eps + log nu (every
+// term of the block's rows), and the entropy piece follows from
+//   sum blk (alpha + beta - c)/eps = sum_x xm alpha/eps + sum_y col beta/eps - transport/eps.
+// A node whose normalised sum is below kTiny or whose scale would overflow takes the exact
+// per-term path; a cell whose candidate box does not fit shared memory takes the per-node
+// factorised path (cut_fast) for every node.
+__global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
                                                         const double* alpha, const double* beta,
-                                                        double trunc, double cut_log,
-                                                        const double* tmax, double* trunc_out,
-                                                        int32_t* boxes_out) {
+                                                        const double* Lx, double trunc,
+                                                        double cut_log, const double* tmax,
+                                                        double* trunc_out, int32_t* boxes_out,
+                                                        int smem_doubles) {
     extern __shared__ double dsm[];
     __shared__ double red[NW];
     __shared__ int redi[NW];
     __shared__ double xs_a[64], xs_lm[64], xs_mu[64], xs_c0[64], xs_c1[64], xs_c2[64];
-    __shared__ double xs_ex[64], xs_ae[64];
+    __shared__ double xs_ex[64], xs_ae[64], exb[64];
     __shared__ int xs_t[64], xs_i0[64], xs_i1[64], xs_i2[64];
     __shared__ int n_sh;
     __shared__ double s_amax;
@@ -1669,7 +1689,8 @@ __global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
     if (threadIdx.x == 0) {
         int n = 0;
         double am = kNegInf;
-        for (int t = 0; t < bs && n < 64; ++t) {
+        for (int t = 0; t < bs && t < 64; ++t) {
+            exb[t] = 0.0;
             int t0, t1, t2;
             unflat(t, bx.e[1], bx.e[2], t0, t1, t2);
             const int xi0 = bx.o[0] + t0, xi1 = bx.o[1] + t1, xi2 = bx.o[2] + t2;
@@ -1691,15 +1712,19 @@ __global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
         }
         n_sh = n;
         s_amax = am;
-        for (int k = 0; k < n; ++k) xs_ex[k] = exp(xs_ae[k] + xs_lm[k] - am);
+        for (int k = 0; k < n; ++k) {
+            xs_ex[k] = exp(xs_ae[k] + xs_lm[k] - am);
+            exb[xs_t[k]] = xs_ex[k];
+        }
     }
-    // per-axis tables over the whole Y axis: Kn_a, d_a^2, column shifts
     CutTabs T;
+    double* free_sm;
     {
         double* p = dsm;
         for (int a = 0; a < 3; ++a) { T.n[a] = g.ny[a]; T.K[a] = p; p += bx.e[a] * g.ny[a]; }
         for (int a = 0; a < 3; ++a) { T.D[a] = p; p += bx.e[a] * g.ny[a]; }
         for (int a = 0; a < 3; ++a) { T.c[a] = p; p += g.ny[a]; }
+        free_sm = p;
         for (int a = 0; a < 3; ++a) {
             double* K = const_cast<double*>(T.K[a]);
             double* D = const_cast<double*>(T.D[a]);
@@ -1731,10 +1756,8 @@ __global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
     const int tn0 = (g.ny[0] + kCutTile - 1) / kCutTile, tn1 = (g.ny[1] + kCutTile - 1) / kCutTile,
               tn2 = (g.ny[2] + kCutTile - 1) / kCutTile;
     const int64_t ntile = (int64_t)tn0 * tn1 * tn2;
-    double xacc[64];
-    for (int k = 0; k < 64; ++k) xacc[k] = 0.0;
-    double mass = 0.0, tr = 0.0, klp = 0.0, rem = 0.0;
-    int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = -1, hi1 = -1, hi2 = -1;
+    // ---- candidate box: the surviving tiles' bounding box
+    int cl0 = INT_MAX, cl1 = INT_MAX, cl2 = INT_MAX, ch0 = -1, ch1 = -1, ch2 = -1;
     for (int64_t t = threadIdx.x; t < ntile; t += NT) {
         int ta0, ta1, ta2;
         unflat(t, tn1, tn2, ta0, ta1, ta2);
@@ -1746,54 +1769,177 @@ __global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
         const double g2 = gap1(xlo[2], xhi[2], coord(g.y_org, g.y_dx, 2, yl2), coord(g.y_org, g.y_dx, 2, yh2));
         const double d2 = g0 * g0 + g1 * g1 + g2 * g2;
         if (amax + tmax[t] - d2 / eps < cut_log - 1.0) continue;
-        for (int y0 = yl0; y0 <= yh0; ++y0)
-            for (int y1 = yl1; y1 <= yh1; ++y1)
-                for (int y2 = yl2; y2 <= yh2; ++y2) {
-                    const int64_t id = ((int64_t)y0 * g.ny[1] + y1) * g.ny[2] + y2;
-                    const double nu = s.nu[id];
-                    const double lnu = s.log_nu[id];
-                    const double bt = beta[id];
-                    double col, trc = 0.0, klc = 0.0;
-                    if (cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0, y1, y2,
-                                 bt, lnu, true, col, trc, klc, xacc)) {
-                        tr += trc;
-                        klp += klc;
-                    } else {
-                        col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
-                                      coord(g.y_org, g.y_dx, 0, y0), coord(g.y_org, g.y_dx, 1, y1),
-                                      coord(g.y_org, g.y_dx, 2, y2), nu, lnu, bt, cut_log, &tr,
-                                      &klp, xacc);
-                    }
-                    mass += col;
-                    if (col >= trunc) {
-                        lo0 = min(lo0, y0); hi0 = max(hi0, y0);
-                        lo1 = min(lo1, y1); hi1 = max(hi1, y1);
-                        lo2 = min(lo2, y2); hi2 = max(hi2, y2);
-                    } else {
-                        rem += col;
-                    }
-                }
+        cl0 = min(cl0, yl0); ch0 = max(ch0, yh0);
+        cl1 = min(cl1, yl1); ch1 = max(ch1, yh1);
+        cl2 = min(cl2, yl2); ch2 = max(ch2, yh2);
     }
+    cl0 = bmin_i(cl0, redi); cl1 = bmin_i(cl1, redi); cl2 = bmin_i(cl2, redi);
+    ch0 = bmax_i(ch0, redi); ch1 = bmax_i(ch1, redi); ch2 = bmax_i(ch2, redi);
+    const int m0 = ch0 >= 0 ? ch0 - cl0 + 1 : 0, m1 = ch0 >= 0 ? ch1 - cl1 + 1 : 0,
+              m2 = ch0 >= 0 ? ch2 - cl2 + 1 : 0;
+    const int s0 = bx.e[0], s1 = bx.e[1], s2 = bx.e[2];
+    const int64_t used = free_sm - dsm;
+    const int64_t need = 2 * (int64_t)s0 * s1 * m2 + 3 * (int64_t)s0 * m1 * m2;
+    const bool sep = need <= smem_doubles - used;
+    double mass = 0.0, tr = 0.0, klp = 0.0, rem = 0.0;
+    double xacc[64];   // per-term path scratch (the X-marginals come from the global sweep)
+    for (int k = 0; k < 64; ++k) xacc[k] = 0.0;
+    int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = -1, hi1 = -1, hi2 = -1;
+    double* U1 = free_sm;
+    double* U1c = U1 + (int64_t)s0 * s1 * m2;
+    double* U2 = U1c + (int64_t)s0 * s1 * m2;
+    double* U2c2 = U2 + (int64_t)s0 * m1 * m2;
+    double* U2c1 = U2c2 + (int64_t)s0 * m1 * m2;
+    const double* K0 = T.K[0];
+    const double* K1 = T.K[1];
+    const double* K2 = T.K[2];
+    const double* D0 = T.D[0];
+    const double* D1 = T.D[1];
+    const double* D2 = T.D[2];
+    const int n0 = g.ny[0], n1 = g.ny[1], n2 = g.ny[2];
+    if (sep && m0 > 0) {
+        // stage 1 (axis 2): U1[x0][x1][y2] = sum_x2 exb K2, U1c with K2 d2^2
+        const int nu1 = s0 * s1 * m2;
+        for (int t = threadIdx.x; t < nu1; t += NT) {
+            const int q = t / m2, y2 = t - q * m2;
+            const double* e = exb + q * s2;
+            double u = 0.0, uc = 0.0;
+            for (int x2 = 0; x2 < s2; ++x2) {
+                const double kv = e[x2] * K2[x2 * n2 + cl2 + y2];
+                u += kv;
+                uc = fma(kv, D2[x2 * n2 + cl2 + y2], uc);
+            }
+            U1[t] = u;
+            U1c[t] = uc;
+        }
+        __syncthreads();
+        // stage 2 (axis 1): U2[x0][y1][y2] = sum_x1 U1 K1; U2c2 from U1c; U2c1 with K1 d1^2
+        const int nu2 = s0 * m1 * m2;
+        for (int t = threadIdx.x; t < nu2; t += NT) {
+            const int x0 = t / (m1 * m2), r = t - x0 * m1 * m2;
+            const int y1 = r / m2, y2 = r - y1 * m2;
+            double u = 0.0, uc2 = 0.0, uc1 = 0.0;
+            for (int x1 = 0; x1 < s1; ++x1) {
+                const double kv = K1[x1 * n1 + cl1 + y1];
+                const double a1 = U1[(x0 * s1 + x1) * m2 + y2];
+                u = fma(a1, kv, u);
+                uc2 = fma(U1c[(x0 * s1 + x1) * m2 + y2], kv, uc2);
+                uc1 = fma(a1 * kv, D1[x1 * n1 + cl1 + y1], uc1);
+            }
+            U2[t] = u;
+            U2c2[t] = uc2;
+            U2c1[t] = uc1;
+        }
+        __syncthreads();
+        // stage 3 (axis 0) per candidate node
+        const int nc = m0 * m1 * m2;
+        Step3<NT> p(threadIdx.x, m1, m2);
+        for (int t = threadIdx.x; t < nc; t += NT, p.next()) {
+            const int y0 = cl0 + p.i0, y1 = cl1 + p.i1, y2 = cl2 + p.i2;
+            const int64_t id = ((int64_t)y0 * n1 + y1) * n2 + y2;
+            const double bt = beta[id];
+            const double lnu = s.log_nu[id];
+            const double logF = bt / eps + lnu + amax + (T.c[0][y0] + T.c[1][y1] + T.c[2][y2]);
+            const int r = p.i1 * m2 + p.i2;
+            double S = 0.0, Sc = 0.0;
+            for (int x0 = 0; x0 < s0; ++x0) {
+                const double kv = K0[x0 * n0 + y0];
+                const int q = x0 * m1 * m2 + r;
+                S = fma(U2[q], kv, S);
+                Sc = fma(U2c2[q] + U2c1[q] + U2[q] * D0[x0 * n0 + y0], kv, Sc);
+            }
+            double col, trc;
+            if (logF <= 700.0 && S >= kTiny) {
+                const double F = exp(logF);
+                col = F * S;
+                trc = F * Sc;
+            } else {
+                trc = 0.0;
+                double scratch = 0.0;   // per-term entropy pieces: the formula below covers them
+                col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
+                              coord(g.y_org, g.y_dx, 0, y0), coord(g.y_org, g.y_dx, 1, y1),
+                              coord(g.y_org, g.y_dx, 2, y2), s.nu[id], lnu, bt, cut_log, &trc,
+                              &scratch, xacc);
+            }
+            tr += trc;
+            klp += col * (bt / eps);
+            mass += col;
+            if (col >= trunc) {
+                lo0 = min(lo0, y0); hi0 = max(hi0, y0);
+                lo1 = min(lo1, y1); hi1 = max(hi1, y1);
+                lo2 = min(lo2, y2); hi2 = max(hi2, y2);
+            } else {
+                rem += col;
+            }
+        }
+    } else if (m0 > 0) {
+        // the candidate box exceeds shared memory: per-node factorised path over the tiles
+        for (int64_t t = threadIdx.x; t < ntile; t += NT) {
+            int ta0, ta1, ta2;
+            unflat(t, tn1, tn2, ta0, ta1, ta2);
+            const int yl0 = ta0 * kCutTile, yl1 = ta1 * kCutTile, yl2 = ta2 * kCutTile;
+            const int yh0 = min(n0, yl0 + kCutTile) - 1, yh1 = min(n1, yl1 + kCutTile) - 1,
+                      yh2 = min(n2, yl2 + kCutTile) - 1;
+            const double g0 = gap1(xlo[0], xhi[0], coord(g.y_org, g.y_dx, 0, yl0), coord(g.y_org, g.y_dx, 0, yh0));
+            const double g1 = gap1(xlo[1], xhi[1], coord(g.y_org, g.y_dx, 1, yl1), coord(g.y_org, g.y_dx, 1, yh1));
+            const double g2 = gap1(xlo[2], xhi[2], coord(g.y_org, g.y_dx, 2, yl2), coord(g.y_org, g.y_dx, 2, yh2));
+            if (amax + tmax[t] - (g0 * g0 + g1 * g1 + g2 * g2) / eps < cut_log - 1.0) continue;
+            for (int y0 = yl0; y0 <= yh0; ++y0)
+                for (int y1 = yl1; y1 <= yh1; ++y1)
+                    for (int y2 = yl2; y2 <= yh2; ++y2) {
+                        const int64_t id = ((int64_t)y0 * n1 + y1) * n2 + y2;
+                        const double bt = beta[id];
+                        const double lnu = s.log_nu[id];
+                        double col, trc = 0.0, klc = 0.0, scratch = 0.0;
+                        if (!cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0,
+                                      y1, y2, bt, lnu, true, col, trc, klc, xacc))
+                            col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
+                                          coord(g.y_org, g.y_dx, 0, y0),
+                                          coord(g.y_org, g.y_dx, 1, y1),
+                                          coord(g.y_org, g.y_dx, 2, y2), s.nu[id], lnu, bt,
+                                          cut_log, &trc, &scratch, xacc);
+                        tr += trc;
+                        klp += col * (bt / eps);
+                        mass += col;
+                        if (col >= trunc) {
+                            lo0 = min(lo0, y0); hi0 = max(hi0, y0);
+                            lo1 = min(lo1, y1); hi1 = max(hi1, y1);
+                            lo2 = min(lo2, y2); hi2 = max(hi2, y2);
+                        } else {
+                            rem += col;
+                        }
+                    }
+        }
+    }
+    // klp holds sum_y col beta/eps; the entropy piece adds the X side and the transport
     mass = bsum(mass, red);
     tr = bsum(tr, red);
     klp = bsum(klp, red);
     rem = bsum(rem, red);
     lo0 = bmin_i(lo0, redi); lo1 = bmin_i(lo1, redi); lo2 = bmin_i(lo2, redi);
     hi0 = bmax_i(hi0, redi); hi1 = bmax_i(hi1, redi); hi2 = bmax_i(hi2, redi);
-    for (int k = threadIdx.x; k < bs; k += NT) s.x_marg[(int64_t)i * bs + k] = 0.0;
-    __syncthreads();
-    for (int k = 0; k < nxn; ++k) {
-        const double v = bsum(xacc[k], red);
-        if (threadIdx.x == 0) s.x_marg[(int64_t)i * bs + xs_t[k]] = v;
+    // X-marginals from the global X sweep: xm = mu exp(alpha/eps + L)
+    double xa = 0.0;
+    for (int k = threadIdx.x; k < bs; k += NT) {
+        int t0, t1, t2;
+        unflat(k, bx.e[1], bx.e[2], t0, t1, t2);
+        const int64_t id = ((int64_t)(bx.o[0] + t0) * g.nx[1] + bx.o[1] + t1) * g.nx[2] + bx.o[2] + t2;
+        const double mu = s.mu[id];
+        double xm = 0.0;
+        if (mu > 0) {
+            xm = mu * exp(alpha[id] / eps + Lx[id]);
+            xa += xm * (alpha[id] / eps);
+        }
+        s.x_marg[(int64_t)i * bs + k] = xm;
     }
-    __syncthreads();
+    xa = bsum(xa, red);
     int ne0 = 0, ne1 = 0, ne2 = 0;
     if (hi0 >= 0) { ne0 = hi0 - lo0 + 1; ne1 = hi1 - lo1 + 1; ne2 = hi2 - lo2 + 1; }
     if (threadIdx.x == 0) {
         double mmu = 0.0;
         for (int k = 0; k < nxn; ++k) mmu += xs_mu[k];
         s.transport[i] = tr;
-        s.kl[i] = klp - mass + mmu * g.nu_total;
+        s.kl[i] = (xa + klp - tr / eps) - mass + mmu * g.nu_total;
         trunc_out[i] = rem;
         int32_t* ob = boxes_out + (int64_t)i * 6;
         ob[0] = hi0 >= 0 ? lo0 : 0; ob[1] = ne0;
@@ -1808,10 +1954,22 @@ __global__ void __launch_bounds__(NT) cut_plan3f_kernel(dd3_geom g, dd3_state s,
         int a0, a1, a2;
         unflat(t, ne1, ne2, a0, a1, a2);
         const int y0 = lo0 + a0, y1 = lo1 + a1, y2 = lo2 + a2;
-        const int64_t id = ((int64_t)y0 * g.ny[1] + y1) * g.ny[2] + y2;
-        double col, trc, klc;
-        if (!cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0, y1, y2, beta[id],
-                      s.log_nu[id], false, col, trc, klc, dummy))
+        const int64_t id = ((int64_t)y0 * n1 + y1) * n2 + y2;
+        double col = -1.0;
+        if (sep) {
+            const double logF = beta[id] / eps + s.log_nu[id] + amax +
+                                (T.c[0][y0] + T.c[1][y1] + T.c[2][y2]);
+            const int r = (y1 - cl1) * m2 + (y2 - cl2);
+            double S = 0.0;
+            for (int x0 = 0; x0 < s0; ++x0) S = fma(U2[x0 * m1 * m2 + r], K0[x0 * n0 + y0], S);
+            if (logF <= 700.0 && S >= kTiny) col = exp(logF) * S;
+        } else {
+            double trc, klc;
+            if (!cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0, y1, y2,
+                          beta[id], s.log_nu[id], false, col, trc, klc, dummy))
+                col = -1.0;
+        }
+        if (col < 0.0)
             col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
                           coord(g.y_org, g.y_dx, 0, y0), coord(g.y_org, g.y_dx, 1, y1),
                           coord(g.y_org, g.y_dx, 2, y2), s.nu[id], s.log_nu[id], beta[id],
@@ -2034,29 +2192,50 @@ extern "C" int dd3_product_init(const dd3_geom* g, const dd3_state* s, double mu
     return dd_set_error(cudaGetLastError());
 }
 
-extern "C" int64_t dd3_cut_tiles(const dd3_geom* g) {
+static int64_t cut_tile_count(const dd3_geom* g) {
     const int k = v3::kCutTile;
     return (int64_t)((g->ny[0] + k - 1) / k) * ((g->ny[1] + k - 1) / k) * ((g->ny[2] + k - 1) / k);
+}
+
+extern "C" int64_t dd3_cut_tiles(const dd3_geom* g) {
+    // workspace of dd3_cut_plan: tile maxima, beta/eps + log nu (Y grid), the global X
+    // sweep (X grid) and its grid-LSE workspace
+    const int64_t nx = (int64_t)g->nx[0] * g->nx[1] * g->nx[2];
+    const int64_t ny = (int64_t)g->ny[0] * g->ny[1] * g->ny[2];
+    return cut_tile_count(g) + ny + nx + dd3_grid_ws(g) + 16;
 }
 
 extern "C" int dd3_cut_plan(const dd3_geom* g, const dd3_state* s, const double* alpha,
                             const double* beta, double trunc, double cut_log, double* tile_max,
                             double* trunc_out, int32_t* boxes_out, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    v3::cut_tiles_kernel<<<v3_blocks(dd3_cut_tiles(g)), v3::NT, 0, st>>>(*g, beta, s->log_nu,
-                                                                          tile_max);
-    // factorised kernel when its per-axis tables fit shared memory (block_a x ny_a each)
+    const int64_t nx = (int64_t)g->nx[0] * g->nx[1] * g->nx[2];
+    const int64_t ny = (int64_t)g->ny[0] * g->ny[1] * g->ny[2];
+    double* tmax = tile_max;
+    double* bv = tmax + cut_tile_count(g);
+    double* Lx = bv + ny;
+    double* lws = Lx + nx;
+    v3::cut_tiles_kernel<<<v3_blocks(cut_tile_count(g)), v3::NT, 0, st>>>(*g, beta, s->log_nu,
+                                                                           tmax);
+    // separable kernel when its per-axis tables fit shared memory (block_a x ny_a each)
     int64_t tab = 0;
     for (int a = 0; a < 3; ++a) tab += 2 * (int64_t)s->block[a] * g->ny[a] + g->ny[a];
-    const int64_t smem = tab * (int64_t)sizeof(double);
-    if (smem <= 160 * 1024 && s->block[0] * s->block[1] * s->block[2] <= 64) {
-        cudaFuncSetAttribute(v3::cut_plan3f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        v3::cut_plan3f_kernel<<<s->n_basic, v3::NT, (size_t)smem, st>>>(
-            *g, *s, alpha, beta, trunc, cut_log, tile_max, trunc_out, boxes_out);
+    const int64_t static_b = 8 * 1024;   // the kernel's static shared arrays (< 8 KB)
+    const int64_t avail = 227 * 1024 - static_b;
+    if (tab * (int64_t)sizeof(double) <= avail / 2 && s->block[0] * s->block[1] * s->block[2] <= 64) {
+        v3::cut_bv_kernel<<<v3_blocks(ny), v3::NT, 0, st>>>(ny, beta, s->log_nu, g->eps, bv);
+        int rc = grid_lse3(g, bv, Lx, 1, lws, 0, nullptr, st);
+        if (rc) return rc;
+        cudaError_t e = cudaFuncSetAttribute(v3::cut_plan3s_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)avail);
+        if (e != cudaSuccess) return dd_set_error(e);
+        v3::cut_plan3s_kernel<<<s->n_basic, v3::NT, (size_t)avail, st>>>(
+            *g, *s, alpha, beta, Lx, trunc, cut_log, tmax, trunc_out, boxes_out,
+            (int)(avail / sizeof(double)));
     } else {
         v3::cut_plan3_kernel<<<s->n_basic, v3::NT, 0, st>>>(*g, *s, alpha, beta, trunc, cut_log,
-                                                             tile_max, trunc_out, boxes_out);
+                                                             tmax, trunc_out, boxes_out);
     }
     return dd_set_error(cudaGetLastError());
 }
