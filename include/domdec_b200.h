@@ -379,12 +379,16 @@ typedef struct dd3_batch {
     double* cstat;             /* [n_cells*8] gap, first_gap, iters, conv, nu_minus_clamped,
                                   newton_clamped, balance_fallbacks, target_miss */
     double* cstat2;            /* [n_cells*8] drift nodes, truncated total, executed
-                                  iterations, sweep fallbacks, 4 unused */
+                                  iterations, sweep fallbacks, Newton evaluations, Sinkhorn
+                                  loop cycles (clock64), 2 unused */
     double delta;
     int32_t max_iters;
     int32_t newton_max_iters;
     double newton_tol;
     double trunc;
+    int32_t smem_doubles;      /* shared-memory doubles per cell CTA for the hot per-cell
+                                  arrays (the host sizes it for the batch's largest window;
+                                  a cell that does not fit keeps them in the workspace) */
 } dd3_batch;
 
 /* Workspace doubles of dd3_grid_lse for the geometry. */

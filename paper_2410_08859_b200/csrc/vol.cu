@@ -562,6 +562,22 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     C.lnu = W + l.lnu; C.m = W + l.m; C.lm = W + l.lm; C.beta = W + l.beta; C.z = W + l.z;
     for (int a = 0; a < 3; ++a) { C.kn[a] = W + l.kn[a]; C.c[a] = W + l.c[a]; }
     C.s1 = W + l.s1; C.s2 = W + l.s2;
+    {
+        // the arrays every Sinkhorn iteration re-reads (z, beta, the stage scratch, the axis
+        // tables) in shared memory when they fit this CTA's dynamic allocation
+        extern __shared__ double dyn[];
+        const int64_t s1n = l.s2 - l.s1, s2n = l.total - 1 - l.s2;
+        const int64_t tabn = l.s1 - l.kn[0];
+        const int64_t need = 2 * C.ny + s1n + s2n + tabn;
+        if (need <= b.smem_doubles) {
+            double* p = dyn;
+            C.z = p; p += C.ny;
+            C.beta = p; p += C.ny;
+            C.s1 = p; p += s1n;
+            C.s2 = p; p += s2n;
+            for (int a = 0; a < 3; ++a) { C.kn[a] = p + (l.kn[a] - l.kn[0]); C.c[a] = p + (l.c[a] - l.kn[0]); }
+        }
+    }
     const double eps = g.eps, lam = g.lam;
     const double ratio = eps * lam / (eps + lam);
     const int bs = s.block[0] * s.block[1] * s.block[2];
@@ -670,6 +686,8 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     double gap = kInf, first_g = __builtin_nan("");
     bool conv = false, have_first = false;
     int iters = 0, ndeg_max = 0, nfb = 0;
+    long long nsteps = 0;        // Newton evaluations of this thread (diagnostic)
+    const long long t_loop0 = clock64();
     for (int k = 1; k <= b.max_iters; ++k) {
         nfb += sweep_x<T>(C, g, sh);
         if (k >= 2) {
@@ -686,7 +704,7 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
         for (int64_t y = threadIdx.x; y < C.ny; y += T) {
             int deg = 0;
             C.beta[y] = dd::newton_node(C.z[y], C.m[y], true, C.beta[y], eps, lam, b.newton_tol,
-                                        b.newton_max_iters, &deg, nullptr, nullptr, C.lm[y]);
+                                        b.newton_max_iters, &deg, &nsteps, nullptr, C.lm[y]);
             nd += deg;
         }
         if (nd) atomicAdd(&sh.ndeg, nd);
@@ -701,6 +719,8 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
         if (!have_first) first_g = gg;
         conv = gg / lam <= thr;
     }
+    const long long t_loop = clock64() - t_loop0;
+    const double nsteps_all = bsum<T>((double)nsteps, sh.red);
     // ---- epilogue: split by members (cells.py:350-393)
     // mu_bar = exp(-alpha'/lam) mu, alpha' = -ratio L (the extra X half-step)
     for (int64_t x = threadIdx.x; x < C.nx; x += T)
@@ -1011,7 +1031,7 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
         cst[0] = gap; cst[1] = first_g; cst[2] = iters; cst[3] = conv ? 1.0 : 0.0;
         cst[4] = nclamped; cst[5] = ndeg_max; cst[6] = s_fb; cst[7] = miss;
         cst2[0] = drift_nodes; cst2[1] = trunc_total; cst2[2] = iters; cst2[3] = nfb;
-        cst2[4] = 0; cst2[5] = 0; cst2[6] = 0; cst2[7] = 0;
+        cst2[4] = nsteps_all; cst2[5] = (double)t_loop; cst2[6] = 0; cst2[7] = 0;
     }
 }
 
@@ -2139,9 +2159,22 @@ extern "C" int64_t dd3_cell_ws_size(const int32_t* w, const int32_t* n) {
 extern "C" int dd3_cell_solve(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
                               void* stream) {
     if (b->n_cells <= 0) return 0;
-    cudaFuncSetCacheConfig(v3::cell_solve3_kernel<v3::CELL_NT>, cudaFuncCachePreferL1);
+    // dynamic shared memory for the hot per-cell arrays (the kernel falls back to the
+    // global workspace for a cell whose arrays do not fit)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, v3::cell_solve3_kernel<v3::CELL_NT>);
+    if (e != cudaSuccess) return dd_set_error(e);
+    const int64_t cap = 227 * 1024 - (int64_t)fa.sharedSizeBytes - 1024;
+    int64_t bytes = (int64_t)b->smem_doubles * (int64_t)sizeof(double);
+    if (bytes > cap) bytes = cap;
+    if (bytes < 0) bytes = 0;
+    dd3_batch bb = *b;
+    bb.smem_doubles = (int32_t)(bytes / (int64_t)sizeof(double));
+    e = cudaFuncSetAttribute(v3::cell_solve3_kernel<v3::CELL_NT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return dd_set_error(e);
     v3::cell_solve3_kernel<v3::CELL_NT>
-        <<<b->n_cells, v3::CELL_NT, 0, (cudaStream_t)stream>>>(*g, *s, *b);
+        <<<b->n_cells, v3::CELL_NT, (size_t)bytes, (cudaStream_t)stream>>>(*g, *s, bb);
     return dd_set_error(cudaGetLastError());
 }
 

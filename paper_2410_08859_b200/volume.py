@@ -620,6 +620,16 @@ def _ws_total(w, n0, n1, n2) -> np.ndarray:
     return 5 * nx + 5 * ny + w0 * n0 + w1 * n1 + w2 * n2 + n0 + n1 + n2 + s1 + s2 + 1
 
 
+def _hot_doubles(w, n0, n1, n2) -> np.ndarray:
+    """Shared-memory doubles of a cell's hot arrays (z, beta, stage scratch, axis tables;
+    mirrors the kernel's placement in csrc/vol.cu)."""
+    w0, w1, w2 = (int(x) for x in w)
+    ny = n0 * n1 * n2
+    s1 = np.maximum(w0 * w1 * n2, n0 * n1 * w2)
+    s2 = np.maximum(w0 * n1 * n2, n0 * w1 * w2)
+    return 2 * ny + s1 + s2 + w0 * n0 + w1 * n1 + w2 * n2 + n0 + n1 + n2
+
+
 class _Batch3:
     """Device arenas and host tables of one solved batch of composite cells."""
 
@@ -687,7 +697,8 @@ class _Batch3:
             xarena=self.xarena.data_ptr(), mbox=self.mbox.data_ptr(), mstat=self.mstat.data_ptr(),
             cstat=self.cstat.data_ptr(), cstat2=self.cstat2.data_ptr(), delta=cfg.delta,
             max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
-            newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold)
+            newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold,
+            smem_doubles=int(_hot_doubles(pt.nxw, ne[0], ne[1], ne[2]).max(initial=0)))
         for a in range(3):
             self.batch.nxw[a] = pt.nxw[a]
         self.tot_y = tot_y

@@ -37,7 +37,9 @@ def solve(self):
     print(f"    batch cells={self.n} t={t:.3f}s ny mean={self.ny.mean():.0f} max={self.ny.max()} "
           f"iters mean={it.mean():.0f} p50={np.median(it):.0f} max={it.max():.0f} "
           f"capped={(it >= self.cfg.max_iters).sum()} nonconv={(c1[:, 3] == 0).sum()} "
-          f"fallback_sweeps={int(c2[:, 3].sum())}", flush=True)
+          f"fallback_sweeps={int(c2[:, 3].sum())} newton/node-iter="
+          f"{c2[:, 4].sum() / max((c2[:, 2] * self.ny).sum(), 1):.2f} "
+          f"cycles/iter(longest)={c2[np.argmax(it), 5] / max(it.max(), 1):.0f}", flush=True)
 
 
 V._Batch3.solve = solve
