@@ -1737,34 +1737,6 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
             exb[xs_t[k]] = xs_ex[k];
         }
     }
-    CutTabs T;
-    double* free_sm;
-    {
-        double* p = dsm;
-        for (int a = 0; a < 3; ++a) { T.n[a] = g.ny[a]; T.K[a] = p; p += bx.e[a] * g.ny[a]; }
-        for (int a = 0; a < 3; ++a) { T.D[a] = p; p += bx.e[a] * g.ny[a]; }
-        for (int a = 0; a < 3; ++a) { T.c[a] = p; p += g.ny[a]; }
-        free_sm = p;
-        for (int a = 0; a < 3; ++a) {
-            double* K = const_cast<double*>(T.K[a]);
-            double* D = const_cast<double*>(T.D[a]);
-            double* cc = const_cast<double*>(T.c[a]);
-            for (int ya = threadIdx.x; ya < g.ny[a]; ya += NT) {
-                const double yc = coord(g.y_org, g.y_dx, a, ya);
-                double cm = kNegInf;
-                for (int xa = 0; xa < bx.e[a]; ++xa) {
-                    const double d = coord(g.x_org, g.x_dx, a, bx.o[a] + xa) - yc;
-                    cm = fmax(cm, -(d * d) / eps);
-                }
-                cc[ya] = cm;
-                for (int xa = 0; xa < bx.e[a]; ++xa) {
-                    const double d = coord(g.x_org, g.x_dx, a, bx.o[a] + xa) - yc;
-                    K[xa * g.ny[a] + ya] = exp(-(d * d) / eps - cm);
-                    D[xa * g.ny[a] + ya] = d * d;
-                }
-            }
-        }
-    }
     __syncthreads();
     const int nxn = n_sh;
     const double amax = s_amax;
@@ -1798,9 +1770,48 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
     const int m0 = ch0 >= 0 ? ch0 - cl0 + 1 : 0, m1 = ch0 >= 0 ? ch1 - cl1 + 1 : 0,
               m2 = ch0 >= 0 ? ch2 - cl2 + 1 : 0;
     const int s0 = bx.e[0], s1 = bx.e[1], s2 = bx.e[2];
+    // per-axis tables over the candidate ranges only (base pointers shifted so they are
+    // indexed by absolute Y node): Kn_a, d_a^2, column shifts
+    const int mm[3] = {m0, m1, m2};
+    const int cl[3] = {cl0, cl1, cl2};
+    const int64_t tabn = 2 * ((int64_t)s0 * m0 + (int64_t)s1 * m1 + (int64_t)s2 * m2) + m0 + m1 + m2;
+    const bool tabs_fit = tabn <= smem_doubles;
+    CutTabs T;
+    double* free_sm = dsm;
+    if (tabs_fit && m0 > 0) {
+        double* p = dsm;
+        double* Kb[3];
+        double* Db[3];
+        double* cb[3];
+        for (int q = 0; q < 3; ++q) { Kb[q] = p; p += (int64_t)bx.e[q] * mm[q]; }
+        for (int q = 0; q < 3; ++q) { Db[q] = p; p += (int64_t)bx.e[q] * mm[q]; }
+        for (int q = 0; q < 3; ++q) { cb[q] = p; p += mm[q]; }
+        free_sm = p;
+        for (int q = 0; q < 3; ++q) {
+            T.n[q] = mm[q];
+            T.K[q] = Kb[q] - cl[q];
+            T.D[q] = Db[q] - cl[q];
+            T.c[q] = cb[q] - cl[q];
+            for (int r = threadIdx.x; r < mm[q]; r += NT) {
+                const double yc = coord(g.y_org, g.y_dx, q, cl[q] + r);
+                double cm = kNegInf;
+                for (int xq = 0; xq < bx.e[q]; ++xq) {
+                    const double d = coord(g.x_org, g.x_dx, q, bx.o[q] + xq) - yc;
+                    cm = fmax(cm, -(d * d) / eps);
+                }
+                cb[q][r] = cm;
+                for (int xq = 0; xq < bx.e[q]; ++xq) {
+                    const double d = coord(g.x_org, g.x_dx, q, bx.o[q] + xq) - yc;
+                    Kb[q][xq * mm[q] + r] = exp(-(d * d) / eps - cm);
+                    Db[q][xq * mm[q] + r] = d * d;
+                }
+            }
+        }
+    }
+    __syncthreads();
     const int64_t used = free_sm - dsm;
     const int64_t need = 2 * (int64_t)s0 * s1 * m2 + 3 * (int64_t)s0 * m1 * m2;
-    const bool sep = need <= smem_doubles - used;
+    const bool sep = tabs_fit && need <= smem_doubles - used;
     double mass = 0.0, tr = 0.0, klp = 0.0, rem = 0.0;
     double xacc[64];   // per-term path scratch (the X-marginals come from the global sweep)
     for (int k = 0; k < 64; ++k) xacc[k] = 0.0;
@@ -1825,9 +1836,9 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
             const double* e = exb + q * s2;
             double u = 0.0, uc = 0.0;
             for (int x2 = 0; x2 < s2; ++x2) {
-                const double kv = e[x2] * K2[x2 * n2 + cl2 + y2];
+                const double kv = e[x2] * K2[x2 * m2 + cl2 + y2];
                 u += kv;
-                uc = fma(kv, D2[x2 * n2 + cl2 + y2], uc);
+                uc = fma(kv, D2[x2 * m2 + cl2 + y2], uc);
             }
             U1[t] = u;
             U1c[t] = uc;
@@ -1840,11 +1851,11 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
             const int y1 = r / m2, y2 = r - y1 * m2;
             double u = 0.0, uc2 = 0.0, uc1 = 0.0;
             for (int x1 = 0; x1 < s1; ++x1) {
-                const double kv = K1[x1 * n1 + cl1 + y1];
+                const double kv = K1[x1 * m1 + cl1 + y1];
                 const double a1 = U1[(x0 * s1 + x1) * m2 + y2];
                 u = fma(a1, kv, u);
                 uc2 = fma(U1c[(x0 * s1 + x1) * m2 + y2], kv, uc2);
-                uc1 = fma(a1 * kv, D1[x1 * n1 + cl1 + y1], uc1);
+                uc1 = fma(a1 * kv, D1[x1 * m1 + cl1 + y1], uc1);
             }
             U2[t] = u;
             U2c2[t] = uc2;
@@ -1863,10 +1874,10 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
             const int r = p.i1 * m2 + p.i2;
             double S = 0.0, Sc = 0.0;
             for (int x0 = 0; x0 < s0; ++x0) {
-                const double kv = K0[x0 * n0 + y0];
+                const double kv = K0[x0 * m0 + y0];
                 const int q = x0 * m1 * m2 + r;
                 S = fma(U2[q], kv, S);
-                Sc = fma(U2c2[q] + U2c1[q] + U2[q] * D0[x0 * n0 + y0], kv, Sc);
+                Sc = fma(U2c2[q] + U2c1[q] + U2[q] * D0[x0 * m0 + y0], kv, Sc);
             }
             double col, trc;
             if (logF <= 700.0 && S >= kTiny) {
@@ -1894,6 +1905,7 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
         }
     } else if (m0 > 0) {
         // the candidate box exceeds shared memory: per-node factorised path over the tiles
+        // (per-term exact path when not even the tables fit)
         for (int64_t t = threadIdx.x; t < ntile; t += NT) {
             int ta0, ta1, ta2;
             unflat(t, tn1, tn2, ta0, ta1, ta2);
@@ -1911,7 +1923,8 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
                         const double bt = beta[id];
                         const double lnu = s.log_nu[id];
                         double col, trc = 0.0, klc = 0.0, scratch = 0.0;
-                        if (!cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0,
+                        if (!tabs_fit ||
+                            !cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0,
                                       y1, y2, bt, lnu, true, col, trc, klc, xacc))
                             col = cut_col(g, xs_c0, xs_c1, xs_c2, xs_a, xs_lm, xs_mu, nxn,
                                           coord(g.y_org, g.y_dx, 0, y0),
@@ -1981,9 +1994,9 @@ __global__ void __launch_bounds__(NT) cut_plan3s_kernel(dd3_geom g, dd3_state s,
                                 (T.c[0][y0] + T.c[1][y1] + T.c[2][y2]);
             const int r = (y1 - cl1) * m2 + (y2 - cl2);
             double S = 0.0;
-            for (int x0 = 0; x0 < s0; ++x0) S = fma(U2[x0 * m1 * m2 + r], K0[x0 * n0 + y0], S);
+            for (int x0 = 0; x0 < s0; ++x0) S = fma(U2[x0 * m1 * m2 + r], K0[x0 * m0 + y0], S);
             if (logF <= 700.0 && S >= kTiny) col = exp(logF) * S;
-        } else {
+        } else if (tabs_fit) {
             double trc, klc;
             if (!cut_fast(T, xs_ex, xs_ae, xs_i0, xs_i1, xs_i2, nxn, amax, eps, y0, y1, y2,
                           beta[id], s.log_nu[id], false, col, trc, klc, dummy))
@@ -2250,12 +2263,9 @@ extern "C" int dd3_cut_plan(const dd3_geom* g, const dd3_state* s, const double*
     double* lws = Lx + nx;
     v3::cut_tiles_kernel<<<v3_blocks(cut_tile_count(g)), v3::NT, 0, st>>>(*g, beta, s->log_nu,
                                                                            tmax);
-    // separable kernel when its per-axis tables fit shared memory (block_a x ny_a each)
-    int64_t tab = 0;
-    for (int a = 0; a < 3; ++a) tab += 2 * (int64_t)s->block[a] * g->ny[a] + g->ny[a];
     const int64_t static_b = 8 * 1024;   // the kernel's static shared arrays (< 8 KB)
     const int64_t avail = 227 * 1024 - static_b;
-    if (tab * (int64_t)sizeof(double) <= avail / 2 && s->block[0] * s->block[1] * s->block[2] <= 64) {
+    if (s->block[0] * s->block[1] * s->block[2] <= 64) {
         v3::cut_bv_kernel<<<v3_blocks(ny), v3::NT, 0, st>>>(ny, beta, s->log_nu, g->eps, bv);
         int rc = grid_lse3(g, bv, Lx, 1, lws, 0, nullptr, st);
         if (rc) return rc;

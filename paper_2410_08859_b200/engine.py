@@ -568,6 +568,56 @@ def _member_boxes(st: PlanState, pt: _PartTables, ids) -> np.ndarray:
     return _union_boxes(bx, full)
 
 
+def _cut_plan_embedded(st: "PlanState", dp: DeviceProblem, alpha, beta, trunc: float,
+                       trunc_out, cut_log: float | None = None) -> None:
+    """warm_start_plan's plan cut (engine.py:294-322) through the three-axis kernel
+    (``dd3_cut_plan``: candidate boxes from tile bounds, separable column sums, X-marginals
+    from one global X sweep) on the (1, n0, n1) embedding of this 2D state: slots,
+    X-marginals and fragments share their layout; the boxes come back as (0, 1) + box4.
+    Terms below e^``cut_log`` are culled from 512^2 nodes up (-60, default), every
+    non-zero term is kept on smaller grids."""
+    import torch
+
+    g = dp.geom
+    g3 = _lib.Geom3()
+    for a, (nx, ny, ox, oy) in enumerate(((1, 1, 0.0, 0.0), (g.nx0, g.ny0, g.x_org0, g.y_org0),
+                                          (g.nx1, g.ny1, g.x_org1, g.y_org1))):
+        g3.nx[a], g3.ny[a], g3.x_org[a], g3.y_org[a] = nx, ny, ox, oy
+    g3.first_axis = 3 - st.ndim
+    g3.x_dx, g3.y_dx, g3.eps, g3.lam, g3.nu_total = g.x_dx, g.y_dx, g.eps, g.lam, g.nu_total
+    if cut_log is None:
+        cut_log = -60.0 if dp.ny >= 512 * 512 else -800.0
+    nb = st.n_basic
+    dev = dp.device
+    bx6 = torch.zeros((nb, 6), dtype=torch.int32, device=dev)
+    bx6[:, 1] = 1
+    bx6[:, 2:] = st.basic_xbox.view(nb, 4)
+    yb6 = torch.zeros(nb * 6, dtype=torch.int32, device=dev)
+    work = torch.empty(int(_lib.lib().dd3_cut_tiles(g3)), dtype=torch.float64, device=dev)
+
+    def state3(with_values: bool):
+        s3 = _lib.State3(mu=dp.mu.data_ptr(), nu=dp.nu.data_ptr(), log_mu=dp.log_mu.data_ptr(),
+                         log_nu=dp.log_nu.data_ptr(), n_basic=nb, basic_xbox=bx6.data_ptr(),
+                         basic_mass=st.basic_mass.data_ptr(), ybox=yb6.data_ptr(),
+                         yval=st.yval.data_ptr() if with_values else None, cap=st.cap,
+                         x_marg=st.x_marg_d.data_ptr(), transport=st.transport_d.data_ptr(),
+                         kl=st.kl_d.data_ptr())
+        s3.block[0], s3.block[1], s3.block[2] = 1, st.block[0], st.block[1]
+        return s3
+
+    boxes = torch.zeros(nb * 6, dtype=torch.int32, device=dev)
+    lib = _lib.lib()
+    _lib.check(lib.dd3_cut_plan(g3, state3(False), alpha.data_ptr(), beta.data_ptr(), trunc,
+                                float(cut_log), work.data_ptr(), trunc_out.data_ptr(),
+                                boxes.data_ptr(), _lib.stream_handle()))
+    bh = boxes.view(-1, 6).cpu().numpy().astype(np.int64)
+    st.ensure_cap(int((bh[:, 1] * bh[:, 3] * bh[:, 5]).max(initial=1)))
+    _lib.check(lib.dd3_cut_plan(g3, state3(True), alpha.data_ptr(), beta.data_ptr(), trunc,
+                                float(cut_log), work.data_ptr(), trunc_out.data_ptr(),
+                                boxes.data_ptr(), _lib.stream_handle()))
+    st.ybox.view(nb, 4).copy_(yb6.view(nb, 6)[:, 2:])
+
+
 def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta: float = 1e-3,
                     max_iters: int = 20_000, trunc_threshold: float = 1e-15,
                     dp: DeviceProblem | None = None, alpha0=None, beta0=None) -> PlanState:
@@ -588,17 +638,7 @@ def warm_start_plan(problem: TransportProblem, partitions: Decomposition, delta:
     st = PlanState(problem, partitions.basic, dp, cap=1)
     L = _lib.lib()
     trunc_out = torch.zeros(st.n_basic, dtype=torch.float64, device=dp.device)
-    boxes = torch.zeros(st.n_basic * 4, dtype=torch.int32, device=dp.device)
-    s = st.state_struct()
-    s.yval = None
-    _lib.check(L.dd_cut_plan(dp.geom, s, res.alpha.data_ptr(), res.beta.data_ptr(),
-                             float(trunc_threshold), trunc_out.data_ptr(), boxes.data_ptr(),
-                             _lib.stream_handle()))
-    bh = boxes.view(-1, 4).cpu().numpy()
-    st.ensure_cap(int((bh[:, 1].astype(np.int64) * bh[:, 3]).max(initial=1)))
-    _lib.check(L.dd_cut_plan(dp.geom, st.state_struct(), res.alpha.data_ptr(),
-                             res.beta.data_ptr(), float(trunc_threshold), trunc_out.data_ptr(),
-                             boxes.data_ptr(), _lib.stream_handle()))
+    _cut_plan_embedded(st, dp, res.alpha, res.beta, float(trunc_threshold), trunc_out)
     st.sync_boxes()
     st.truncated_mass = float(trunc_out.sum().item())
     for part in partitions.composites:
