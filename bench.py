@@ -163,10 +163,9 @@ def run_solve(prob, cfg, eps_start, levels=None):
 
 def fetch_result(st):
     """Device->host read of the result a caller consumes: boxes, marginals, duals, score."""
-    boxes = st.ybox.cpu()
-    vals = st.yval.cpu()
+    boxes, vals, _ = st.download_marginals()    # compacted on the device
     duals = [t.cpu() for t in st.global_duals] if st.global_duals is not None else []
-    d2h = boxes.numel() * 4 + vals.numel() * 8 + sum(t.numel() * 8 for t in duals)
+    d2h = boxes.nbytes + vals.nbytes + sum(t.numel() * 8 for t in duals)
     return d2h
 
 

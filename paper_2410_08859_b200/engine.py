@@ -453,8 +453,7 @@ class PlanState:
     # ---- host views (reference-shaped)
     @property
     def nu_i(self) -> list:
-        boxes = self.ybox.view(-1, 4).cpu().numpy()
-        vals = self.yval.view(self.n_basic, self.cap).cpu().numpy()
+        boxes, flat, offs = self.download_marginals()
         out = []
         for i in range(self.n_basic):
             b = boxes[i]
@@ -462,9 +461,24 @@ class PlanState:
             if b[1] == 0 or b[3] == 0:
                 out.append(SparseCellMarginal.empty(self.ndim))
                 continue
-            v = vals[i, :b[1] * b[3]].reshape(b[1], b[3])
+            v = flat[offs[i]:offs[i + 1]].reshape(b[1], b[3])
             out.append(SparseCellMarginal(box, v[0] if self.ndim == 1 else v))
         return out
+
+    def download_marginals(self):
+        """(boxes [n_basic, 4], concatenated values, offsets): the basic-cell Y-marginals
+        compacted on the device (only the entries inside each box leave it)."""
+        import torch
+
+        b = self.ybox.view(-1, 4).to(torch.int64)
+        sizes = b[:, 1] * b[:, 3]
+        vals = self.yval.view(self.n_basic, self.cap)
+        idx = torch.arange(self.cap, device=vals.device)[None, :] < sizes[:, None]
+        flat = vals[idx].cpu().numpy()
+        boxes = self.ybox.view(-1, 4).cpu().numpy()
+        szh = boxes[:, 1].astype(np.int64) * boxes[:, 3]
+        offs = np.concatenate([[0], np.cumsum(szh)])
+        return boxes, flat, offs
 
     @property
     def mu_nodes(self) -> list:
@@ -509,12 +523,16 @@ class PlanState:
         return out
 
     def sparsity(self) -> dict:
-        boxes = self.ybox.view(-1, 4).cpu().numpy()
-        sizes = (boxes[:, 1].astype(np.int64) * boxes[:, 3])
+        """Stored and non-zero entries of the basic-cell marginals (engine.py:198-201),
+        counted on the device (only two scalars leave it)."""
+        import torch
+
+        b = self.ybox.view(-1, 4).to(torch.int64)
+        sizes = b[:, 1] * b[:, 3]
         vals = self.yval.view(self.n_basic, self.cap)
-        idx = np.arange(self.cap)[None, :] < sizes[:, None]
-        nz = int(((vals != 0).cpu().numpy() & idx).sum())
-        return {"stored_entries": int(sizes.sum()), "nonzero_entries": nz}
+        idx = torch.arange(self.cap, device=vals.device)[None, :] < sizes[:, None]
+        nz = int(((vals != 0) & idx).sum().item())
+        return {"stored_entries": int(sizes.sum().item()), "nonzero_entries": nz}
 
     def clone(self) -> "PlanState":
         c = object.__new__(PlanState)

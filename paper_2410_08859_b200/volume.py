@@ -432,8 +432,7 @@ class PlanState3:
     # ---- host views (reference-shaped)
     @property
     def nu_i(self) -> list:
-        boxes = self.ybox.view(-1, 6).cpu().numpy()
-        vals = self.yval.view(self.n_basic, self.cap).cpu().numpy()
+        boxes, flat, offs = self.download_marginals()
         out = []
         for i in range(self.n_basic):
             b = boxes[i]
@@ -441,9 +440,23 @@ class PlanState3:
             if b[1] == 0 or b[3] == 0 or b[5] == 0:
                 out.append(SparseCellMarginal.empty(self.ndim))
                 continue
-            v = vals[i, :b[1] * b[3] * b[5]].reshape([e for _, e in box])
-            out.append(SparseCellMarginal(box, v))
+            out.append(SparseCellMarginal(box, flat[offs[i]:offs[i + 1]].reshape(
+                [e for _, e in box])))
         return out
+
+    def download_marginals(self):
+        """(boxes [n_basic, 6], concatenated values, offsets), compacted on the device."""
+        import torch
+
+        b = self.ybox.view(-1, 6).to(torch.int64)
+        sizes = b[:, 1] * b[:, 3] * b[:, 5]
+        vals = self.yval.view(self.n_basic, self.cap)
+        idx = torch.arange(self.cap, device=vals.device)[None, :] < sizes[:, None]
+        flat = vals[idx].cpu().numpy()
+        boxes = self.ybox.view(-1, 6).cpu().numpy()
+        szh = boxes[:, 1].astype(np.int64) * boxes[:, 3] * boxes[:, 5]
+        offs = np.concatenate([[0], np.cumsum(szh)])
+        return boxes, flat, offs
 
     @property
     def mu_nodes(self) -> list:
@@ -490,12 +503,15 @@ class PlanState3:
         return out
 
     def sparsity(self) -> dict:
-        boxes = self.ybox.view(-1, 6).cpu().numpy().astype(np.int64)
-        sizes = boxes[:, 1] * boxes[:, 3] * boxes[:, 5]
+        """Stored and non-zero entries of the basic-cell marginals, counted on the device."""
+        import torch
+
+        b = self.ybox.view(-1, 6).to(torch.int64)
+        sizes = b[:, 1] * b[:, 3] * b[:, 5]
         vals = self.yval.view(self.n_basic, self.cap)
-        idx = np.arange(self.cap)[None, :] < sizes[:, None]
-        nz = int(((vals != 0).cpu().numpy() & idx).sum())
-        return {"stored_entries": int(sizes.sum()), "nonzero_entries": nz}
+        idx = torch.arange(self.cap, device=vals.device)[None, :] < sizes[:, None]
+        nz = int(((vals != 0) & idx).sum().item())
+        return {"stored_entries": int(sizes.sum().item()), "nonzero_entries": nz}
 
     def clone(self) -> "PlanState3":
         c = object.__new__(PlanState3)
