@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-export DD_LIB_PATH=$PWD/build_nt1024/libdomdec_b200.so
-DD_PROBE_BATCHES=0 timeout 400 python scripts/probe_spec.py 2 99999 > gpurun_out/ms1024_nt1024.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 400 -k "default" > gpurun_out/p_nt1024.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_volume.py tests/test_gpu_sharded.py tests/test_gpu_volume_sharded.py tests/test_gpu_fp32.py -q --timeout 600 -x > gpurun_out/p_sp.log 2>&1
+timeout 600 python bench.py --cpu-sample 0 > gpurun_out/bench_sp.log 2>&1
+timeout 600 python bench.py --config vol_128 --cpu-sample 0 > gpurun_out/bench_vol_sp.log 2>&1
