@@ -147,3 +147,48 @@ def test_global_sinkhorn_matches_reference():
     assert rel_err(r.alpha.cpu().numpy().reshape(n, n), g["alpha"]) < 1e-10
     assert rel_err(r.beta.cpu().numpy().reshape(n, n), g["beta"]) < 1e-10
     assert r.gap == pytest.approx(float(g["gap"]), rel=1e-8)
+
+
+def test_cut_plan_2d_kernel_matches_embedded_three_axis_cut():
+    """The 2D per-term plan cut (dd_cut_plan, every term of the full Y grid) and the
+    three-axis separable cut the warm start uses on the (1, n0, n1) embedding agree:
+    same boxes, marginals / X-marginals / fragments to 1e-12."""
+    import warnings
+
+    import torch
+    from _engine_run import problem_from_golden
+    from paper_2410_08859_b200 import _lib
+    from paper_2410_08859_b200.decomposition import make_decomposition
+    from paper_2410_08859_b200.engine import PlanState, _cut_plan_embedded
+    from paper_2410_08859_b200.sinkhorn import DeviceProblem, SolverConfig, sinkhorn_solve
+
+    g = load("mix32_staggered")
+    prob = problem_from_golden(g)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        dec = make_decomposition(prob.mu, int(g["s"]))
+    dp = DeviceProblem(prob)
+    res = sinkhorn_solve(dp, config=SolverConfig(delta=1e-3))
+    a = PlanState(prob, dec.basic, dp, cap=1)
+    tr_a = torch.zeros(a.n_basic, dtype=torch.float64, device="cuda")
+    boxes = torch.zeros(a.n_basic * 4, dtype=torch.int32, device="cuda")
+    L = _lib.lib()
+    s = a.state_struct()
+    s.yval = None
+    _lib.check(L.dd_cut_plan(dp.geom, s, res.alpha.data_ptr(), res.beta.data_ptr(), 1e-15,
+                             tr_a.data_ptr(), boxes.data_ptr(), _lib.stream_handle()))
+    bh = boxes.view(-1, 4).cpu().numpy()
+    a.ensure_cap(int((bh[:, 1].astype(np.int64) * bh[:, 3]).max(initial=1)))
+    _lib.check(L.dd_cut_plan(dp.geom, a.state_struct(), res.alpha.data_ptr(), res.beta.data_ptr(),
+                             1e-15, tr_a.data_ptr(), boxes.data_ptr(), _lib.stream_handle()))
+    b = PlanState(prob, dec.basic, dp, cap=1)
+    tr_b = torch.zeros(b.n_basic, dtype=torch.float64, device="cuda")
+    _cut_plan_embedded(b, dp, res.alpha, res.beta, 1e-15, tr_b)
+    assert np.array_equal(a.ybox.cpu().numpy(), b.ybox.cpu().numpy())
+    for ma, mb in zip(a.nu_i, b.nu_i):
+        assert ma.box == mb.box
+        if not ma.is_empty:
+            assert rel_err(mb.values, ma.values) < 1e-12
+    assert rel_err(b.x_marg_d.cpu().numpy(), a.x_marg_d.cpu().numpy()) < 1e-12
+    assert rel_err(b.transport, a.transport) < 1e-12
+    assert rel_err(b.kl, a.kl) < 1e-12
