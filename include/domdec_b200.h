@@ -420,9 +420,12 @@ int dd3_cell_solve(const dd3_geom* g, const dd3_state* s, const dd3_batch* b, vo
 int dd3_cell_delta(const dd3_geom* g, const dd3_state* s, const dd3_batch* b, double theta_safe,
                    double* dy, double* cd, void* stream);
 /* Commit theta-blends (per cell theta[c]); stores duals, stitches alpha into alpha_grid
- * (nullable); errs[c*4] = x_err, y_err, truncated mass added, unused. */
+ * (nullable); errs[c*4] = x_err, y_err, truncated mass added, unused.  If yrun is
+ * non-NULL it is updated in place: += new window - old window, clipped at 0
+ * (iteration_sequential, engine.py:829-830; one cell per call). */
 int dd3_cell_commit(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
-                    const double* theta, double* alpha_grid, double* errs, void* stream);
+                    const double* theta, double* alpha_grid, double* yrun, double* errs,
+                    void* stream);
 /* out (Y grid) = base (nullable: 0) + sum_i scale_i * v_i over item boxes, accumulated in
  * item order (product rounded before the add).  Item i: box at box + i*bstride, values
  * at vals + (voff ? voff[i] : i*vstride), compact row-major over its box; scale nullable.

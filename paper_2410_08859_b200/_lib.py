@@ -91,7 +91,7 @@ _SIGS = {
     "dd3_cell_ws_size": ([vp, vp], i64),
     "dd3_cell_solve": ([G3, S3, B3, vp], C.c_int),
     "dd3_cell_delta": ([G3, S3, B3, dbl, vp, vp, vp], C.c_int),
-    "dd3_cell_commit": ([G3, S3, B3, vp, vp, vp, vp], C.c_int),
+    "dd3_cell_commit": ([G3, S3, B3, vp, vp, vp, vp, vp], C.c_int),
     "dd3_gather": ([G3, C.c_int, vp, C.c_int, vp, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp],
                    C.c_int),
     "dd3_cell_terms": ([G3, S3, vp, vp], C.c_int),

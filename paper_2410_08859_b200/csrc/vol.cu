@@ -1118,7 +1118,7 @@ __global__ void __launch_bounds__(NT) cell_delta3_kernel(dd3_geom g, dd3_state s
 
 __global__ void __launch_bounds__(NT) cell_commit3_kernel(dd3_geom g, dd3_state s, dd3_batch b,
                                                           const double* theta, double* alpha_grid,
-                                                          double* errs) {
+                                                          double* yrun, double* errs) {
     __shared__ double red[NW];
     __shared__ int redi[NW];
     __shared__ int32_t sobox[64 * 6];
@@ -1237,10 +1237,16 @@ __global__ void __launch_bounds__(NT) cell_commit3_kernel(dd3_geom g, dd3_state 
         unflat(y, yb.e[1], yb.e[2], y0, y1, y2);
         const int64_t id = ((int64_t)(yb.o[0] + y0) * g.ny[1] + yb.o[1] + y1) * g.ny[2] + yb.o[2] + y2;
         const double nu = s.nu[id];
-        double yn = 0.0;
-        for (int k = 0; k < n_mem; ++k) yn += th > 0.0 ? V[(int64_t)k * ny + y] : OLD[(int64_t)k * ny + y];
+        double yn = 0.0, yo = 0.0;
+        for (int k = 0; k < n_mem; ++k) {
+            yn += th > 0.0 ? V[(int64_t)k * ny + y] : OLD[(int64_t)k * ny + y];
+            yo += OLD[(int64_t)k * ny + y];
+        }
         const double num = b.mdens[yoff + y] * nu;
         yerr += fabs(yn + num - exp(-beta[y] / g.lam) * nu);
+        // sequential mode: running Y-marginal += new window - old window, clipped at 0
+        // (engine.py:829-830)
+        if (yrun) yrun[id] = fmax(yrun[id] + (yn - yo), 0.0);
     }
     double xerr = 0.0;
     for (int k = 0; k < n_mem; ++k) {
@@ -2200,11 +2206,11 @@ extern "C" int dd3_cell_delta(const dd3_geom* g, const dd3_state* s, const dd3_b
 }
 
 extern "C" int dd3_cell_commit(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
-                               const double* theta, double* alpha_grid, double* errs,
-                               void* stream) {
+                               const double* theta, double* alpha_grid, double* yrun,
+                               double* errs, void* stream) {
     if (b->n_cells <= 0) return 0;
     v3::cell_commit3_kernel<<<b->n_cells, v3::NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, theta,
-                                                                            alpha_grid, errs);
+                                                                            alpha_grid, yrun, errs);
     return dd_set_error(cudaGetLastError());
 }
 

@@ -44,7 +44,7 @@ __all__ = ["VolumeProblem", "GridSweeper3", "PlanState3", "initial_plan_state3",
            "warm_start_plan3", "iteration_parallel3", "domdec_solve3", "multiscale_solve3",
            "STRATEGIES_3D"]
 
-STRATEGIES_3D = ("staggered", "fast", "safe")
+STRATEGIES_3D = ("staggered", "fast", "safe", "swift", "sequential")
 MAX_MEMBERS = 64
 
 
@@ -728,14 +728,14 @@ class _Batch3:
         c2 = self.cstat2[:self.n * 8].view(self.n, 8).cpu().numpy()
         return c1, c2
 
-    def commit(self, theta: np.ndarray, alpha_grid=None) -> np.ndarray:
+    def commit(self, theta: np.ndarray, alpha_grid=None, yrun=None) -> np.ndarray:
         import torch
 
         st = self.st
         th = torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64)).to(st.dp.device)
         errs = st.buf.get("errs", self.n * 4, torch.float64)
         _lib.check(_lib.lib().dd3_cell_commit(st.dp.geom, st.state_struct(self.store), self.batch,
-                                              th.data_ptr(), _lib.ptr(alpha_grid),
+                                              th.data_ptr(), _lib.ptr(alpha_grid), _lib.ptr(yrun),
                                               errs.data_ptr(), _lib.stream_handle()))
         e = errs[:self.n * 4].view(self.n, 4).cpu().numpy().copy()
         if len(self.mflat):
@@ -852,6 +852,38 @@ def cell_lse_flops3(w, n0, n1, n2):
     return 2.0 * (y_sweep + x_sweep)
 
 
+def iteration_sequential3(plan: PlanState3, part: CompositePartition, config, stats):
+    """Cell-by-cell pass in lattice row-major order on a running Y-marginal, each
+    cell committed at theta = 1 before the next is set up (engine.py:799-836).
+    The running marginal is updated on the device by the commit kernel."""
+    import torch
+
+    if _shard() is not None:
+        raise ValueError("the sequential sweep is inherently serial; run it on one rank")
+    cfg = config.cell_config()
+    pt = _tables(part)
+    if stats.alpha is None:
+        stats.alpha = torch.zeros(plan.dp.nx, dtype=torch.float64, device=plan.dp.device)
+    t0 = time.perf_counter()
+    y_run = plan.assemble_device(plan.buf.get("yrun", plan.dp.ny, torch.float64))
+    stats.assemble_time += time.perf_counter() - t0
+    for j in range(pt.ncomp):
+        t0 = time.perf_counter()
+        bt = _Batch3(plan, pt, np.array([j], dtype=np.int64), y_run, cfg)
+        bt.solve()
+        _absorb(stats, bt)
+        stats.solve_time += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        e = bt.commit(np.ones(1), stats.alpha, y_run)
+        stats.commit_time += time.perf_counter() - t0
+        stats.x_err += float(e[0, 0])
+        stats.y_err += float(e[0, 1])
+        plan.truncated_mass += float(e[0, 2])
+        stats.truncated_mass += float(e[0, 2])
+    stats.action = "sequential"
+    return plan
+
+
 def iteration_parallel3(plan: PlanState3, part: CompositePartition, strategy, config, stats):
     """Snapshot, batch solve, weighted commit (engine.py:839-922), on the device.
 
@@ -900,6 +932,12 @@ def iteration_parallel3(plan: PlanState3, part: CompositePartition, strategy, co
         elif strategy.kind == "safe":
             th = 1.0 / kb
             actions.append("safe")
+        elif strategy.kind == "swift":
+            # better of greedy (ones) and safe (1/K), ties to greedy (engine.py:543-554)
+            scorer = BlendScorer3(plan, bt, snapshot, 1.0 / kb, pos, kb)
+            greedy = scorer.energy_at(1.0) <= scorer.energy_at(1.0 / kb)
+            th = 1.0 if greedy else 1.0 / kb
+            actions.append("greedy" if greedy else "safe")
         else:
             scorer = BlendScorer3(plan, bt, snapshot, 1.0 / kb, pos, kb)
             e_base = scorer.energy_at(0.0)
@@ -968,7 +1006,10 @@ def domdec_solve3(problem: TransportProblem, partitions: Decomposition, strategy
         part = partitions.composites[(k - 1) % len(partitions.composites)]
         stats = IterationStats(k=k, label=part.label)
         t0 = time.perf_counter()
-        iteration_parallel3(state, part, strategy, config, stats)
+        if strategy.kind == "sequential":
+            iteration_sequential3(state, part, config, stats)
+        else:
+            iteration_parallel3(state, part, strategy, config, stats)
         sb = state.energy()
         if k % check_every == 0 or k == config.max_iters:
             t1 = time.perf_counter()

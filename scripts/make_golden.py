@@ -119,6 +119,12 @@ VOL_CASES = [
          warm=False, seed=4),
     dict(name="vol32_warm", n=32, s=4, lam=1.0, strategy="staggered", delta=2e-5, max_iters=4,
          warm=True, seed=5),
+    dict(name="vol8_swift", n=8, s=2, lam=0.8, strategy="swift", delta=1e-5, max_iters=4,
+         warm=False, seed=6),
+    dict(name="vol8_sequential", n=8, s=2, lam=1.0, strategy="sequential", delta=1e-5,
+         max_iters=4, warm=False, seed=7),
+    dict(name="vol16_swift_warm", n=16, s=4, lam=1.0, strategy="swift", delta=2e-5,
+         max_iters=3, warm=True, seed=8),
 ]
 
 

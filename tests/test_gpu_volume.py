@@ -25,9 +25,10 @@ DUAL_TOL = 1e-9
 OBJ_TOL = 1e-10
 
 VOL_CASES = ["vol8_staggered", "vol8_safe", "vol8_fast_warm", "vol16_warm", "vol16_cold",
-             "vol32_warm"]
-EMBEDDED_CASES = ["toy1d_staggered", "toy1d_safe", "toy1d_fast", "mix16_staggered", "mix16_warm",
-                  "mix32_staggered", "mix16_cellcap", "mix16_zeros", "pr1_64"]
+             "vol32_warm", "vol8_swift", "vol8_sequential", "vol16_swift_warm"]
+EMBEDDED_CASES = ["toy1d_staggered", "toy1d_safe", "toy1d_fast", "toy1d_swift", "toy1d_sequential",
+                  "toy1d_cellcap_swift", "mix16_staggered", "mix16_warm", "mix32_staggered",
+                  "mix16_cellcap", "mix16_zeros", "pr1_64"]
 
 
 def _box6(b):
