@@ -426,6 +426,18 @@ int dd3_cell_delta(const dd3_geom* g, const dd3_state* s, const dd3_batch* b, do
 int dd3_cell_commit(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
                     const double* theta, double* alpha_grid, double* yrun, double* errs,
                     void* stream);
+/* opt strategy (engine.py:378-527): out[c] = lam * sum over cell c's members of
+ * KL((1 - theta[c]) x_old + theta[c] x_new | mu) (BlendScorer._d1_blend). */
+int dd3_blend_d1(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
+                 const double* theta, double* out, void* stream);
+/* Coordinate-descent pieces of cell c (_coordinate_root's g_and_h, lam-free):
+ * out[0..1] = X-side sum d log(x/mu), sum d^2/x; out[2..3] = Y-side sum dy log(y/nu),
+ * sum dy^2/y with y = clip(clip(ycur - th_cur dy, 0) + th dy, 0). */
+int dd3_opt_gh(const dd3_geom* g, const dd3_state* s, const dd3_batch* b, const double* dy,
+               int c, double th, double th_cur, const double* ycur, double* out, void* stream);
+/* ycur[window of cell c] = clip(ycur + dth * dy_c, 0) (BlendScorer.set_theta). */
+int dd3_opt_set(const dd3_geom* g, const dd3_batch* b, const double* dy, int c, double dth,
+                double* ycur, void* stream);
 /* out (Y grid) = base (nullable: 0) + sum_i scale_i * v_i over item boxes, accumulated in
  * item order (product rounded before the add).  Item i: box at box + i*bstride, values
  * at vals + (voff ? voff[i] : i*vstride), compact row-major over its box; scale nullable.

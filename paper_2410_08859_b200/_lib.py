@@ -28,6 +28,7 @@ EXPORTS = [
     "dd3_grid_ws", "dd3_grid_lse", "dd3_prolong", "dd3_cell_ws_size", "dd3_cell_solve",
     "dd3_cell_delta", "dd3_cell_commit", "dd3_gather", "dd3_cell_terms", "dd3_product_init",
     "dd3_cut_tiles", "dd3_cut_plan", "dd3_seed_duals", "dd3_sinkhorn_ws", "dd3_sinkhorn_run",
+    "dd3_blend_d1", "dd3_opt_gh", "dd3_opt_set",
 ]
 
 i32, i64, dbl, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
@@ -92,6 +93,9 @@ _SIGS = {
     "dd3_cell_solve": ([G3, S3, B3, vp], C.c_int),
     "dd3_cell_delta": ([G3, S3, B3, dbl, vp, vp, vp], C.c_int),
     "dd3_cell_commit": ([G3, S3, B3, vp, vp, vp, vp, vp], C.c_int),
+    "dd3_blend_d1": ([G3, S3, B3, vp, vp, vp], C.c_int),
+    "dd3_opt_gh": ([G3, S3, B3, vp, C.c_int, dbl, dbl, vp, vp, vp], C.c_int),
+    "dd3_opt_set": ([G3, B3, vp, C.c_int, dbl, vp, vp], C.c_int),
     "dd3_gather": ([G3, C.c_int, vp, C.c_int, vp, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp],
                    C.c_int),
     "dd3_cell_terms": ([G3, S3, vp, vp], C.c_int),
@@ -181,7 +185,7 @@ KERNELS_PER_CALL = {
     "dd_opt_set": 1, "dd_refine": 1, "dd_prolong": 1,
     "dd3_grid_lse": 6, "dd3_prolong": 1, "dd3_cell_solve": 1, "dd3_cell_delta": 1,
     "dd3_cell_commit": 1, "dd3_gather": 1, "dd3_cell_terms": 1, "dd3_product_init": 1,
-    "dd3_cut_plan": 2, "dd3_seed_duals": 1,
+    "dd3_cut_plan": 2, "dd3_seed_duals": 1, "dd3_blend_d1": 1, "dd3_opt_gh": 1, "dd3_opt_set": 1,
 }
 
 

@@ -1114,6 +1114,101 @@ __global__ void __launch_bounds__(NT) cell_delta3_kernel(dd3_geom g, dd3_state s
     }
 }
 
+// ---- opt strategy pieces (engine.py:378-470, 473-527) ---------------------------------
+
+// out[c] = lam * sum over cell c's members of KL((1 - theta_c) xo + theta_c xn | mu)
+// (BlendScorer._d1_blend at a per-cell weight; energy_at of a general theta vector)
+__global__ void __launch_bounds__(NT) blend_d1_3_kernel(dd3_geom g, dd3_state s, dd3_batch b,
+                                                        const double* theta, double* out) {
+    __shared__ double red[NW];
+    const int c = blockIdx.x;
+    const int32_t* d = b.desc + (int64_t)c * 16;
+    const int n_mem = d[13], mb = d[14];
+    const int64_t xoff = b.offs[(int64_t)c * 4 + 3];
+    const int bs = s.block[0] * s.block[1] * s.block[2];
+    const double th = theta[c];
+    double tot = 0.0;
+    for (int k = 0; k < n_mem; ++k) {
+        const int i = b.members[mb + k];
+        const double* xo = s.x_marg + (int64_t)i * bs;
+        const double* xn = b.xarena + xoff + (int64_t)k * bs;
+        tot += bsum(block_kl(g, s, i, xn, th, xo, 1), red);
+    }
+    if (threadIdx.x == 0) out[c] = g.lam * tot;
+}
+
+// Derivative pieces of the blend objective in cell c's weight (coordinate descent):
+// out[0] = sum d log(x/mu), out[1] = sum d^2/x over the members' X blocks, d = xn - xo,
+// x = (1-th) xo + th xn; out[2] = sum dy log(y/nu), out[3] = sum dy^2/y over the cell's
+// Y window, y = clip(clip(ycur - th_cur dy, 0) + th dy, 0).  Entries with a zero update
+// direction are skipped (the reference's np.where(d == 0, 0, ...)).  All lam-free.
+__global__ void __launch_bounds__(NT) opt_gh3_kernel(dd3_geom g, dd3_state s, dd3_batch b,
+                                                     const double* dy, int c, double th,
+                                                     double th_cur, const double* ycur,
+                                                     double* out) {
+    __shared__ double red[NW];
+    const int32_t* d = b.desc + (int64_t)c * 16;
+    const B3 yb = ldbox(d + 7);
+    const int n_mem = d[13], mb = d[14];
+    const int64_t ny = bsize(yb);
+    const int64_t yoff = b.offs[(int64_t)c * 4 + 0], xoff = b.offs[(int64_t)c * 4 + 3];
+    const int bs = s.block[0] * s.block[1] * s.block[2];
+    double gx = 0.0, hx = 0.0;
+    for (int k = 0; k < n_mem; ++k) {
+        const int i = b.members[mb + k];
+        const B3 bx = ldbox(s.basic_xbox + (int64_t)i * 6);
+        const int nb = bx.e[0] * bx.e[1] * bx.e[2];
+        const double* xo = s.x_marg + (int64_t)i * bs;
+        const double* xn = b.xarena + xoff + (int64_t)k * bs;
+        for (int t = threadIdx.x; t < nb; t += NT) {
+            int t0, t1, t2;
+            unflat(t, bx.e[1], bx.e[2], t0, t1, t2);
+            const double mu = s.mu[((int64_t)(bx.o[0] + t0) * g.nx[1] + bx.o[1] + t1) * g.nx[2] +
+                                   bx.o[2] + t2];
+            if (!(mu > 0)) continue;
+            const double dd = xn[t] - xo[t];
+            if (dd == 0.0) continue;
+            const double x = (1.0 - th) * xo[t] + th * xn[t];
+            gx += dd * log(x / mu);
+            hx += dd * dd / x;
+        }
+    }
+    double gy = 0.0, hy = 0.0;
+    for (int64_t y = threadIdx.x; y < ny; y += NT) {
+        const double dv = dy[yoff + y];
+        if (dv == 0.0) continue;
+        int y0, y1, y2;
+        unflat(y, yb.e[1], yb.e[2], y0, y1, y2);
+        const int64_t id = ((int64_t)(yb.o[0] + y0) * g.ny[1] + yb.o[1] + y1) * g.ny[2] +
+                           yb.o[2] + y2;
+        const double ybv = fmax(ycur[id] - th_cur * dv, 0.0);
+        const double yv = fmax(ybv + th * dv, 0.0);
+        gy += dv * log(yv / s.nu[id]);
+        hy += dv * dv / yv;
+    }
+    gx = bsum(gx, red);
+    hx = bsum(hx, red);
+    gy = bsum(gy, red);
+    hy = bsum(hy, red);
+    if (threadIdx.x == 0) { out[0] = gx; out[1] = hx; out[2] = gy; out[3] = hy; }
+}
+
+// ycur[window of cell c] = clip(ycur + dth * dy, 0)   (BlendScorer.set_theta)
+__global__ void __launch_bounds__(NT) opt_set3_kernel(dd3_geom g, dd3_batch b, const double* dy,
+                                                      int c, double dth, double* ycur) {
+    const int32_t* d = b.desc + (int64_t)c * 16;
+    const B3 yb = ldbox(d + 7);
+    const int64_t ny = bsize(yb);
+    const int64_t yoff = b.offs[(int64_t)c * 4 + 0];
+    for (int64_t y = threadIdx.x; y < ny; y += NT) {
+        int y0, y1, y2;
+        unflat(y, yb.e[1], yb.e[2], y0, y1, y2);
+        const int64_t id = ((int64_t)(yb.o[0] + y0) * g.ny[1] + yb.o[1] + y1) * g.ny[2] +
+                           yb.o[2] + y2;
+        ycur[id] = fmax(ycur[id] + dth * dy[yoff + y], 0.0);
+    }
+}
+
 // ---- commit (engine.py:726-785) ------------------------------------------------------
 
 __global__ void __launch_bounds__(NT) cell_commit3_kernel(dd3_geom g, dd3_state s, dd3_batch b,
@@ -2202,6 +2297,29 @@ extern "C" int dd3_cell_delta(const dd3_geom* g, const dd3_state* s, const dd3_b
     if (b->n_cells <= 0) return 0;
     v3::cell_delta3_kernel<<<b->n_cells, v3::NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, theta_safe,
                                                                            dy, cd);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd3_blend_d1(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
+                            const double* theta, double* out, void* stream) {
+    if (b->n_cells <= 0) return 0;
+    v3::blend_d1_3_kernel<<<b->n_cells, v3::NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, theta, out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd3_opt_gh(const dd3_geom* g, const dd3_state* s, const dd3_batch* b,
+                          const double* dy, int c, double th, double th_cur, const double* ycur,
+                          double* out, void* stream) {
+    if (c < 0 || c >= b->n_cells) return dd_set_error(cudaErrorInvalidValue);
+    v3::opt_gh3_kernel<<<1, v3::NT, 0, (cudaStream_t)stream>>>(*g, *s, *b, dy, c, th, th_cur,
+                                                               ycur, out);
+    return dd_set_error(cudaGetLastError());
+}
+
+extern "C" int dd3_opt_set(const dd3_geom* g, const dd3_batch* b, const double* dy, int c,
+                           double dth, double* ycur, void* stream) {
+    if (c < 0 || c >= b->n_cells) return dd_set_error(cudaErrorInvalidValue);
+    v3::opt_set3_kernel<<<1, v3::NT, 0, (cudaStream_t)stream>>>(*g, *b, dy, c, dth, ycur);
     return dd_set_error(cudaGetLastError());
 }
 

@@ -974,6 +974,9 @@ class BlendScorer:
         self.theta = np.zeros(self.n)
         self.evaluations = 0
 
+    def opt_state(self) -> "_OptState":
+        return _OptState(self)
+
     # reference-shaped incremental view (engine.py:458-470), kept on the device
     def _op(self) -> "_OptState":
         if getattr(self, "_opt", None) is None:
@@ -1125,12 +1128,12 @@ def get_weights_opt(old_cells, new_cells, part, scorer: BlendScorer, max_sweeps:
     iterate, greedy, safe} (engine.py:557-588)."""
     ids = _cell_ids(new_cells)
     k = len(ids)
-    if scorer.batch.shard is not None:
+    if getattr(scorer, "sharded", False) or getattr(scorer.batch, "shard", None) is not None:
         raise ValueError("the opt strategy needs per-cell global coordination inside a batch; "
                          "slab-sharded solves support safe, fast, swift and staggered")
     ones, safe = np.ones(k), np.full(k, 1.0 / k)
     start = ones if scorer.energy_at(ones) <= scorer.energy_at(safe) else safe
-    op = _OptState(scorer)
+    op = scorer.opt_state()
     for i in range(k):
         op.set_theta(i, float(start[i]))
     for _ in range(max_sweeps):

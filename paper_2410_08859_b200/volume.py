@@ -44,7 +44,7 @@ __all__ = ["VolumeProblem", "GridSweeper3", "PlanState3", "initial_plan_state3",
            "warm_start_plan3", "iteration_parallel3", "domdec_solve3", "multiscale_solve3",
            "STRATEGIES_3D"]
 
-STRATEGIES_3D = ("staggered", "fast", "safe", "swift", "sequential")
+STRATEGIES_3D = ("staggered", "fast", "safe", "swift", "opt", "sequential")
 MAX_MEMBERS = 64
 
 
@@ -781,9 +781,45 @@ class BlendScorer3:
         self.theta_safe = float(theta_safe)
         self.dev = dev
 
-    def energy_at(self, theta: float) -> float:
+    def opt_state(self) -> "_OptState3":
+        return _OptState3(self)
+
+    def _energy_vec(self, th) -> float:
+        """energy_at of a per-cell weight vector (engine.py:441-456): per-cell pieces
+        in cell order, d1 of each blended cell from ``dd3_blend_d1``, then the Y-side
+        KL of clip(snapshot + sum_c theta_c dy_c)."""
         import torch
 
+        if self.sharded:
+            raise ValueError("per-cell weight vectors need the whole batch on one rank")
+        b, p = self.batch, self.plan
+        thd = torch.from_numpy(np.ascontiguousarray(th, dtype=np.float64)).to(self.dev)
+        d1c = p.buf.get("blend_d1", max(b.n, 1), torch.float64)
+        _lib.check(_lib.lib().dd3_blend_d1(p.dp.geom, p.state_struct(b.store), b.batch,
+                                           thd.data_ptr(), d1c.data_ptr(), _lib.stream_handle()))
+        d1n = d1c[:b.n].cpu().numpy()
+        t, kl, d1 = self.base_t, self.base_kl, self.base_d1
+        for c in range(self.n_all):
+            tc = float(th[c])
+            if tc:
+                t += tc * self.cd[c, 0]
+                kl += tc * self.cd[c, 1]
+                d1 += float(d1n[c]) - self.cd[c, 2]
+        y = p.buf.get("blend_y", p.dp.ny, torch.float64)
+        part = p._partial(y)
+        npart = ctypes.c_int(0)
+        _lib.check(_lib.lib().dd3_gather(
+            p.dp.geom, b.n, b.ybox_d.data_ptr(), 6, self.dy.data_ptr(), 0,
+            b.yoff_d.data_ptr(), thd.data_ptr(), self.snapshot.data_ptr(), y.data_ptr(), 2,
+            p.dp.nu.data_ptr(), part.data_ptr(), ctypes.byref(npart), _lib.stream_handle()))
+        d2 = self.lam * float(part[:npart.value].sum().item())
+        return t + self.eps * kl + d1 + d2
+
+    def energy_at(self, theta) -> float:
+        import torch
+
+        if np.ndim(theta) == 1:
+            return self._energy_vec(np.asarray(theta, dtype=np.float64))
         b, p = self.batch, self.plan
         t, kl, d1 = self.base_t, self.base_kl, self.base_d1
         th = float(theta)
@@ -814,6 +850,54 @@ class BlendScorer3:
             _shard().all_reduce(y[:p.dp.ny])
             d2 = self.lam * p.grid_kl(y, clip=True, base=self.snapshot)
         return t + self.eps * kl + d1 + d2
+
+
+class _OptState3:
+    """Incremental blend view for coordinate descent on the three-axis path
+    (BlendScorer.set_theta / minimize_coordinate, engine.py:458-470), on the device."""
+
+    def __init__(self, scorer: BlendScorer3):
+        import torch
+
+        self.sc = scorer
+        p = scorer.plan
+        ny = p.dp.ny
+        self.ycur = p.buf.get("opt_ycur", ny, torch.float64)
+        self.ycur[:ny].copy_(scorer.snapshot[:ny])
+        self.out = p.buf.get("opt_out", 4, torch.float64)
+        self.lin = scorer.cd[:, 0] + scorer.eps * scorer.cd[:, 1]
+        self.theta = np.zeros(scorer.n_all)
+
+    def set_theta(self, i: int, th: float) -> None:
+        sc = self.sc
+        dth = th - self.theta[i]
+        if dth:
+            _lib.check(_lib.lib().dd3_opt_set(sc.plan.dp.geom, sc.batch.batch, sc.dy.data_ptr(),
+                                              int(i), float(dth), self.ycur.data_ptr(),
+                                              _lib.stream_handle()))
+        self.theta[i] = th
+
+    def minimize_coordinate(self, i: int, tol: float) -> float:
+        from .engine import _coordinate_root
+
+        sc = self.sc
+        p, b = sc.plan, sc.batch
+        lam = sc.lam
+        lin = float(self.lin[i])
+        th_cur = float(self.theta[i])
+        sstruct = p.state_struct(b.store)
+
+        def gh(th):
+            _lib.check(_lib.lib().dd3_opt_gh(p.dp.geom, sstruct, b.batch, sc.dy.data_ptr(), int(i),
+                                             float(th), th_cur, self.ycur.data_ptr(),
+                                             self.out.data_ptr(), _lib.stream_handle()))
+            o = self.out[:4].cpu().numpy()
+            with np.errstate(invalid="ignore"):
+                g = lin + lam * float(o[0]) + lam * float(o[2])
+                h = lam * float(o[1]) + lam * float(o[3])
+            return g, h
+
+        return _coordinate_root(gh, tol)
 
 
 # -- iterations ---------------------------------------------------------------------------
@@ -938,6 +1022,18 @@ def iteration_parallel3(plan: PlanState3, part: CompositePartition, strategy, co
             greedy = scorer.energy_at(1.0) <= scorer.energy_at(1.0 / kb)
             th = 1.0 if greedy else 1.0 / kb
             actions.append("greedy" if greedy else "safe")
+        elif strategy.kind == "opt":
+            # cyclic coordinate descent on per-cell weights (engine.py:557-588)
+            if sh is not None:
+                raise ValueError("the opt strategy needs per-cell global coordination inside a "
+                                 "batch; slab-sharded solves support safe, fast, swift and "
+                                 "staggered")
+            from .engine import get_weights_opt
+            scorer = BlendScorer3(plan, bt, snapshot, 1.0 / kb)
+            w = get_weights_opt(None, list(range(kb)), part, scorer, strategy.opt_max_sweeps,
+                                strategy.opt_tol).theta
+            th = np.array([w[c] for c in range(kb)])
+            actions.append("opt")
         else:
             scorer = BlendScorer3(plan, bt, snapshot, 1.0 / kb, pos, kb)
             e_base = scorer.energy_at(0.0)
@@ -953,7 +1049,7 @@ def iteration_parallel3(plan: PlanState3, part: CompositePartition, strategy, co
                 stats.safe_fallbacks += 1
         stats.score_time += time.perf_counter() - t0
         t0 = time.perf_counter()
-        e = bt.commit(np.full(bt.n, th), stats.alpha)
+        e = bt.commit(th if np.ndim(th) == 1 else np.full(bt.n, th), stats.alpha)
         es = e[:, :3].sum(axis=0)
         if sh is not None:
             es = sh.reduce_np(es, "sum", plan.dp.device)

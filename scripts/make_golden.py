@@ -125,6 +125,10 @@ VOL_CASES = [
          max_iters=4, warm=False, seed=7),
     dict(name="vol16_swift_warm", n=16, s=4, lam=1.0, strategy="swift", delta=2e-5,
          max_iters=3, warm=True, seed=8),
+    dict(name="vol8_opt", n=8, s=2, lam=0.8, strategy="opt", delta=1e-5, max_iters=4,
+         warm=False, seed=9),
+    dict(name="vol16_opt_warm", n=16, s=4, lam=1.0, strategy="opt", delta=2e-5, max_iters=2,
+         warm=True, seed=10),
 ]
 
 

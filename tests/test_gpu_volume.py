@@ -23,11 +23,19 @@ pytestmark = pytest.mark.gpu
 MARG_TOL = 1e-9
 DUAL_TOL = 1e-9
 OBJ_TOL = 1e-10
+# opt strategy: the blend weights come from the reference's cyclic coordinate descent,
+# which stops once no weight moves by more than opt_tol = 1e-9 (engine.py:557-588).  The
+# two sides' g/h sums differ in the last ulp, so a sweep can stop one step apart and the
+# weights agree only to ~opt_tol; a blended marginal (and the duals stored with it) moves
+# linearly with that.  The objective is stationary in theta at the optimum, so it stays
+# at OBJ_TOL.
+OPT_STATE_TOL = 5e-9
 
 VOL_CASES = ["vol8_staggered", "vol8_safe", "vol8_fast_warm", "vol16_warm", "vol16_cold",
-             "vol32_warm", "vol8_swift", "vol8_sequential", "vol16_swift_warm"]
+             "vol32_warm", "vol8_swift", "vol8_sequential", "vol16_swift_warm", "vol8_opt",
+             "vol16_opt_warm"]
 EMBEDDED_CASES = ["toy1d_staggered", "toy1d_safe", "toy1d_fast", "toy1d_swift", "toy1d_sequential",
-                  "toy1d_cellcap_swift", "mix16_staggered", "mix16_warm", "mix32_staggered",
+                  "toy1d_cellcap_swift", "toy1d_opt", "mix16_zeros_warm_opt", "mix16_staggered", "mix16_warm", "mix32_staggered",
                   "mix16_cellcap", "mix16_zeros", "pr1_64"]
 
 
@@ -71,6 +79,7 @@ def _run(g):
 
 
 def _check(g, prob, st, rep):
+    tol = OPT_STATE_TOL if str(g["strategy"]) == "opt" else MARG_TOL
     assert rep.iterations == int(g["iterations"])
     assert [r.action for r in rep.trace] == [str(a) for a in g["trace_action"]]
     np.testing.assert_allclose([r.total for r in rep.trace], g["trace_total"], rtol=OBJ_TOL)
@@ -87,7 +96,7 @@ def _check(g, prob, st, rep):
         assert mine_b == want_b, f"cell {i}: box {mine_b} != reference {want_b}"
         want = _dense(want_b, g["nu_i_val"][offs[i]:offs[i + 1]], shape3)
         mine = _dense(mine_b, nu_i[i].values, shape3)
-        assert rel_err(mine, want) < MARG_TOL, f"cell {i}"
+        assert rel_err(mine, want) < tol, f"cell {i}"
     duals = st.duals
     for k, key in enumerate(g["dual_keys"]):
         label, j = str(key).split(":")
@@ -95,10 +104,10 @@ def _check(g, prob, st, rep):
         a = g["dual_alpha"][g["dual_alpha_off"][k]:g["dual_alpha_off"][k + 1]]
         b = g["dual_beta"][g["dual_beta_off"][k]:g["dual_beta_off"][k + 1]]
         assert _box6([c for ax in d.beta_box for c in ax]) == _box6(g["dual_beta_box"][k])
-        assert rel_err(d.alpha, a) < DUAL_TOL, key
-        assert rel_err(d.beta, b) < DUAL_TOL, key
-    np.testing.assert_allclose(st.transport, g["transport"], rtol=1e-9, atol=1e-18)
-    np.testing.assert_allclose(st.kl, g["kl"], rtol=1e-9, atol=1e-15)
+        assert rel_err(d.alpha, a) < max(tol, DUAL_TOL), key
+        assert rel_err(d.beta, b) < max(tol, DUAL_TOL), key
+    np.testing.assert_allclose(st.transport, g["transport"], rtol=tol, atol=1e-18)
+    np.testing.assert_allclose(st.kl, g["kl"], rtol=tol, atol=1e-15)
     assert rep.rel_pd_gap == pytest.approx(float(g["rel_pd_gap"]), rel=1e-6, abs=1e-12)
 
 
