@@ -274,8 +274,14 @@ struct SweepScratch {
     double* f32s;   // fp32 mode: slopes the current tables use [X0, X1, Y0, Y1], valid [X, Y]
 };
 
-__device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
-                           double* out, SweepScratch sc) {
+// gred != nullptr: the cell gap test's per-thread terms (cells.py:336-340) are summed in
+// the output loop (thread t owns outputs t, t + DD_NT, ... in both loops, so the sums are
+// the separate loop's bit for bit) and each warp's sum is published in gred[wid] before
+// the sweep's final barrier.  Returns false when an output underflowed (the sweep was
+// redone stage-wise and the fused terms are void).
+__device__ bool cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
+                           double* out, SweepScratch sc, double* gred = nullptr,
+                           double lam = 1.0) {
     const int ny0 = c.ye0, ny1 = c.ye1, ny = c.ny, nx = nw0 * nw1;
     double lmax = kNegInf;
     int y = threadIdx.x;
@@ -347,6 +353,7 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
     }
     __syncthreads();
     int bad = 0;
+    double part = 0.0;
     for (int o = threadIdx.x; o < nx; o += DD_NT) {
         const int x0 = o / nw1, x1 = o - x0 * nw1;
         const double* kr = w.K0y + (int64_t)x0 * ny0;
@@ -358,15 +365,36 @@ __device__ void cell_lse_x(const Ws& w, const CellWin& c, int nw0, int nw1, doub
         }
         if (k < ny0) s0 = fma(kr[k], T[(int64_t)k * nw1 + x1], s0);
         const double sm = s0 + s1;
-        if (sm >= kTiny) out[o] = log(sm) + B;
-        else ++bad;
+        if (sm >= kTiny) {
+            const double Lv = log(sm) + B;
+            out[o] = Lv;
+            if (gred) {
+                const double mu = w.mu[o];
+                if (mu > 0) {
+                    const double a = w.alpha[o];
+                    const double lr = a / eps + Lv;
+                    const double px = mu * exp(lr);
+                    const double ref = mu * exp(-a / lam);
+                    part += px * (lr + a / lam) - px + ref;
+                }
+            }
+        } else {
+            ++bad;
+        }
+    }
+    if (gred) {
+        part = warp_sum(part);
+        if ((threadIdx.x & 31) == 0) gred[threadIdx.x >> 5] = part;
     }
     if (bad) *sc.flag = 1;
     __syncthreads();
     if (*sc.flag) {
         cell_lse_x_staged(w, c, nw0, nw1, eps, out);
+        return false;
     }
+    return true;
 }
+
 
 __device__ void cell_lse_y(const Ws& w, const CellWin& c, int nw0, int nw1, double eps,
                            double ratio, double* out, SweepScratch sc) {
@@ -1311,46 +1339,72 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
         if (tid < 2) { ndeg_sh[tid] = 0; moved_sh[tid] = 0; }
         int par = 0;
         stag_k = 0;
-        for (int k = 1; k <= b.max_iters; ++k) {
-            sweep_x<kF32>(w, cw, nw0, nw1, eps, ratio, w.L, sc);
-            if (k >= 2) {
-                double part = 0.0;
-                for (int x = tid; x < nx; x += DD_NT) {
-                    const double mu = w.mu[x];
-                    if (mu > 0) {
-                        const double a = w.alpha[x];
-                        const double lr = a / eps + w.L[x];
-                        const double px = mu * exp(lr);
-                        const double ref = mu * exp(-a / lam);
-                        part += px * (lr + a / lam) - px + ref;
-                    }
+        auto gap_terms = [&]() {
+            double part = 0.0;
+            for (int x = tid; x < nx; x += DD_NT) {
+                const double mu = w.mu[x];
+                if (mu > 0) {
+                    const double a = w.alpha[x];
+                    const double lr = a / eps + w.L[x];
+                    const double px = mu * exp(lr);
+                    const double ref = mu * exp(-a / lam);
+                    part += px * (lr + a / lam) - px + ref;
                 }
-                gap = lam * block_sum1(part, red2, par);
-                par ^= 1;
-                if (!have_first) { first_gap = gap; have_first = true; }
-                if (gap / lam <= thr) { converged = true; break; }
             }
-            // alpha = -ratio L is fused into the Y sweep's row preparation
-            sweep_y<kF32>(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
+            return block_sum1(part, red2, par);
+        };
+        auto newton_loop = [&](int cur) {
             int ndeg = 0;
             bool moved = false;
             for (int y = tid; y < ny; y += DD_NT) {
                 int dg = 0;
-                {
-                    const double ob = w.beta[y];
-                    const double lmv = lmw[y];
-                    const double nb = newton_node(w.ty[y], w.m[y], has_m, ob, eps, lam,
-                                                  b.newton_tol, b.newton_max_iters, &dg,
-                                                  &newton_steps, nullptr, lmv);
-                    moved |= (nb != ob);
-                    w.beta[y] = nb;
-                }
+                const double ob = w.beta[y];
+                const double nb = newton_node(w.ty[y], w.m[y], has_m, ob, eps, lam,
+                                              b.newton_tol, b.newton_max_iters, &dg,
+                                              &newton_steps, nullptr, lmw[y]);
+                moved |= (nb != ob);
+                w.beta[y] = nb;
                 ndeg += dg;
             }
-            const int cur = k & 1;
             if (ndeg) atomicAdd(&ndeg_sh[cur], ndeg);
             if (moved) moved_sh[cur] = 1;
             __syncthreads();
+        };
+        for (int k = 1; k <= b.max_iters; ++k) {
+            const int cur = k & 1;
+            if constexpr (!kF32) {
+                // fp64: the gap terms ride in the X sweep's output loop and its final
+                // barrier (the same per-thread sums and warp order as gap_terms)
+                const bool fused = cell_lse_x(w, cw, nw0, nw1, eps, w.L, sc,
+                                              k >= 2 ? red2 + par * DD_NW : nullptr, lam);
+                if (k >= 2) {
+                    double t = 0.0;
+                    if (fused) {
+                        const double* r = red2 + par * DD_NW;
+#pragma unroll
+                        for (int q = 0; q < DD_NW; ++q) t += r[q];
+                    } else {
+                        t = gap_terms();
+                    }
+                    gap = lam * t;
+                    par ^= 1;
+                    if (!have_first) { first_gap = gap; have_first = true; }
+                    if (gap / lam <= thr) { converged = true; break; }
+                }
+                // alpha = -ratio L is fused into the Y sweep's row preparation
+                sweep_y<kF32>(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
+                newton_loop(cur);
+            } else {
+                sweep_x<kF32>(w, cw, nw0, nw1, eps, ratio, w.L, sc);
+                if (k >= 2) {
+                    gap = lam * gap_terms();
+                    par ^= 1;
+                    if (!have_first) { first_gap = gap; have_first = true; }
+                    if (gap / lam <= thr) { converged = true; break; }
+                }
+                sweep_y<kF32>(w, cw, nw0, nw1, eps, ratio, w.ty, sc);
+                newton_loop(cur);
+            }
             // the previous iteration's count is final here (ordered by this barrier)
             newton_clamped = max(newton_clamped, ndeg_sh[cur]);
             const bool any_moved = moved_sh[cur] != 0;

@@ -119,9 +119,11 @@ __device__ __forceinline__ double block_max1(double v, double* red2, int parity)
     double* r = red2 + parity * DD_NW;
     if (lane == 0) r[wid] = v;
     __syncthreads();
-    double t = r[0];
+    // every warp folds the DD_NW partials across its lanes (max is exact, so the
+    // result does not depend on the order): one shared load per thread instead of DD_NW
+    double t = r[lane & (DD_NW - 1)];
 #pragma unroll
-    for (int k = 1; k < DD_NW; ++k) t = fmax(t, r[k]);
+    for (int o = DD_NW / 2; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
     return t;
 }
 
