@@ -375,6 +375,13 @@ def main():
                 "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": int(d2h)},
                 "gpu_launches": int(launches), "clocks": clk.summary()}
+        if args.precision == "fp32" and any("sweep_fallbacks" in r.diagnostics
+                                            for _, _, r in rep.stages):
+            line["fp32_sweeps"] = {
+                "cell_sweeps": int(sum(2 * r.diagnostics.get("cell_iterations", 0)
+                                       for _, _, r in rep.stages)),
+                "redone_in_fp64": int(sum(r.diagnostics.get("sweep_fallbacks", 0)
+                                          for _, _, r in rep.stages))}
         if world > 1:
             from paper_2410_08859_b200.engine import _SHARD as sh
             if sh is not None:

@@ -389,6 +389,10 @@ typedef struct dd3_batch {
     int32_t smem_doubles;      /* shared-memory doubles per cell CTA for the hot per-cell
                                   arrays (the host sizes it for the batch's largest window;
                                   a cell that does not fit keeps them in the workspace) */
+    int32_t precision;         /* 0: fp64 sweeps; 1: fp32 mode (the six contractions, their
+                                  tables and weights in fp32 with the linear part of the X-side
+                                  potential absorbed into the tables; state, Newton, gap test
+                                  and epilogue fp64; north_star tolerance 1e-4) */
 } dd3_batch;
 
 /* Workspace doubles of dd3_grid_lse for the geometry. */

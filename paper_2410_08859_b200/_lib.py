@@ -80,7 +80,7 @@ class Batch3(C.Structure):
                 ("alpha", vp), ("beta", vp), ("mdens", vp), ("work", vp), ("marena", vp),
                 ("xarena", vp), ("mbox", vp), ("mstat", vp), ("cstat", vp), ("cstat2", vp),
                 ("delta", dbl), ("max_iters", i32), ("newton_max_iters", i32),
-                ("newton_tol", dbl), ("trunc", dbl), ("smem_doubles", i32)]
+                ("newton_tol", dbl), ("trunc", dbl), ("smem_doubles", i32), ("precision", i32)]
 
 
 G3, S3, B3 = C.POINTER(Geom3), C.POINTER(State3), C.POINTER(Batch3)

@@ -1361,7 +1361,7 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
                 const double ob = w.beta[y];
                 const double nb = newton_node(w.ty[y], w.m[y], has_m, ob, eps, lam,
                                               b.newton_tol, b.newton_max_iters, &dg,
-                                              &newton_steps, nullptr, lmw[y]);
+                                              &newton_steps, nullptr, lmw[y], kF32);
                 moved |= (nb != ob);
                 w.beta[y] = nb;
                 ndeg += dg;

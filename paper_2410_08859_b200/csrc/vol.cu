@@ -388,6 +388,10 @@ struct Sh {
     int redi[32];
     int flag;
     int ndeg;
+    // fp32 mode: per-axis slopes the current tables absorb, rebuild request, force flag
+    double slope[3];
+    int rebuild;
+    int force;
 };
 
 // X sweep: L[x] = log sum_y exp(b[y] - c(x,y)/eps), b = beta/eps + lnu.
@@ -515,6 +519,238 @@ __device__ __forceinline__ double coord(const double* org, double dx, int a, int
     return org[a] + dx * (double)idx;
 }
 
+// ---- fp32 mode of the fast sweeps (north_star fp32 mode: 1e-4 relative) ---------------
+// The six contractions, their tables, weights and stage intermediates run in fp32; the
+// state (alpha, beta, L, z), the Newton Y-step, the gap test and the epilogue stay fp64.
+// A cell's X-side potential a = alpha/eps + log mu varies by (displacement / h) per node,
+// hundreds across the 2s-node window: more than fp32's exponent range, so one global
+// shift would underflow the dominant terms of most outputs.  Its linear part is
+// absorbed into the per-axis tables instead (still separable):
+//   a[x] - c(x,y)/eps = (a[x] - s.x) + sum_a (-(x_a - y_a)^2/eps + s_a x_a)
+//   L[x] + s.x        = log sum_y exp(b[y]) prod_a exp(-(x_a - y_a)^2/eps + s_a x_a)
+// with s_a the per-node slope of alpha/eps along axis a (x_a = window index), so the
+// shifted weights of both sweeps stay O(curvature).  Tables are Y-normalised as in the
+// fp64 path (column shifts c_a in fp64) and rebuilt when a slope moves by more than
+// kSlopeTol over the window.  An output whose shifted fp32 sum is below kTinyF may have
+// lost terms to underflow: that sweep is redone by the exact fp64 stage-wise path and
+// the slopes are refreshed.
+constexpr float kTinyF = 1e-30f;
+constexpr double kSlopeTol = 4.0;
+
+__device__ __forceinline__ float* f32p(double* p) { return reinterpret_cast<float*>(p); }
+
+// slopes of alpha/eps along the window's centre lines (one thread)
+__device__ __forceinline__ void slopes_now(const Cell& C, double eps, double* s) {
+    const int m0 = C.w[0] / 2, m1 = C.w[1] / 2, m2 = C.w[2] / 2;
+    const int w1 = C.w[1], w2 = C.w[2];
+    s[0] = C.w[0] > 1 ? (C.alpha[((C.w[0] - 1) * w1 + m1) * w2 + m2] - C.alpha[m1 * w2 + m2]) /
+                            ((C.w[0] - 1) * eps) : 0.0;
+    s[1] = w1 > 1 ? (C.alpha[(m0 * w1 + w1 - 1) * w2 + m2] - C.alpha[(m0 * w1) * w2 + m2]) /
+                        ((w1 - 1) * eps) : 0.0;
+    s[2] = w2 > 1 ? (C.alpha[(m0 * w1 + m1) * w2 + w2 - 1] - C.alpha[(m0 * w1 + m1) * w2]) /
+                        ((w2 - 1) * eps) : 0.0;
+    for (int a = 0; a < 3; ++a) if (!isfinite(s[a])) s[a] = 0.0;
+}
+
+// Tf_a[x_a][y_a] = exp(-(d^2)/eps + s_a x_a - c_a(y_a)), c_a(y_a) = max over x_a (fp64)
+template <int T>
+__device__ void build_tables_f32(const Cell& C, const dd3_geom& g, const Sh& sh) {
+    const double eps = g.eps;
+    for (int a = 0; a < 3; ++a) {
+        const double sa = sh.slope[a];
+        float* tf = f32p(C.kn[a]);
+        for (int ya = threadIdx.x; ya < C.n[a]; ya += T) {
+            const double yc = coord(g.y_org, g.y_dx, a, C.yb.o[a] + ya);
+            double cm = kNegInf;
+            for (int xa = 0; xa < C.w[a]; ++xa) {
+                const double dd_ = coord(g.x_org, g.x_dx, a, C.xb.o[a] + xa) - yc;
+                cm = fmax(cm, -(dd_ * dd_) / eps + sa * (double)xa);
+            }
+            C.c[a][ya] = cm;
+            for (int xa = 0; xa < C.w[a]; ++xa) {
+                const double dd_ = coord(g.x_org, g.x_dx, a, C.xb.o[a] + xa) - yc;
+                tf[(int64_t)xa * C.n[a] + ya] = expf((float)(-(dd_ * dd_) / eps + sa * (double)xa - cm));
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Thread 0 compares the slopes of the current alpha with the ones the tables absorb;
+// the tables are rebuilt when one moved by more than kSlopeTol over the window (or after
+// a fallback).  Called by every thread after a barrier that published alpha.
+template <int T>
+__device__ void refresh_tables_f32(const Cell& C, const dd3_geom& g, Sh& sh) {
+    if (threadIdx.x == 0) {
+        double s[3];
+        slopes_now(C, g.eps, s);
+        int mv = sh.force;
+        for (int a = 0; a < 3; ++a)
+            if (fabs(s[a] - sh.slope[a]) * (double)(C.w[a] - 1) > kSlopeTol) mv = 1;
+        if (mv) for (int a = 0; a < 3; ++a) sh.slope[a] = s[a];
+        sh.rebuild = mv;
+        sh.force = 0;
+    }
+    __syncthreads();
+    if (sh.rebuild) build_tables_f32<T>(C, g, sh);
+}
+
+// fp32 contraction stage (cstage's indexing)
+template <int T>
+__device__ __forceinline__ void cstage32(const float* __restrict__ in, int A, int K, int B, int O,
+                                         const float* __restrict__ tab, int tk, int to,
+                                         float* __restrict__ out) {
+    const int n = A * O * B;
+    Step3<T> p(threadIdx.x, O, B);
+    for (int t = threadIdx.x; t < n; t += T, p.next()) {
+        const float* src = in + (p.i0 * K) * B + p.i2;
+        const float* tp = tab + p.i1 * to;
+        float S0 = 0.f, S1 = 0.f;
+        int k = 0;
+        for (; k + 1 < K; k += 2) {
+            S0 = fmaf(src[k * B], tp[k * tk], S0);
+            S1 = fmaf(src[(k + 1) * B], tp[(k + 1) * tk], S1);
+        }
+        if (k < K) S0 = fmaf(src[k * B], tp[k * tk], S0);
+        out[t] = S0 + S1;
+    }
+    __syncthreads();
+}
+
+template <int T>
+__device__ int sweep_x32(const Cell& C, const dd3_geom& g, Sh& sh) {
+    const double eps = g.eps, inv_eps = 1.0 / g.eps;
+    const int ny = (int)C.ny, nx = (int)C.nx;
+    const double sl0 = sh.slope[0], sl1 = sh.slope[1], sl2 = sh.slope[2];
+    double mx = kNegInf;
+    {
+        Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+        for (int y = threadIdx.x; y < ny; y += T, p.next()) {
+            const double bp = C.beta[y] * inv_eps + C.lnu[y] +
+                              (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]);
+            mx = fmax(mx, bp);
+        }
+    }
+    double M = bmax<T>(mx, sh.red);
+    if (!isfinite(M)) M = 0.0;
+    float* zf = f32p(C.z);
+    float* s1f = f32p(C.s1);
+    float* s2f = f32p(C.s2);
+    {
+        Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+        for (int y = threadIdx.x; y < ny; y += T, p.next()) {
+            const double bp = C.beta[y] * inv_eps + C.lnu[y] +
+                              (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]);
+            zf[y] = expf((float)(bp - M));
+        }
+    }
+    if (threadIdx.x == 0) sh.flag = 0;
+    __syncthreads();
+    cstage32<T>(zf, C.n[0] * C.n[1], C.n[2], 1, C.w[2], f32p(C.kn[2]), 1, C.n[2], s1f);
+    cstage32<T>(s1f, C.n[0], C.n[1], C.w[2], C.w[1], f32p(C.kn[1]), 1, C.n[1], s2f);
+    int bad = 0;
+    {
+        const int ob = C.w[1] * C.w[2];
+        const int n0 = C.n[0];
+        const float* k0 = f32p(C.kn[0]);
+        for (int t = threadIdx.x; t < nx; t += T) {
+            int x0, x1, x2;
+            unflat(t, C.w[1], C.w[2], x0, x1, x2);
+            const float* s2 = s2f + (x1 * C.w[2] + x2);
+            const float* kt = k0 + x0 * n0;
+            float S0 = 0.f, S1 = 0.f;
+            int k = 0;
+            for (; k + 1 < n0; k += 2) {
+                S0 = fmaf(s2[k * ob], kt[k], S0);
+                S1 = fmaf(s2[(k + 1) * ob], kt[k + 1], S1);
+            }
+            if (k < n0) S0 = fmaf(s2[k * ob], kt[k], S0);
+            const float S = S0 + S1;
+            if (!(S >= kTinyF)) bad = 1;
+            C.L[t] = (double)logf(S) + M - (sl0 * (double)x0 + sl1 * (double)x1 + sl2 * (double)x2);
+        }
+    }
+    if (bad) sh.flag = 1;
+    __syncthreads();
+    if (!sh.flag) return 0;
+    // exact stage-wise path on b = beta/eps + lnu (fp64); slopes refreshed afterwards
+    for (int y = threadIdx.x; y < ny; y += T) C.z[y] = C.beta[y] / eps + C.lnu[y];
+    if (threadIdx.x == 0) sh.force = 1;
+    __syncthreads();
+    const int* xo = C.xb.o;
+    const int* yo = C.yb.o;
+    xstage<T>(C.z, C.n[0] * C.n[1], C.n[2], 1, C.w[2], g.x_org[2], g.x_dx, xo[2], g.y_org[2],
+           g.y_dx, yo[2], eps, C.s1);
+    xstage<T>(C.s1, C.n[0], C.n[1], C.w[2], C.w[1], g.x_org[1], g.x_dx, xo[1], g.y_org[1], g.y_dx,
+           yo[1], eps, C.s2);
+    xstage<T>(C.s2, 1, C.n[0], C.w[1] * C.w[2], C.w[0], g.x_org[0], g.x_dx, xo[0], g.y_org[0],
+           g.y_dx, yo[0], eps, C.L);
+    return 1;
+}
+
+template <int T>
+__device__ int sweep_y32(const Cell& C, const dd3_geom& g, Sh& sh) {
+    const double eps = g.eps, inv_eps = 1.0 / g.eps;
+    const int ny = (int)C.ny, nx = (int)C.nx;
+    const double sl0 = sh.slope[0], sl1 = sh.slope[1], sl2 = sh.slope[2];
+    double mx = kNegInf;
+    for (int x = threadIdx.x; x < nx; x += T) {
+        int x0, x1, x2;
+        unflat(x, C.w[1], C.w[2], x0, x1, x2);
+        const double a = C.alpha[x] * inv_eps + C.lmu[x];
+        C.av[x] = a;
+        mx = fmax(mx, a - (sl0 * (double)x0 + sl1 * (double)x1 + sl2 * (double)x2));
+    }
+    double M = bmax<T>(mx, sh.red);
+    if (!isfinite(M)) M = 0.0;
+    float* lf = f32p(C.L);
+    float* s1f = f32p(C.s1);
+    float* s2f = f32p(C.s2);
+    for (int x = threadIdx.x; x < nx; x += T) {
+        int x0, x1, x2;
+        unflat(x, C.w[1], C.w[2], x0, x1, x2);
+        lf[x] = expf((float)(C.av[x] - (sl0 * (double)x0 + sl1 * (double)x1 + sl2 * (double)x2) - M));
+    }
+    if (threadIdx.x == 0) sh.flag = 0;
+    __syncthreads();
+    cstage32<T>(lf, C.w[0] * C.w[1], C.w[2], 1, C.n[2], f32p(C.kn[2]), C.n[2], 1, s1f);
+    cstage32<T>(s1f, C.w[0], C.w[1], C.n[2], C.n[1], f32p(C.kn[1]), C.n[1], 1, s2f);
+    int bad = 0;
+    {
+        const int ob = C.n[1] * C.n[2];
+        const int n0 = C.n[0], w0 = C.w[0];
+        const float* k0 = f32p(C.kn[0]);
+        Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+        for (int t = threadIdx.x; t < ny; t += T, p.next()) {
+            const float* s2 = s2f + (p.i1 * C.n[2] + p.i2);
+            const float* kt = k0 + p.i0;
+            float S0 = 0.f, S1 = 0.f;
+            int k = 0;
+            for (; k + 1 < w0; k += 2) {
+                S0 = fmaf(s2[k * ob], kt[k * n0], S0);
+                S1 = fmaf(s2[(k + 1) * ob], kt[(k + 1) * n0], S1);
+            }
+            if (k < w0) S0 = fmaf(s2[k * ob], kt[k * n0], S0);
+            const float S = S0 + S1;
+            if (!(S >= kTinyF)) bad = 1;
+            C.z[t] = (double)logf(S) + M + (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]);
+        }
+    }
+    if (bad) sh.flag = 1;
+    __syncthreads();
+    if (!sh.flag) return 0;
+    if (threadIdx.x == 0) sh.force = 1;
+    const int* xo = C.xb.o;
+    const int* yo = C.yb.o;
+    xstage<T>(C.av, C.w[0] * C.w[1], C.w[2], 1, C.n[2], g.y_org[2], g.y_dx, yo[2], g.x_org[2],
+           g.x_dx, xo[2], eps, C.s1);
+    xstage<T>(C.s1, C.w[0], C.w[1], C.n[2], C.n[1], g.y_org[1], g.y_dx, yo[1], g.x_org[1], g.x_dx,
+           xo[1], eps, C.s2);
+    xstage<T>(C.s2, 1, C.w[0], C.n[1] * C.n[2], C.n[0], g.y_org[0], g.y_dx, yo[0], g.x_org[0],
+           g.x_dx, xo[0], eps, C.z);
+    return 1;
+}
+
 // cost and -cost/eps of window nodes x (X window index) and y (Y window index)
 __device__ __forceinline__ double cell_cost(const Cell& C, const dd3_geom& g, int x0, int x1,
                                             int x2, int y0, int y1, int y2) {
@@ -539,7 +775,7 @@ __device__ __forceinline__ void member_block(const dd3_state& s, const Cell& C, 
 #ifndef DD3_MIN_BLOCKS
 #define DD3_MIN_BLOCKS 2   // resident cell CTAs per SM (2: <= 128 registers, no spills)
 #endif
-template <int T>
+template <int T, int F32>
 __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     cell_solve3_kernel(dd3_geom g, dd3_state s, dd3_batch b) {
     __shared__ Sh sh;
@@ -648,7 +884,7 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     }
     // per-axis Y-normalised tables Kn_a[x_a][y_a] = exp(-(d^2)/eps - c_a(y_a)),
     // c_a(y_a) = max over x_a of -(d^2)/eps
-    for (int a = 0; a < 3; ++a) {
+    if (!F32) for (int a = 0; a < 3; ++a) {
         for (int ya = threadIdx.x; ya < C.n[a]; ya += T) {
             const double yc = coord(g.y_org, g.y_dx, a, C.yb.o[a] + ya);
             double cm = kNegInf;
@@ -688,8 +924,13 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     int iters = 0, ndeg_max = 0, nfb = 0;
     long long nsteps = 0;        // Newton evaluations of this thread (diagnostic)
     const long long t_loop0 = clock64();
+    if (F32) {
+        // fp32 mode: tables absorb the slopes of the warm alpha (barrier above published it)
+        if (threadIdx.x == 0) sh.force = 1;
+        refresh_tables_f32<T>(C, g, sh);
+    }
     for (int k = 1; k <= b.max_iters; ++k) {
-        nfb += sweep_x<T>(C, g, sh);
+        nfb += F32 ? sweep_x32<T>(C, g, sh) : sweep_x<T>(C, g, sh);
         if (k >= 2) {
             const double gg = lam * gap_sum<T>(C, g, sh);
             if (!have_first) { first_g = gg; have_first = true; }
@@ -697,14 +938,16 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
         }
         for (int64_t x = threadIdx.x; x < C.nx; x += T) C.alpha[x] = -ratio * C.L[x];
         __syncthreads();
-        nfb += sweep_y<T>(C, g, sh);
+        if (F32) refresh_tables_f32<T>(C, g, sh);
+        nfb += F32 ? sweep_y32<T>(C, g, sh) : sweep_y<T>(C, g, sh);
         if (threadIdx.x == 0) sh.ndeg = 0;
         __syncthreads();
         int nd = 0;
         for (int64_t y = threadIdx.x; y < C.ny; y += T) {
             int deg = 0;
             C.beta[y] = dd::newton_node(C.z[y], C.m[y], true, C.beta[y], eps, lam, b.newton_tol,
-                                        b.newton_max_iters, &deg, &nsteps, nullptr, C.lm[y]);
+                                        b.newton_max_iters, &deg, &nsteps, nullptr, C.lm[y],
+                                        F32 != 0);
             nd += deg;
         }
         if (nd) atomicAdd(&sh.ndeg, nd);
@@ -713,7 +956,7 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
         iters = k;
     }
     if (!conv) {
-        nfb += sweep_x<T>(C, g, sh);
+        nfb += F32 ? sweep_x32<T>(C, g, sh) : sweep_x<T>(C, g, sh);
         const double gg = lam * gap_sum<T>(C, g, sh);
         gap = gg;
         if (!have_first) first_g = gg;
@@ -2275,8 +2518,11 @@ extern "C" int dd3_cell_solve(const dd3_geom* g, const dd3_state* s, const dd3_b
     if (b->n_cells <= 0) return 0;
     // dynamic shared memory for the hot per-cell arrays (the kernel falls back to the
     // global workspace for a cell whose arrays do not fit)
+    if (b->precision != 0 && b->precision != 1) return dd_set_error(cudaErrorInvalidValue);
+    auto kern = b->precision ? v3::cell_solve3_kernel<v3::CELL_NT, 1>
+                             : v3::cell_solve3_kernel<v3::CELL_NT, 0>;
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, v3::cell_solve3_kernel<v3::CELL_NT>);
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return dd_set_error(e);
     const int64_t cap = 227 * 1024 - (int64_t)fa.sharedSizeBytes - 1024;
     int64_t bytes = (int64_t)b->smem_doubles * (int64_t)sizeof(double);
@@ -2284,11 +2530,9 @@ extern "C" int dd3_cell_solve(const dd3_geom* g, const dd3_state* s, const dd3_b
     if (bytes < 0) bytes = 0;
     dd3_batch bb = *b;
     bb.smem_doubles = (int32_t)(bytes / (int64_t)sizeof(double));
-    e = cudaFuncSetAttribute(v3::cell_solve3_kernel<v3::CELL_NT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return dd_set_error(e);
-    v3::cell_solve3_kernel<v3::CELL_NT>
-        <<<b->n_cells, v3::CELL_NT, (size_t)bytes, (cudaStream_t)stream>>>(*g, *s, bb);
+    kern<<<b->n_cells, v3::CELL_NT, (size_t)bytes, (cudaStream_t)stream>>>(*g, *s, bb);
     return dd_set_error(cudaGetLastError());
 }
 

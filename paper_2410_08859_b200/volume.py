@@ -714,7 +714,8 @@ class _Batch3:
             cstat=self.cstat.data_ptr(), cstat2=self.cstat2.data_ptr(), delta=cfg.delta,
             max_iters=cfg.max_iters, newton_max_iters=cfg.newton_max_iters,
             newton_tol=cfg.newton_tol, trunc=cfg.trunc_threshold,
-            smem_doubles=int(_hot_doubles(pt.nxw, ne[0], ne[1], ne[2]).max(initial=0)))
+            smem_doubles=int(_hot_doubles(pt.nxw, ne[0], ne[1], ne[2]).max(initial=0)),
+            precision=1 if getattr(cfg, "precision", "fp64") == "fp32" else 0)
         for a in range(3):
             self.batch.nxw[a] = pt.nxw[a]
         self.tot_y = tot_y
