@@ -207,16 +207,29 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
         // (t > 0: exp(-t), w + log1p(e), 1/(1+e); t <= 0: exp(t), lm + log1p(e), e/(1+e)).
         const double t = w - lm;
         const bool pos = t > 0;
-        const double e = exp(pos ? -t : t);
-        const double l1 = log1p(e);
+        double e, l1, sig;
+        if (relaxed) {
+            // fp32 mode: the transcendental part log1p(exp(-|t|)) in [0, ln 2] and the
+            // slope factor in fp32; w, lm, the sum g and the iterate stay fp64.  The
+            // error of l1 is relative (~1e-7 (1 + |t|)), and l1 / sig ~ 1 + e, so the
+            // root moves by ~1e-7 (1 + |t|) in beta/eps: inside the 1e-4 bar.  sig only
+            // sets the Newton slope (convergence rate, not the root).
+            const float ef = expf((float)(pos ? -t : t));
+            e = (double)ef;
+            l1 = (double)log1pf(ef);
+            sig = (double)((pos ? 1.0f : ef) * __frcp_rn(1.0f + ef));
+        } else {
+            e = exp(pos ? -t : t);
+            l1 = log1p(e);
+            sig = (pos ? 1.0 : e) / (1.0 + e);
+        }
         double la = (pos ? w : lm) + l1;
         if (t == 0) la = w + 0.693147180559945309417232121458176568;
-        double sig = (pos ? 1.0 : e) / (1.0 + e);
         if (t != t) { la = t; sig = t; }
         const double g = la + b * inv_lam;
         if (g == 0.0) break;   // step 0: inactive (avoids the division's slow path)
         const double gp = sig * inv_eps + inv_lam;
-        const double step = g / gp;
+        const double step = relaxed ? g * (double)__frcp_rn((float)gp) : g / gp;
         const bool active = (fabs(g) > tol) || (fabs(step) > 4e-16 * (1.0 + fabs(b)));
         if (!active) break;
         double nb = b - step;
