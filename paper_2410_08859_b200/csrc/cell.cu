@@ -1635,45 +1635,26 @@ __global__ void __launch_bounds__(DD_NT, (kLoop ? 2 : (kPass == 0 ? DD_CELL_MIN_
                 w.ty[y] = cs;
             }
             __syncthreads();
-            if (tid == 0) {
+            {
+                // every thread follows the same control flow from the shared surplus
+                // table; each _move_mass (cells.py:488-507) runs across the block
+                __shared__ double stage_sh[256], pub_sh[4];
                 int di = 0, ri = 0;
                 while (di < nd && ri < nr) {
                     const int dk = donors[di], rk = recips[ri];
                     const double amount = fmin(surplus[dk], -surplus[rk]);
-                    // _move_mass (cells.py:488-507)
-                    if (amount > 0) {
-                        double* row = VALS + (int64_t)dk * ny;
-                        double* rrow = VALS + (int64_t)rk * ny;
-                        double cum = 0.0;
-                        int kk = -1;
-                        double prev = 0.0;
-                        for (int y = 0; y < ny; ++y) {
-                            prev = cum;
-                            cum += row[y];
-                            if (cum >= amount) { kk = y; break; }
-                        }
-                        if (kk < 0) {
-                            // donor cannot cover: hand over everything
-                            if (ny > 0 && cum > 0) {
-                                for (int y = 0; y < ny; ++y) { rrow[y] += row[y]; row[y] = 0.0; }
-                            }
-                            fallbacks += 1;
-                        } else {
-                            for (int y = 0; y < kk; ++y) { rrow[y] += row[y]; row[y] = 0.0; }
-                            const double part = amount - (kk ? prev : 0.0);
-                            row[kk] -= part;
-                            rrow[kk] += part;
-                        }
-                    }
-                    surplus[dk] -= amount;
-                    surplus[rk] += amount;
-                    if (surplus[dk] <= tol[dk]) ++di;
-                    if (surplus[rk] >= -tol[rk]) ++ri;
+                    if (amount > 0)
+                        fallbacks += move_mass_block<DD_NT, 256>(VALS + (int64_t)dk * ny,
+                                                                 VALS + (int64_t)rk * ny, ny, amount,
+                                                                 stage_sh, pub_sh);
+                    const double sd = surplus[dk] - amount, sr = surplus[rk] + amount;
+                    __syncthreads();
+                    if (tid == 0) { surplus[dk] = sd; surplus[rk] = sr; }
+                    __syncthreads();
+                    if (sd <= tol[dk]) ++di;
+                    if (sr >= -tol[rk]) ++ri;
                 }
-                sh_flag[0] = fallbacks;
             }
-            __syncthreads();
-            fallbacks = sh_flag[0];
             for (int k = 0; k < nmem; ++k)
                 for (int y = tid; y < ny; y += DD_NT) {
                     double v = VALS[(int64_t)k * ny + y];

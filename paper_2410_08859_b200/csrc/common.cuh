@@ -286,6 +286,63 @@ __device__ __forceinline__ double newton_node(double z, double m, bool has_m, do
 }
 
 
+
+// _move_mass (cells.py:483-502) across a thread block, same arithmetic as the reference's
+// sequential walk: the donor row's running sum is accumulated by ONE thread in node
+// order (numpy cumsum's order; chunks of S nodes staged through shared memory by the
+// whole block, so the chain runs at the DADD latency instead of a global load per node),
+// the first node whose running sum reaches `amount` is published, and the element-wise
+// moves (rowr[y] += rowd[y]; rowd[y] = 0 below that node, the partial move on it) run
+// across the block.  Returns 1 when the donor cannot cover the amount (everything is
+// handed over: the reference's fallback).  Every thread of the block must call it;
+// stage holds S (<= T) doubles and pub 4 doubles of shared memory.
+template <int T, int S = T>
+__device__ int move_mass_block(double* rowd, double* rowr, int64_t ny, double amount,
+                               double* stage, double* pub) {
+    static_assert(S <= T, "one staged node per thread");
+    double cum = 0.0;   // thread 0 only
+    if (threadIdx.x == 0) { pub[0] = -1.0; pub[1] = 0.0; pub[2] = 0.0; }
+    __syncthreads();
+    for (int64_t base = 0; base < ny; base += S) {
+        const int64_t y = base + threadIdx.x;
+        if (threadIdx.x < S) stage[threadIdx.x] = y < ny ? rowd[y] : 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int n = (int)((ny - base) < (int64_t)S ? (ny - base) : (int64_t)S);
+            for (int j = 0; j < n; ++j) {
+                const double prev = cum;
+                cum += stage[j];
+                if (cum >= amount) {
+                    pub[0] = (double)(base + j);
+                    pub[1] = prev;
+                    break;
+                }
+            }
+            pub[2] = cum;
+        }
+        __syncthreads();
+        if (pub[0] >= 0.0) break;
+    }
+    const int64_t kk = (int64_t)pub[0];
+    const double prev = pub[1], total = pub[2];
+    int fb = 0;
+    if (kk < 0) {
+        if (ny > 0 && total > 0) {
+            for (int64_t y = threadIdx.x; y < ny; y += T) { rowr[y] += rowd[y]; rowd[y] = 0.0; }
+        }
+        fb = 1;
+    } else {
+        for (int64_t y = threadIdx.x; y < kk; y += T) { rowr[y] += rowd[y]; rowd[y] = 0.0; }
+        if (threadIdx.x == 0) {
+            const double part = amount - (kk ? prev : 0.0);
+            rowd[kk] -= part;
+            rowr[kk] += part;
+        }
+    }
+    __syncthreads();
+    return fb;
+}
+
 }  // namespace dd
 
 // Deterministic boxed gather-sum (grid.cu): out = base + sum_i scale_i * v_i over

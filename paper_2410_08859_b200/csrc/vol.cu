@@ -1003,6 +1003,7 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     // ---- balancing (cells.py:446-480): member reference masses and targets
     __shared__ double s_mbar[64], s_mass[64], s_tgt[64], s_sur[64];
     __shared__ int s_fb, s_moved;
+    __shared__ double stage_sh[T], pub_sh[4];
     for (int k = 0; k < n_mem; ++k) {
         const int* lo = mlo + 3 * k;
         const int* be = mbe + 3 * k;
@@ -1044,7 +1045,9 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
             C.z[y] = cs;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        {
+            // donor / recipient walk (cells.py:446-480): every thread follows the same
+            // control flow from the shared surplus table; each move runs across the block
             int donors[64], recips[64];
             int nd = 0, nr = 0;
             for (int k = 0; k < n_mem; ++k) {
@@ -1056,35 +1059,17 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
             while (di < nd && ri < nr) {
                 const int dk = donors[di], rk = recips[ri];
                 const double amount = fmin(s_sur[dk], -s_sur[rk]);
-                // _move_mass (cells.py:483-502)
-                if (amount > 0) {
-                    double* rowd = V + (int64_t)dk * C.ny;
-                    double* rowr = V + (int64_t)rk * C.ny;
-                    double cum = 0.0, prev = 0.0;
-                    int64_t kk = -1;
-                    for (int64_t y = 0; y < C.ny; ++y) {
-                        prev = cum;
-                        cum += rowd[y];
-                        if (cum >= amount) { kk = y; break; }
-                    }
-                    if (kk < 0) {
-                        if (C.ny && cum > 0) {
-                            for (int64_t y = 0; y < C.ny; ++y) { rowr[y] += rowd[y]; rowd[y] = 0.0; }
-                        }
-                        ++fb;
-                    } else {
-                        for (int64_t y = 0; y < kk; ++y) { rowr[y] += rowd[y]; rowd[y] = 0.0; }
-                        const double part = amount - (kk ? prev : 0.0);
-                        rowd[kk] -= part;
-                        rowr[kk] += part;
-                    }
-                }
-                s_sur[dk] -= amount;
-                s_sur[rk] += amount;
-                if (s_sur[dk] <= 1e-13 * fmax(s_tgt[dk], 1e-300)) ++di;
-                if (s_sur[rk] >= -1e-13 * fmax(s_tgt[rk], 1e-300)) ++ri;
+                if (amount > 0)
+                    fb += dd::move_mass_block<T>(V + (int64_t)dk * C.ny, V + (int64_t)rk * C.ny,
+                                                 C.ny, amount, stage_sh, pub_sh);
+                const double sd = s_sur[dk] - amount, sr = s_sur[rk] + amount;
+                __syncthreads();
+                if (threadIdx.x == 0) { s_sur[dk] = sd; s_sur[rk] = sr; }
+                __syncthreads();
+                if (sd <= 1e-13 * fmax(s_tgt[dk], 1e-300)) ++di;
+                if (sr >= -1e-13 * fmax(s_tgt[rk], 1e-300)) ++ri;
             }
-            s_fb = fb;
+            if (threadIdx.x == 0) s_fb = fb;
         }
         __syncthreads();
         // clip, then restore every column's sum bitwise (cells.py:505-545)
