@@ -760,6 +760,51 @@ __device__ __forceinline__ double cell_cost(const Cell& C, const dd3_geom& g, in
     return d0 * d0 + d1 * d1 + d2 * d2;
 }
 
+// Y-normalised fp64 tables Kn_a[x_a][y_a] = exp(-(d^2)/eps - c_a(y_a)), c_a = max over x_a
+template <int T>
+__device__ void build_tables_f64(const Cell& C, const dd3_geom& g) {
+    const double eps = g.eps;
+    for (int a = 0; a < 3; ++a) {
+        for (int ya = threadIdx.x; ya < C.n[a]; ya += T) {
+            const double yc = coord(g.y_org, g.y_dx, a, C.yb.o[a] + ya);
+            double cm = kNegInf;
+            for (int xa = 0; xa < C.w[a]; ++xa) {
+                const double dd_ = coord(g.x_org, g.x_dx, a, C.xb.o[a] + xa) - yc;
+                cm = fmax(cm, -(dd_ * dd_) / eps);
+            }
+            C.c[a][ya] = cm;
+            for (int xa = 0; xa < C.w[a]; ++xa) {
+                const double dd_ = coord(g.x_org, g.x_dx, a, C.xb.o[a] + xa) - yc;
+                C.kn[a][(int64_t)xa * C.n[a] + ya] = exp(-(dd_ * dd_) / eps - cm);
+            }
+        }
+    }
+}
+
+// cstage with the squared axis distance folded in (x -> y direction, tab[k*tk + o]):
+//   out[(a*O+o)*B+b] (+)= sum_k in[(a*K+k)*B+b] * d(k,o)^2 * tab[k*tk + o],
+// d(k,o) = x coordinate of window node xi0 + k minus y coordinate of window node o.
+template <int T>
+__device__ __forceinline__ void cstage_sq(const double* __restrict__ in, int A, int K, int B, int O,
+                                          const double* __restrict__ tab, int tk, const Cell& C,
+                                          const dd3_geom& g, int axis, int xi0, bool accumulate,
+                                          double* __restrict__ out) {
+    const int n = A * O * B;
+    Step3<T> p(threadIdx.x, O, B);
+    for (int t = threadIdx.x; t < n; t += T, p.next()) {
+        const double* src = in + (p.i0 * K) * B + p.i2;
+        const double* tp = tab + p.i1;
+        const double yc = coord(g.y_org, g.y_dx, axis, C.yb.o[axis] + p.i1);
+        double S = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const double d = coord(g.x_org, g.x_dx, axis, C.xb.o[axis] + xi0 + k) - yc;
+            S = fma(src[k * B] * (d * d), tp[k * tk], S);
+        }
+        out[t] = accumulate ? out[t] + S : S;
+    }
+    __syncthreads();
+}
+
 // ---- the cell solve kernel -----------------------------------------------------------
 
 __device__ __forceinline__ void member_block(const dd3_state& s, const Cell& C, int i, int* lo,
@@ -884,21 +929,7 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     }
     // per-axis Y-normalised tables Kn_a[x_a][y_a] = exp(-(d^2)/eps - c_a(y_a)),
     // c_a(y_a) = max over x_a of -(d^2)/eps
-    if (!F32) for (int a = 0; a < 3; ++a) {
-        for (int ya = threadIdx.x; ya < C.n[a]; ya += T) {
-            const double yc = coord(g.y_org, g.y_dx, a, C.yb.o[a] + ya);
-            double cm = kNegInf;
-            for (int xa = 0; xa < C.w[a]; ++xa) {
-                const double dd_ = coord(g.x_org, g.x_dx, a, C.xb.o[a] + xa) - yc;
-                cm = fmax(cm, -(dd_ * dd_) / eps);
-            }
-            C.c[a][ya] = cm;
-            for (int xa = 0; xa < C.w[a]; ++xa) {
-                const double dd_ = coord(g.x_org, g.x_dx, a, C.xb.o[a] + xa) - yc;
-                C.kn[a][(int64_t)xa * C.n[a] + ya] = exp(-(dd_ * dd_) / eps - cm);
-            }
-        }
-    }
+    if (!F32) build_tables_f64<T>(C, g);
     const int nclamped = (int)bsum<T>((double)nclamp, sh.red);   // (barrier)
     if (!(mass > 0)) {
         // zero-mass cell: untouched, converged (cells.py:245-264)
@@ -969,37 +1000,186 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
     for (int64_t x = threadIdx.x; x < C.nx; x += T)
         C.av[x] = exp(-(-ratio * C.L[x]) / lam) * C.mu[x];
     __syncthreads();
-    for (int64_t y = threadIdx.x; y < C.ny; y += T) {
+    // Exact per-term split of member k at Y node y (the reference's dense evaluation)
+    auto split_exact = [&](int k, int64_t y) {
         int y0, y1, y2;
         unflat(y, C.n[1], C.n[2], y0, y1, y2);
         const double bt = C.beta[y] / eps;
         const double ln = C.lnu[y];
+        const int* lo = mlo + 3 * k;
+        const int* be = mbe + 3 * k;
+        double sp = 0.0, stc = 0.0, stl = 0.0, smc = 0.0;
+        for (int t0 = 0; t0 < be[0]; ++t0)
+            for (int t1 = 0; t1 < be[1]; ++t1)
+                for (int t2 = 0; t2 < be[2]; ++t2) {
+                    const int x0 = lo[0] + t0, x1 = lo[1] + t1, x2 = lo[2] + t2;
+                    const int64_t x = ((int64_t)x0 * C.w[1] + x1) * C.w[2] + x2;
+                    const double cost = cell_cost(C, g, x0, x1, x2, y0, y1, y2);
+                    const double sc = C.alpha[x] / eps + bt + (-cost / eps);
+                    const double p = exp(sc + C.lmu[x] + ln);
+                    sp += p;
+                    stc += p * cost;
+                    stl += p * sc;
+                    smc += cost * C.mu[x];
+                }
+        const int64_t q = (int64_t)k * C.ny + y;
+        R[q] = sp;
+        V[q] = sp;
+        TC[q] = stc;
+        TL[q] = stl;
+        MC[q] = smc;
+    };
+    // Separable split: per member k the sums over its block x of p = exp(a[x] + b[y] -
+    // c(x,y)/eps) (a = alpha/eps + log mu, b = beta/eps + log nu), of p cost and of
+    // p alpha/eps are three-stage contractions of the block weights u = exp(a - max a)
+    // against the Y-normalised tables (one table carrying d_a^2 for the cost sums);
+    // sum p sc follows from sc = alpha/eps + beta/eps - cost/eps.  A node whose shifted
+    // sum is below kTiny may have lost terms to underflow and is redone per term.
+    // Scratch: block weights and stage-1 outputs in s1, stage-2 outputs in s2.
+    bool sep = true;
+    {
+        const int64_t s1cap = l.s2 - l.s1, s2cap = l.total - 1 - l.s2;
+        for (int k = 0; k < n_mem; ++k) {
+            const int* be = mbe + 3 * k;
+            const int nbk = be[0] * be[1] * be[2];
+            if (2 * (int64_t)nbk + 3 * (int64_t)be[0] * be[1] * C.n[2] > s1cap) sep = false;
+            if ((int64_t)be[0] * C.n[1] * C.n[2] > s2cap) sep = false;
+            if (be[0] > 16 || be[1] > 16 || be[2] > 16) sep = false;
+        }
+    }
+    if (!sep) {
+        for (int64_t y = threadIdx.x; y < C.ny; y += T)
+            for (int k = 0; k < n_mem; ++k) split_exact(k, y);
+        __syncthreads();
+    } else {
+        if (F32) { build_tables_f64<T>(C, g); __syncthreads(); }
+        __shared__ double s_ma[3][16];
         for (int k = 0; k < n_mem; ++k) {
             const int* lo = mlo + 3 * k;
             const int* be = mbe + 3 * k;
-            double sp = 0.0, stc = 0.0, stl = 0.0, smc = 0.0;
-            for (int t0 = 0; t0 < be[0]; ++t0)
-                for (int t1 = 0; t1 < be[1]; ++t1)
-                    for (int t2 = 0; t2 < be[2]; ++t2) {
-                        const int x0 = lo[0] + t0, x1 = lo[1] + t1, x2 = lo[2] + t2;
-                        const int64_t x = ((int64_t)x0 * C.w[1] + x1) * C.w[2] + x2;
-                        const double cost = cell_cost(C, g, x0, x1, x2, y0, y1, y2);
-                        const double sc = C.alpha[x] / eps + bt + (-cost / eps);
-                        const double p = exp(sc + C.lmu[x] + ln);
-                        sp += p;
-                        stc += p * cost;
-                        stl += p * sc;
-                        smc += cost * C.mu[x];
+            const int nbk = be[0] * be[1] * be[2];
+            double* U = C.s1;
+            double* UA = U + nbk;
+            double* T1 = UA + nbk;
+            double* T1a = T1 + be[0] * be[1] * C.n[2];
+            double* T1c = T1a + be[0] * be[1] * C.n[2];
+            double* T2 = C.s2;
+            // block weights, shifted by the block's own maximum; mu marginals per axis
+            double amx = kNegInf;
+            for (int t = threadIdx.x; t < nbk; t += T) {
+                int t0, t1, t2;
+                unflat(t, be[1], be[2], t0, t1, t2);
+                const int64_t x = ((int64_t)(lo[0] + t0) * C.w[1] + lo[1] + t1) * C.w[2] + lo[2] + t2;
+                amx = fmax(amx, C.alpha[x] / eps + C.lmu[x]);
+            }
+            double Ak = bmax<T>(amx, sh.red);
+            if (!isfinite(Ak)) Ak = 0.0;
+            if (threadIdx.x < 48) s_ma[threadIdx.x / 16][threadIdx.x % 16] = 0.0;
+            __syncthreads();
+            for (int t = threadIdx.x; t < nbk; t += T) {
+                int t0, t1, t2;
+                unflat(t, be[1], be[2], t0, t1, t2);
+                const int64_t x = ((int64_t)(lo[0] + t0) * C.w[1] + lo[1] + t1) * C.w[2] + lo[2] + t2;
+                const double ae = C.alpha[x] / eps;
+                const double u = exp(ae + C.lmu[x] - Ak);
+                U[t] = u;
+                UA[t] = u * ae;
+            }
+            if (threadIdx.x < be[0] + be[1] + be[2]) {
+                // marginals of mu over the other two block axes (sequential, fixed order)
+                const int a = threadIdx.x < be[0] ? 0 : (threadIdx.x < be[0] + be[1] ? 1 : 2);
+                const int i = threadIdx.x - (a == 0 ? 0 : (a == 1 ? be[0] : be[0] + be[1]));
+                double m = 0.0;
+                for (int t0 = 0; t0 < be[0]; ++t0)
+                    for (int t1 = 0; t1 < be[1]; ++t1)
+                        for (int t2 = 0; t2 < be[2]; ++t2) {
+                            if ((a == 0 ? t0 : (a == 1 ? t1 : t2)) != i) continue;
+                            m += C.mu[((int64_t)(lo[0] + t0) * C.w[1] + lo[1] + t1) * C.w[2] + lo[2] + t2];
+                        }
+                s_ma[a][i] = m;
+            }
+            __syncthreads();
+            // stage 1 (x2 -> y2): plain weights, alpha-weighted, d2^2-weighted
+            const double* k2 = C.kn[2] + (int64_t)lo[2] * C.n[2];
+            const double* k1 = C.kn[1] + (int64_t)lo[1] * C.n[1];
+            const double* k0 = C.kn[0] + (int64_t)lo[0] * C.n[0];
+            cstage<T>(U, be[0] * be[1], be[2], 1, C.n[2], k2, C.n[2], 1, T1);
+            cstage<T>(UA, be[0] * be[1], be[2], 1, C.n[2], k2, C.n[2], 1, T1a);
+            cstage_sq<T>(U, be[0] * be[1], be[2], 1, C.n[2], k2, C.n[2], C, g, 2, lo[2], false, T1c);
+            const int ob = C.n[1] * C.n[2];
+            const int n0 = C.n[0];
+            // pass A: S = sum p-weights, cost part along axis 0
+            cstage<T>(T1, be[0], be[1], C.n[2], C.n[1], k1, C.n[1], 1, T2);
+            {
+                Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+                for (int t = threadIdx.x; t < (int)C.ny; t += T, p.next()) {
+                    const double* s2 = T2 + (p.i1 * C.n[2] + p.i2);
+                    const double yc = coord(g.y_org, g.y_dx, 0, C.yb.o[0] + p.i0);
+                    double S = 0.0, Cc = 0.0;
+                    for (int q = 0; q < be[0]; ++q) {
+                        const double kv = k0[(int64_t)q * n0 + p.i0];
+                        const double d = coord(g.x_org, g.x_dx, 0, C.xb.o[0] + lo[0] + q) - yc;
+                        S = fma(s2[q * ob], kv, S);
+                        Cc = fma(s2[q * ob] * (d * d), kv, Cc);
                     }
-            const int64_t q = (int64_t)k * C.ny + y;
-            R[q] = sp;
-            V[q] = sp;
-            TC[q] = stc;
-            TL[q] = stl;
-            MC[q] = smc;
+                    R[(int64_t)k * C.ny + t] = S;
+                    TC[(int64_t)k * C.ny + t] = Cc;
+                }
+            }
+            __syncthreads();
+            // pass B: alpha-weighted sum
+            cstage<T>(T1a, be[0], be[1], C.n[2], C.n[1], k1, C.n[1], 1, T2);
+            {
+                Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+                for (int t = threadIdx.x; t < (int)C.ny; t += T, p.next()) {
+                    const double* s2 = T2 + (p.i1 * C.n[2] + p.i2);
+                    double Sa = 0.0;
+                    for (int q = 0; q < be[0]; ++q) Sa = fma(s2[q * ob], k0[(int64_t)q * n0 + p.i0], Sa);
+                    TL[(int64_t)k * C.ny + t] = Sa;
+                }
+            }
+            __syncthreads();
+            // pass C: cost parts along axes 2 and 1, then the per-node results
+            cstage<T>(T1c, be[0], be[1], C.n[2], C.n[1], k1, C.n[1], 1, T2);
+            cstage_sq<T>(T1, be[0], be[1], C.n[2], C.n[1], k1, C.n[1], C, g, 1, lo[1], true, T2);
+            {
+                Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+                for (int t = threadIdx.x; t < (int)C.ny; t += T, p.next()) {
+                    const double* s2 = T2 + (p.i1 * C.n[2] + p.i2);
+                    double Cc = 0.0;
+                    for (int q = 0; q < be[0]; ++q) Cc = fma(s2[q * ob], k0[(int64_t)q * n0 + p.i0], Cc);
+                    const int64_t q = (int64_t)k * C.ny + t;
+                    const double S = R[q];
+                    if (!(S >= kTiny)) {
+                        split_exact(k, t);
+                        continue;
+                    }
+                    const double bt = C.beta[t] / eps;
+                    const double lsp = bt + C.lnu[t] + (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]) +
+                                       Ak + log(S);
+                    const double sp = exp(lsp);
+                    const double mc = (TC[q] + Cc) / S;     // plan-weighted mean cost
+                    const double ma = TL[q] / S;            // plan-weighted mean alpha/eps
+                    R[q] = sp;
+                    V[q] = sp;
+                    TC[q] = sp * mc;
+                    TL[q] = sp * (ma + bt - mc / eps);
+                    // sum_x cost mu[x] = sum_a sum_i marg_a[i] d_a(i, y_a)^2
+                    double smc = 0.0;
+                    for (int a = 0; a < 3; ++a) {
+                        const int ya = a == 0 ? p.i0 : (a == 1 ? p.i1 : p.i2);
+                        const double yc = coord(g.y_org, g.y_dx, a, C.yb.o[a] + ya);
+                        for (int i = 0; i < be[a]; ++i) {
+                            const double d = coord(g.x_org, g.x_dx, a, C.xb.o[a] + lo[a] + i) - yc;
+                            smc = fma(s_ma[a][i], d * d, smc);
+                        }
+                    }
+                    MC[q] = smc;
+                }
+            }
+            __syncthreads();
         }
     }
-    __syncthreads();
     // ---- balancing (cells.py:446-480): member reference masses and targets
     __shared__ double s_mbar[64], s_mass[64], s_tgt[64], s_sur[64];
     __shared__ int s_fb, s_moved;
