@@ -1374,60 +1374,132 @@ __global__ void __launch_bounds__(T, T >= 512 ? 1 : DD3_MIN_BLOCKS)
         const int* lo = mlo + 3 * k;
         const int* be = mbe + 3 * k;
         const int nbk = be[0] * be[1] * be[2];
-        const int P = max(1, T / max(nbk, 1));
-        const int rowi = threadIdx.x / P, part = threadIdx.x - rowi * P;
-        double acc = 0.0;
-        int64_t xw = -1;
-        if (rowi < nbk) {
-            int t0, t1, t2;
-            unflat(rowi, be[1], be[2], t0, t1, t2);
-            const int x0 = lo[0] + t0, x1 = lo[1] + t1, x2 = lo[2] + t2;
-            xw = ((int64_t)x0 * C.w[1] + x1) * C.w[2] + x2;
-            if (C.mu[xw] > 0) {
-                const double av = C.alpha[xw] / eps;
-                for (int64_t y = part; y < C.ny; y += P) {
-                    const double f = Rk[y];
-                    if (f == 0.0) continue;
-                    int y0, y1, y2;
-                    unflat(y, C.n[1], C.n[2], y0, y1, y2);
-                    const double cost = cell_cost(C, g, x0, x1, x2, y0, y1, y2);
-                    const double sc = av + C.beta[y] / eps + (-cost / eps);
-                    acc += exp(sc + C.lmu[xw] + C.lnu[y]) * f;
+        __shared__ double part_sum[T];
+        bool xdone = false;
+        if (sep && nbk <= T) {
+            // separable form: weights v[y] = f[y] exp(b[y] + sum_a c_a(y_a) - B) (B their
+            // maximum shift) contracted along axis 2, 1, 0 against the Y-normalised tables
+            // restricted to the member's block; xm[x] = exp(a[x] + B + log S[x]).  A block
+            // node whose sum is below kTiny (or overflowed) sends the member to the
+            // per-term path below.
+            double bmx = kNegInf;
+            {
+                Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+                for (int y = threadIdx.x; y < (int)C.ny; y += T, p.next()) {
+                    if (Rk[y] > 0)
+                        bmx = fmax(bmx, C.beta[y] / eps + C.lnu[y] +
+                                            (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]));
                 }
             }
+            double Bk = bmax<T>(bmx, sh.red);
+            const bool anyf = isfinite(Bk);   // false: every f is 0, the member keeps nothing
+            if (!anyf) Bk = 0.0;
+            {
+                Step3<T> p(threadIdx.x, C.n[1], C.n[2]);
+                for (int y = threadIdx.x; y < (int)C.ny; y += T, p.next()) {
+                    const double f = Rk[y];
+                    C.z[y] = f > 0 ? f * exp(C.beta[y] / eps + C.lnu[y] +
+                                             (C.c[0][p.i0] + C.c[1][p.i1] + C.c[2][p.i2]) - Bk)
+                                   : 0.0;
+                }
+            }
+            if (threadIdx.x == 0) sh.flag = 0;
+            __syncthreads();
+            cstage<T>(C.z, C.n[0] * C.n[1], C.n[2], 1, be[2], C.kn[2] + (int64_t)lo[2] * C.n[2], 1,
+                      C.n[2], C.s1);
+            cstage<T>(C.s1, C.n[0], C.n[1], be[2], be[1], C.kn[1] + (int64_t)lo[1] * C.n[1], 1,
+                      C.n[1], C.s2);
+            {
+                const int obx = be[1] * be[2];
+                const int n0 = C.n[0];
+                int bad = 0;
+                for (int t = threadIdx.x; t < nbk; t += T) {
+                    int t0, t1, t2;
+                    unflat(t, be[1], be[2], t0, t1, t2);
+                    const int64_t xx = ((int64_t)(lo[0] + t0) * C.w[1] + lo[1] + t1) * C.w[2] + lo[2] + t2;
+                    const double* s2 = C.s2 + (t1 * be[2] + t2);
+                    const double* kt = C.kn[0] + (int64_t)(lo[0] + t0) * n0;
+                    double S = 0.0;
+                    for (int q = 0; q < n0; ++q) S = fma(s2[q * obx], kt[q], S);
+                    double xm = 0.0;
+                    if (C.mu[xx] > 0) {
+                        if (!anyf) xm = 0.0;
+                        else if (!(S >= kTiny) || !(S < kInf)) bad = 1;
+                        else xm = exp(C.alpha[xx] / eps + C.lmu[xx] + Bk + log(S));
+                    }
+                    part_sum[t] = xm;
+                }
+                if (bad) sh.flag = 1;
+            }
+            __syncthreads();
+            if (!sh.flag) {
+                for (int t = threadIdx.x; t < nbk; t += T) {
+                    int t0, t1, t2;
+                    unflat(t, be[1], be[2], t0, t1, t2);
+                    const int64_t xx = ((int64_t)(lo[0] + t0) * C.w[1] + lo[1] + t1) * C.w[2] + lo[2] + t2;
+                    double xm = part_sum[t];
+                    if (s_ext != 0.0) xm = xm + C.mu[xx] * (s_ext / mass_i);
+                    b.xarena[xoff + (int64_t)k * bs + t] = C.mu[xx] > 0 ? xm : 0.0;
+                }
+                xdone = true;
+            }
+            __syncthreads();
         }
-        // rows beyond T are handled below, one thread per row
-        __shared__ double part_sum[T];
-        __syncthreads();
-        part_sum[threadIdx.x] = acc;
-        __syncthreads();
-        if (part == 0 && rowi < nbk) {
-            double xm = 0.0;
-            for (int q = 0; q < P; ++q) xm += part_sum[threadIdx.x + q];
-            if (s_ext != 0.0) xm = xm + C.mu[xw] * (s_ext / mass_i);
-            b.xarena[xoff + (int64_t)k * bs + rowi] = C.mu[xw] > 0 ? xm : 0.0;
-        }
-        for (int rr = T; rr < nbk; rr += T) {   // blocks above T nodes: one thread per row
-            const int row = rr + threadIdx.x;
-            if (row < nbk) {
+        if (!xdone) {
+            const int P = max(1, T / max(nbk, 1));
+            const int rowi = threadIdx.x / P, part = threadIdx.x - rowi * P;
+            double acc = 0.0;
+            int64_t xw = -1;
+            if (rowi < nbk) {
                 int t0, t1, t2;
-                unflat(row, be[1], be[2], t0, t1, t2);
+                unflat(rowi, be[1], be[2], t0, t1, t2);
                 const int x0 = lo[0] + t0, x1 = lo[1] + t1, x2 = lo[2] + t2;
-                const int64_t xx = ((int64_t)x0 * C.w[1] + x1) * C.w[2] + x2;
-                double xm = 0.0;
-                if (C.mu[xx] > 0) {
-                    for (int64_t y = 0; y < C.ny; ++y) {
+                xw = ((int64_t)x0 * C.w[1] + x1) * C.w[2] + x2;
+                if (C.mu[xw] > 0) {
+                    const double av = C.alpha[xw] / eps;
+                    for (int64_t y = part; y < C.ny; y += P) {
                         const double f = Rk[y];
                         if (f == 0.0) continue;
                         int y0, y1, y2;
                         unflat(y, C.n[1], C.n[2], y0, y1, y2);
                         const double cost = cell_cost(C, g, x0, x1, x2, y0, y1, y2);
-                        const double sc = C.alpha[xx] / eps + C.beta[y] / eps + (-cost / eps);
-                        xm += exp(sc + C.lmu[xx] + C.lnu[y]) * f;
+                        const double sc = av + C.beta[y] / eps + (-cost / eps);
+                        acc += exp(sc + C.lmu[xw] + C.lnu[y]) * f;
                     }
-                    if (s_ext != 0.0) xm = xm + C.mu[xx] * (s_ext / mass_i);
                 }
-                b.xarena[xoff + (int64_t)k * bs + row] = xm;
+            }
+            // rows beyond T are handled below, one thread per row
+            __syncthreads();
+            part_sum[threadIdx.x] = acc;
+            __syncthreads();
+            if (part == 0 && rowi < nbk) {
+                double xm = 0.0;
+                for (int q = 0; q < P; ++q) xm += part_sum[threadIdx.x + q];
+                if (s_ext != 0.0) xm = xm + C.mu[xw] * (s_ext / mass_i);
+                b.xarena[xoff + (int64_t)k * bs + rowi] = C.mu[xw] > 0 ? xm : 0.0;
+            }
+            for (int rr = T; rr < nbk; rr += T) {   // blocks above T nodes: one thread per row
+                const int row = rr + threadIdx.x;
+                if (row < nbk) {
+                    int t0, t1, t2;
+                    unflat(row, be[1], be[2], t0, t1, t2);
+                    const int x0 = lo[0] + t0, x1 = lo[1] + t1, x2 = lo[2] + t2;
+                    const int64_t xx = ((int64_t)x0 * C.w[1] + x1) * C.w[2] + x2;
+                    double xm = 0.0;
+                    if (C.mu[xx] > 0) {
+                        for (int64_t y = 0; y < C.ny; ++y) {
+                            const double f = Rk[y];
+                            if (f == 0.0) continue;
+                            int y0, y1, y2;
+                            unflat(y, C.n[1], C.n[2], y0, y1, y2);
+                            const double cost = cell_cost(C, g, x0, x1, x2, y0, y1, y2);
+                            const double sc = C.alpha[xx] / eps + C.beta[y] / eps + (-cost / eps);
+                            xm += exp(sc + C.lmu[xx] + C.lnu[y]) * f;
+                        }
+                        if (s_ext != 0.0) xm = xm + C.mu[xx] * (s_ext / mass_i);
+                    }
+                    b.xarena[xoff + (int64_t)k * bs + row] = xm;
+                }
             }
         }
         __syncthreads();

@@ -9,3 +9,5 @@ timeout 900 python bench.py --impl reference --steps 2 > gpurun_out/final_bench_
 timeout 600 python bench.py --config vol_128 --cpu-sample 0 > gpurun_out/final_bench_vol128.log 2>&1
 timeout 600 python bench.py --config ms_256 --cpu-sample 0 > gpurun_out/final_bench_ms256.log 2>&1
 timeout 600 python bench.py --precision fp32 --cpu-sample 0 --steps 1 > gpurun_out/final_bench_fp32.log 2>&1
+timeout 600 python bench.py --config vol_128 --precision fp32 --cpu-sample 0 > gpurun_out/final_bench_vol128_fp32.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1
