@@ -191,9 +191,12 @@ def _peak():
         return FP64_NOMINAL_TFLOPS, "B200 datasheet FP64 (no measured FP64 peak committed)"
 
 
-def _ncu_profile():
+def _ncu_profile(nd=2, precision="fp64"):
+    """Committed ncu --set full summary of the dominant kernel of this path (2D / three-axis,
+    fp64 / fp32 mode): DRAM bytes per launch and pipe utilisation for roofline.traffic."""
+    name = "r02_ncu_cell_solve" + ("3" if nd == 3 else "") + ("_fp32" if precision == "fp32" else "")
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r02_ncu_cell_solve.json")))
+        return json.load(open(os.path.join(ROOT, "profiles", name + ".json")))
     except Exception:
         return None
 
@@ -331,7 +334,7 @@ def main():
     mean_ms = float(np.mean(solve_ms)) if solve_ms else float("nan")
     achieved = (flops / max(n_launch, 1)) / (mean_ms * 1e-3) / 1e12 if solve_ms else None
     peak, peak_src = _peak()
-    prof = _ncu_profile()
+    prof = _ncu_profile(nd, args.precision)
     traffic = None
     if prof is not None:
         traffic = {"dram_bytes_per_launch": prof.get("dram_bytes"),
@@ -340,8 +343,6 @@ def main():
                    "source": prof.get("source")}
     kname = ("dd3_cell_solve (cell_solve3_kernel)" if nd == 3 else
              "dd_cell_solve (cell_solve_kernel + cluster variant)")
-    if nd == 3:
-        traffic = None   # the committed ncu capture is of the 2D cell kernel
     roofline = {"bound": "fp64", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if achieved else None, "peak_source": peak_src,

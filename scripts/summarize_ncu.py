@@ -2,6 +2,7 @@
 
     python scripts/summarize_ncu.py launches <launches.csv> "<header line>"
     python scripts/summarize_ncu.py full <report.ncu-rep>
+    python scripts/summarize_ncu.py json <report.ncu-rep> "<source note>"   # bench.py's roofline.traffic input
 """
 import csv, io, subprocess, sys
 from collections import defaultdict
@@ -48,8 +49,33 @@ def full(path):
         print(row[hdr.index("Kernel Name")] + "," + ",".join(row[i] for i in idx))
 
 
+def as_json(path, note):
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rd = list(csv.reader(io.StringIO(out)))
+    hdr, units, row = rd[0], rd[1], rd[2]
+
+    def val(name, scale_units):
+        i = hdr.index(name)
+        return float(row[i].replace(",", "")) * scale_units.get(units[i], 1.0)
+
+    byte_u = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    time_u = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
+    dram = val("dram__bytes_read.sum", byte_u) + val("dram__bytes_write.sum", byte_u)
+    ms = val("gpu__time_duration.sum", time_u)
+    print(json.dumps({
+        "kernel": row[hdr.index("Kernel Name")],
+        "dram_bytes": dram, "duration_ms": ms, "dram_gbs": dram / (ms * 1e-3) / 1e9,
+        "fp64_pipe_pct": val("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", {}),
+        "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active", {}),
+        "warps_active_pct": val("sm__warps_active.avg.pct_of_peak_sustained_active", {}),
+        "source": note}, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "json":
+        as_json(sys.argv[2], sys.argv[3])
     else:
         full(sys.argv[2])
